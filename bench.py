@@ -1,0 +1,329 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 PFT hot path (BASELINE.json configs[1]).
+
+Workload (default, `--workload cfg2`): batched 2-D PFT forward + adjoint,
+complex64, a batch of 64 fields of 1024x1024 (seeded standard-normal real and
+imaginary parts), band M = 256 x 256, p = 32, q = 32, r = 10; the adjoint is
+applied to the forward output. One step = forward + adjoint over the 64 fields
+(128 transforms). Per-rank work is fixed (each rank owns its own 64 fields,
+"scaling": "weak"); there is no data-path collective -- the only NCCL call is
+the max-over-ranks of the step time.
+
+  value   device throughput, transforms/s over all ranks, inputs resident in
+          HBM (input 512 MiB per rank > 126 MB L2, so no explicit flush);
+  e2e     the same metric through the C-ABI host-buffer entry points
+          (pftg_apply_2d_host / pftg_adjoint_2d_host) from pinned host memory,
+          copies inside the timed region;
+  roofline  dominant kernel, algorithmic bytes / CUDA-event duration, vs the
+          measured HBM copy bandwidth in MEASURED_PEAKS.json;
+  cpu_baseline  the reference CPU path (oracle/_ref: the unmodified
+          proj/core pft.cpp compiled with the Eigen/FFTW shims) on a bounded
+          sample, rank 0 at N = 1.
+
+`--impl reference` times the reference CPU implementation with all host
+threads on the same workload (bounded sample per step).
+Other workloads: `--workload cfg1` (single 512^2 complex128 transform, r=12).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+DATA = ROOT / "paper_2408_03532_b200" / "data"
+
+METRIC = "pft_transforms_per_sec"
+
+WORKLOADS = {
+    # name: (table, n, mt, p, dtype, batch, description)
+    "cfg2": ("scope_table_xi4_r10.txt", 1024, 128, 32, "c64", 64,
+             "batched 2-D PFT fwd+adj, complex64, 64 x 1024^2, M=256, p=32, q=32, r=10"),
+    "cfg1": ("scope_table_xi4_r12.txt", 512, 64, 16, "c128", 1,
+             "single 2-D PFT fwd+adj, complex128, 512^2, M=128, p=16, q=32, r=12"),
+}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return float(j["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_reference(workload, fields, threads, repeats=1):
+    """Time the reference CPU implementation (oracle/_ref) on `fields` fields."""
+    from oracle import ref
+    table, n, mt, p, dt, _, _ = WORKLOADS[workload]
+    rp = ref.RefPlan.create(DATA / table, n, n, mt, mt, p, p, 1.0)
+    rng = np.random.default_rng(1234)
+    cdt = np.complex64 if dt == "c64" else np.complex128
+    z = (rng.standard_normal((fields, n, n)) + 1j * rng.standard_normal((fields, n, n)))
+    z = z.astype(cdt).astype(np.complex128)
+    rp.fwd_adj_batch(z[:1], threads=1)  # warm caches / plan
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        rp.fwd_adj_batch(z, threads=threads, want=False)
+        times.append(time.perf_counter() - t0)
+    return times, 2 * fields
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    table, n, mt, p, dt, batch, desc = WORKLOADS[args.workload]
+    fields = max(threads, 8) if args.workload == "cfg2" else 4
+    # warm-up steps, then K timed steps (each step = `fields` fields fwd+adj)
+    for _ in range(args.warmup):
+        cpu_reference(args.workload, min(fields, threads), threads)
+    times, transforms = [], 0
+    for _ in range(args.steps):
+        t, tr = cpu_reference(args.workload, fields, threads)
+        times += t
+        transforms = tr
+    total = sum(times)
+    value = transforms * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "transforms/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded standard-normal fields)",
+        "config": {"workload": args.workload, "description": desc, "sample_fields_per_step": fields},
+        "cpu_baseline": {"value": value, "unit": "transforms/s", "cores": threads, "kind": "reference",
+                         "sample": f"{fields} fields fwd+adj per step ({transforms} transforms), "
+                                   f"unmodified proj/core pft.cpp + Eigen/FFTW shims, "
+                                   f"{threads} threads (one field per thread)"},
+        "e2e": {"value": value, "unit": "transforms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2408_03532_b200 as P
+    from paper_2408_03532_b200._lib import KernelProfile
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    table, n, mt, p, dt, batch, desc = WORKLOADS[args.workload]
+    cdt = torch.complex64 if dt == "c64" else torch.complex128
+    plan = P.pft_plan_2d(n, n, mt, mt, p, p, 1.0, P.ScopeTable.load(DATA / table))
+    M = 2 * mt
+    esize = 8 if dt == "c64" else 16
+    g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    z = torch.complex(torch.randn((batch, n, n), device="cuda", generator=g),
+                      torch.randn((batch, n, n), device="cuda", generator=g)).to(cdt)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        band = P.pft_apply_2d(plan, z)
+        return P.pft_adjoint_2d(plan, band)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk, KernelProfile() as prof:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    transforms_per_step = 2 * batch
+    value = world * transforms_per_step * args.steps / (ms / 1e3)
+    alg_bytes_step = transforms_per_step * (n * n + M * M) * esize
+
+    # dominant kernel roofline (per-launch algorithmic bytes / event time)
+    hbm, peak_kind = peaks()
+    kname = max(prof.ms, key=lambda k: prof.ms[k])
+    launches = prof.count[kname]
+    # rows passes touch each field once: fwd reads n^2, adj writes n^2 (per field)
+    fields_per_launch = batch * args.steps / max(launches, 1)
+    kbytes = {"pft_rows_fwd": n * n * esize, "pft_rows_adj": n * n * esize,
+              "pft_cols_fwd": M * M * esize, "pft_cols_adj": M * M * esize}.get(kname, 0)
+    k_avg_ms = prof.ms[kname] / max(launches, 1)
+    achieved = kbytes * fields_per_launch / (k_avg_ms / 1e3) / 1e9
+    gpu_launches = sum(prof.launches.values())
+
+    # e2e through the host-buffer C-ABI (pinned host memory, copies timed)
+    zh = z.cpu().pin_memory().numpy()
+    bh = np.empty((batch, M, M), zh.dtype)
+    band_pinned = torch.from_numpy(bh).pin_memory()
+    bh = band_pinned.numpy()
+    zback = torch.empty((batch, n, n), dtype=cdt).pin_memory().numpy()
+    from paper_2408_03532_b200._lib import lib, check
+    import ctypes as C
+    code = 0 if dt == "c64" else 1
+
+    def e2e_step():
+        check(lib().pftg_apply_2d_host(plan._h, code, zh.ctypes.data, bh.ctypes.data, batch))
+        check(lib().pftg_adjoint_2d_host(plan._h, code, bh.ctypes.data, zback.ctypes.data, batch))
+
+    e2e_step()
+    barrier()
+    e2e_steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    t_e2e = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    e2e_value = world * transforms_per_step * e2e_steps / t_e2e
+    h2d = batch * (n * n + M * M) * esize
+    d2h = batch * (M * M + n * n) * esize
+
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            fields = 16 if dt == "c64" else 4
+            times, tr = cpu_reference(args.workload, fields, threads)
+            cpu_base = {"value": tr / sum(times), "unit": "transforms/s", "cores": threads,
+                        "kind": "reference",
+                        "sample": f"{fields} fields fwd+adj ({tr} transforms) on {threads} host threads, "
+                                  "unmodified proj/core pft.cpp + Eigen/FFTW shims (oracle/_ref)"}
+        except Exception as exc:  # report, never fall back
+            cpu_base = {"value": None, "unit": "transforms/s", "cores": 0, "kind": "reference",
+                        "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "transforms/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if dt == "c64" else "f64",
+            "data": "synthetic (seeded standard-normal fields)",
+            "config": {"workload": args.workload, "description": desc, "fields_per_rank": batch,
+                       "band": [M, M], "l2": "inputs larger than L2 (no flush)",
+                       "gb_per_s_algorithmic": alg_bytes_step * args.steps / (ms / 1e3) / 1e9 * world,
+                       "parallelism": f"weak-scaled replicas x{world}, no data-path collective"},
+            "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm,
+                         "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                         "peak_kind": peak_kind, "kernel_avg_ms": k_avg_ms,
+                         "kernel_ms": prof.ms, "kernel_launches": prof.count},
+            "e2e": {"value": e2e_value, "unit": "transforms/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": gpu_launches,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu_base,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="cfg2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,136 @@
+"""ctypes binding of libpftg.so (include/pftg.h).
+
+The library is built in-tree (``make -C paper_2408_03532_b200/csrc``, or
+``__graft_entry__.build()``). There is no fallback: if the shared object is
+missing or no sm_100 GPU is present, every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+LIB_PATH = HERE / "libpftg.so"
+
+PFTG_OK, PFTG_EINVAL, PFTG_ELOGIC, PFTG_ERANGE, PFTG_ERUNTIME, PFTG_ECUDA = range(6)
+PFTG_C64, PFTG_C128 = 0, 1
+
+# Every symbol include/pftg.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "pftg_version", "pftg_last_error", "pftg_device_ok", "pftg_profile_begin", "pftg_profile_end",
+    "pftg_table_load", "pftg_table_free", "pftg_table_min_degree",
+    "pftg_plan_2d", "pftg_plan_load", "pftg_plan_save", "pftg_plan_free", "pftg_plan_info",
+    "pftg_plan_tables",
+    "pftg_apply_2d_dev", "pftg_adjoint_2d_dev", "pftg_apply_2d_host", "pftg_adjoint_2d_host",
+    "pftg_band_residual_dev",
+    "pftg_fft2_dev", "pftg_project_modulus_dev", "pftg_crop_centered_dev",
+    "pftg_window_slice_dev", "pftg_set_window_dev", "pftg_pie_object_update_dev",
+    "pftg_epie_probe_update_dev", "pftg_evaluate_dev",
+    "pftg_solver_create", "pftg_solver_run", "pftg_solver_trace", "pftg_solver_result",
+    "pftg_solver_device_state", "pftg_solver_free",
+)
+
+
+class CudaError(RuntimeError):
+    """A CUDA failure inside libpftg (no device, launch error, fault)."""
+
+
+class SolverConfigC(C.Structure):
+    _fields_ = [
+        ("pft_sweeps", C.c_int), ("fft_sweeps", C.c_int),
+        ("beta", C.c_double), ("gamma", C.c_double), ("beta_pft", C.c_double),
+        ("gamma_pft", C.c_double), ("eps_pft", C.c_double), ("tol", C.c_double),
+        ("mt1", C.c_int64), ("mt2", C.c_int64), ("p1", C.c_int64), ("p2", C.c_int64),
+        ("blind", C.c_int), ("shuffled", C.c_int), ("seed", C.c_uint64),
+        ("objective_every", C.c_int),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"libpftg.so not built ({LIB_PATH}); run `make -C paper_2408_03532_b200/csrc` "
+            "or __graft_entry__.build(). There is no CPU fallback.")
+    L = C.CDLL(str(LIB_PATH))
+    vp, sz, dp, i64p = C.c_void_p, C.c_size_t, C.POINTER(C.c_double), C.POINTER(C.c_int64)
+    L.pftg_last_error.restype = C.c_char_p
+    L.pftg_profile_end.argtypes = [dp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.pftg_table_load.argtypes = [C.c_char_p, C.POINTER(vp)]
+    L.pftg_table_free.argtypes = [vp]
+    L.pftg_table_free.restype = None
+    L.pftg_table_min_degree.argtypes = [vp, C.c_double, C.c_double, C.POINTER(C.c_int)]
+    L.pftg_plan_2d.argtypes = [vp, sz, sz, sz, sz, sz, sz, C.c_double, C.POINTER(vp)]
+    L.pftg_plan_load.argtypes = [C.c_char_p, C.POINTER(vp)]
+    L.pftg_plan_save.argtypes = [vp, C.c_char_p]
+    L.pftg_plan_free.argtypes = [vp]
+    L.pftg_plan_free.restype = None
+    L.pftg_plan_info.argtypes = [vp, i64p]
+    L.pftg_plan_tables.argtypes = [vp, C.c_int, dp, dp]
+    L.pftg_apply_2d_dev.argtypes = [vp, C.c_int, vp, vp, sz, vp]
+    L.pftg_adjoint_2d_dev.argtypes = [vp, C.c_int, vp, vp, sz, vp]
+    L.pftg_apply_2d_host.argtypes = [vp, C.c_int, vp, vp, sz]
+    L.pftg_adjoint_2d_host.argtypes = [vp, C.c_int, vp, vp, sz]
+    L.pftg_band_residual_dev.argtypes = [vp, C.c_int, vp, vp, vp, sz, vp]
+    L.pftg_fft2_dev.argtypes = [C.c_int, vp, vp, sz, sz, sz, C.c_int, vp]
+    L.pftg_project_modulus_dev.argtypes = [C.c_int, vp, vp, vp, sz, sz, sz, vp]
+    L.pftg_crop_centered_dev.argtypes = [C.c_int, vp, vp, sz, sz, sz, sz, sz, vp]
+    L.pftg_window_slice_dev.argtypes = [C.c_int, vp, sz, sz, vp, sz, sz, i64p, sz, vp]
+    L.pftg_set_window_dev.argtypes = [C.c_int, vp, sz, sz, vp, sz, sz, C.c_int64, C.c_int64, vp]
+    L.pftg_pie_object_update_dev.argtypes = [C.c_int, vp, vp, vp, sz, C.c_double, vp]
+    L.pftg_epie_probe_update_dev.argtypes = [C.c_int, vp, vp, vp, sz, C.c_double, C.c_int, vp]
+    L.pftg_evaluate_dev.argtypes = [C.c_int, vp, sz, sz, vp, sz, sz, i64p, sz, sz, sz, vp, vp, vp,
+                                    dp, dp, vp]
+    L.pftg_solver_create.argtypes = [C.c_int, vp, sz, sz, vp, sz, sz, i64p, sz, vp,
+                                     C.POINTER(SolverConfigC), vp, C.POINTER(vp)]
+    L.pftg_solver_run.argtypes = [vp, C.c_int]
+    L.pftg_solver_trace.argtypes = [vp, dp, dp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.pftg_solver_result.argtypes = [vp, vp, vp]
+    L.pftg_solver_device_state.argtypes = [vp, C.POINTER(vp), C.POINTER(vp)]
+    L.pftg_solver_free.argtypes = [vp]
+    L.pftg_solver_free.restype = None
+    _lib = L
+    return L
+
+
+KERNEL_NAMES = ("pft_rows_fwd", "pft_cols_fwd", "pft_cols_adj", "pft_rows_adj", "fft_rows",
+                "fft_cols")
+
+
+class KernelProfile:
+    """Context manager over pftg_profile_begin/end: per-kernel CUDA-event time."""
+
+    def __enter__(self):
+        check(lib().pftg_profile_begin())
+        return self
+
+    def __exit__(self, *exc):
+        ms = (C.c_double * 6)()
+        cnt = (C.c_int * 6)()
+        launches = (C.c_int * 6)()
+        check(lib().pftg_profile_end(ms, cnt, launches))
+        self.ms = {KERNEL_NAMES[k]: ms[k] for k in range(6)}
+        self.count = {KERNEL_NAMES[k]: cnt[k] for k in range(6)}
+        self.launches = {KERNEL_NAMES[k]: launches[k] for k in range(6)}
+        return False
+
+
+def check(rc: int) -> None:
+    """Map a pftg status onto the Python analogue of the reference's exception."""
+    if rc == PFTG_OK:
+        return
+    msg = lib().pftg_last_error().decode(errors="replace")
+    if rc == PFTG_EINVAL:
+        raise ValueError(msg)          # std::invalid_argument
+    if rc == PFTG_ERANGE:
+        raise IndexError(msg)          # std::out_of_range
+    if rc == PFTG_ELOGIC:
+        raise RuntimeError(msg)        # std::logic_error
+    if rc == PFTG_ECUDA:
+        raise CudaError(msg)
+    raise OSError(msg)                 # std::runtime_error (I/O, format)

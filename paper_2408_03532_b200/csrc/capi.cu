@@ -1,0 +1,900 @@
+// C-ABI implementation (include/pftg.h): plans, PFT operators, full FFTs,
+// modulus projection, scan geometry, updates and the evaluator.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pftg.h"
+#include "internal.hpp"
+
+namespace pftg {
+
+namespace {
+thread_local std::string g_err;
+}
+
+void set_error(const std::string& m) { g_err = m; }
+
+void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  std::snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d in %s", cudaGetErrorName(e),
+                cudaGetErrorString(e), file, line, what);
+  throw cuda_error(buf);
+}
+
+void ensure_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw cuda_error("pftg: no CUDA device available (this library has no CPU fallback)");
+  }
+  int dev = 0;
+  PFTG_CUDA(cudaGetDevice(&dev));
+  int major = 0;
+  PFTG_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major != 10) throw cuda_error("pftg: built for sm_100a (B200); device has compute capability major " +
+                                    std::to_string(major));
+}
+
+void check_fft_len(std::size_t n) {
+  if (n < 2 || n > 1024 || (n & (n - 1)) != 0)
+    throw std::invalid_argument("pftg: GPU fft2 supports power-of-two sizes in [2, 1024], got " +
+                                std::to_string(n));
+}
+
+// ---- per-kernel timing hook ----
+namespace {
+struct ProfState {
+  std::mutex mu;
+  bool on = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+  int launches[K_NUM] = {};
+};
+ProfState& prof() {
+  static ProfState p;
+  return p;
+}
+cudaEvent_t new_event() {
+  cudaEvent_t e;
+  PFTG_CUDA(cudaEventCreate(&e));
+  return e;
+}
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+}  // namespace
+
+ProfScope::ProfScope(cudaStream_t s, int k) : kid(k), st(s) {
+  ProfState& p = prof();
+  {
+    std::lock_guard<std::mutex> lock(p.mu);
+    ++p.launches[k];
+    if (!p.on) return;
+  }
+  if (capturing(st)) return;
+  e0 = new_event();
+  PFTG_CUDA(cudaEventRecord(e0, st));
+}
+
+ProfScope::~ProfScope() {
+  if (!e0) return;
+  cudaEvent_t e1;
+  if (cudaEventCreate(&e1) != cudaSuccess) return;
+  cudaEventRecord(e1, st);
+  ProfState& p = prof();
+  std::lock_guard<std::mutex> lock(p.mu);
+  p.ev.push_back({kid, {e0, e1}});
+}
+
+Scratch::Scratch(std::size_t bytes, cudaStream_t s) : st(s) {
+  if (bytes == 0) bytes = 16;
+  PFTG_CUDA(cudaMallocAsync(&p, bytes, s));
+}
+Scratch::~Scratch() {
+  if (p) cudaFreeAsync(p, st);
+}
+
+namespace {
+
+template <class T>
+T* dev_upload(const std::vector<T>& h) {
+  T* d = nullptr;
+  PFTG_CUDA(cudaMalloc(&d, sizeof(T) * std::max<std::size_t>(h.size(), 1)));
+  if (!h.empty()) PFTG_CUDA(cudaMemcpy(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+  return d;
+}
+
+int ilog2_exact(std::size_t n) {
+  int l = 0;
+  while ((std::size_t(1) << l) < n) ++l;
+  return l;
+}
+
+// Nonzero part of B[l][j] (pure real for even j, pure imaginary for odd j,
+// minimax.cpp:326-330). Plans loaded from files must keep that structure.
+template <class R>
+std::vector<R> b_values(const Axis& a) {
+  std::vector<R> v(a.q * a.r);
+  for (std::size_t l = 0; l < a.q; ++l)
+    for (int j = 0; j < a.r; ++j) {
+      const cd b = a.B[l * a.r + j];
+      const double zero_part = (j % 2 == 0) ? b.imag() : b.real();
+      if (zero_part != 0.0)
+        throw std::invalid_argument(
+            "pftg: plan B must be real for even j and imaginary for odd j (minimax.cpp:326-330)");
+      v[l * a.r + j] = static_cast<R>((j % 2 == 0) ? b.real() : b.imag());
+    }
+  return v;
+}
+
+template <class R>
+std::vector<typename CT<R>::C> w_transposed(const Axis& a) {
+  const std::size_t M = 2 * a.mt;
+  std::vector<typename CT<R>::C> v(static_cast<std::size_t>(a.r) * M);
+  for (int j = 0; j < a.r; ++j)
+    for (std::size_t i = 0; i < M; ++i) {
+      const cd w = a.W[i * a.r + j];
+      v[j * M + i] = CT<R>::mk(static_cast<R>(w.real()), static_cast<R>(w.imag()));
+    }
+  return v;
+}
+
+template <class R>
+std::vector<typename CT<R>::C> twiddles_host(std::size_t p) {
+  std::vector<typename CT<R>::C> v(std::max<std::size_t>(p / 2, 1));
+  for (std::size_t k = 0; k < p / 2; ++k) {
+    const double a = -2.0 * M_PI * static_cast<double>(k) / static_cast<double>(p);
+    v[k] = CT<R>::mk(static_cast<R>(std::cos(a)), static_cast<R>(std::sin(a)));
+  }
+  return v;
+}
+
+void check_gpu_axis(const Axis& a, const char* which) {
+  const bool pow2 = a.p >= 2 && (a.p & (a.p - 1)) == 0;
+  if (!pow2 || a.p > 128)
+    throw std::invalid_argument(std::string("pftg: GPU PFT needs power-of-two p in [2, 128] (axis ") + which +
+                                ", p=" + std::to_string(a.p) + ")");
+  if (a.r < 1 || a.r > 16)
+    throw std::invalid_argument(std::string("pftg: GPU PFT supports 1 <= r <= 16 (axis ") + which + ")");
+  if (a.n > (1u << 20)) throw std::invalid_argument("pftg: axis too long");
+}
+
+template <class R>
+void upload(const pftg_plan& p, DevTables<R>& t, PftDev<R>& pd) {
+  check_gpu_axis(p.a1, "1");
+  check_gpu_axis(p.a2, "2");
+  t.Bv1 = dev_upload(b_values<R>(p.a1));
+  t.Bv2 = dev_upload(b_values<R>(p.a2));
+  t.W1t = dev_upload(w_transposed<R>(p.a1));
+  t.W2t = dev_upload(w_transposed<R>(p.a2));
+  t.tw1 = dev_upload(twiddles_host<R>(p.a1.p));
+  t.tw2 = dev_upload(twiddles_host<R>(p.a2.p));
+  pd.n1 = static_cast<int>(p.a1.n);
+  pd.n2 = static_cast<int>(p.a2.n);
+  pd.p1 = static_cast<int>(p.a1.p);
+  pd.p2 = static_cast<int>(p.a2.p);
+  pd.q1 = static_cast<int>(p.a1.q);
+  pd.q2 = static_cast<int>(p.a2.q);
+  pd.mt1 = static_cast<int>(p.a1.mt);
+  pd.mt2 = static_cast<int>(p.a2.mt);
+  pd.r1 = p.a1.r;
+  pd.r2 = p.a2.r;
+  pd.M1 = 2 * pd.mt1;
+  pd.M2 = 2 * pd.mt2;
+  pd.lp1 = ilog2_exact(p.a1.p);
+  pd.lp2 = ilog2_exact(p.a2.p);
+  pd.Bv1 = t.Bv1;
+  pd.Bv2 = t.Bv2;
+  pd.W1t = t.W1t;
+  pd.W2t = t.W2t;
+  pd.tw1 = t.tw1;
+  pd.tw2 = t.tw2;
+}
+
+template <class R>
+void free_tables(DevTables<R>& t) {
+  cudaFree(t.Bv1);
+  cudaFree(t.Bv2);
+  cudaFree(t.W1t);
+  cudaFree(t.W2t);
+  cudaFree(t.tw1);
+  cudaFree(t.tw2);
+  t = DevTables<R>{};
+}
+
+}  // namespace
+
+template <>
+const PftDev<float>& plan_dev<float>(const pftg_plan& p) {
+  ensure_device();
+  int dev = 0;
+  PFTG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(p.mu);
+  if (p.dev32 != dev) {
+    if (p.dev32 >= 0) free_tables(p.t32);
+    upload(p, p.t32, p.pd32);
+    p.dev32 = dev;
+  }
+  return p.pd32;
+}
+
+template <>
+const PftDev<double>& plan_dev<double>(const pftg_plan& p) {
+  ensure_device();
+  int dev = 0;
+  PFTG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(p.mu);
+  if (p.dev64 != dev) {
+    if (p.dev64 >= 0) free_tables(p.t64);
+    upload(p, p.t64, p.pd64);
+    p.dev64 = dev;
+  }
+  return p.pd64;
+}
+
+// ---------------------------------------------------------------- operators
+namespace {
+
+template <class R>
+using Cx = typename CT<R>::C;
+
+// Fields per chunk so the chunk's G workspace (~p1*r1*M2 complex per field)
+// stays well inside L2 between the rows and cols passes.
+template <class R>
+std::size_t chunk_fields(const PftDev<R>& pd) {
+  const std::size_t g = sizeof(Cx<R>) * (std::size_t)pd.p1 * pd.r1 * pd.M2;
+  std::size_t c = (24u << 20) / std::max<std::size_t>(g, 1);
+  return std::max<std::size_t>(1, std::min<std::size_t>(c, 65535));
+}
+
+template <class R>
+void apply_dev(const pftg_plan* plan, const void* z, void* band, std::size_t batch, cudaStream_t st) {
+  const PftDev<R>& pd = plan_dev<R>(*plan);
+  const std::size_t chunk = std::min(batch, chunk_fields(pd));
+  const std::size_t gsz = (std::size_t)pd.p1 * pd.r1 * pd.M2;
+  Scratch G(sizeof(Cx<R>) * gsz * chunk, st);
+  const std::size_t nz = (std::size_t)pd.n1 * pd.n2, nb = (std::size_t)pd.M1 * pd.M2;
+  for (std::size_t b0 = 0; b0 < batch; b0 += chunk) {
+    const int nbat = static_cast<int>(std::min(chunk, batch - b0));
+    Src<R> src{static_cast<const Cx<R>*>(z) + b0 * nz, pd.n2, (long long)nz, nullptr, nullptr};
+    launch_fwd_rows<R>(pd, src, G.as<Cx<R>>(), nbat, st);
+    launch_fwd_cols<R>(pd, 0, G.as<Cx<R>>(), static_cast<Cx<R>*>(band) + b0 * nb, nullptr, 0, nullptr, nullptr,
+                       nbat, st);
+  }
+}
+
+template <class R>
+void adjoint_dev(const pftg_plan* plan, const void* band, void* z, std::size_t batch, cudaStream_t st) {
+  const PftDev<R>& pd = plan_dev<R>(*plan);
+  const std::size_t chunk = std::min(batch, chunk_fields(pd));
+  const std::size_t gsz = (std::size_t)pd.p1 * pd.r1 * pd.M2;
+  Scratch G(sizeof(Cx<R>) * gsz * chunk, st);
+  const std::size_t nz = (std::size_t)pd.n1 * pd.n2, nb = (std::size_t)pd.M1 * pd.M2;
+  for (std::size_t b0 = 0; b0 < batch; b0 += chunk) {
+    const int nbat = static_cast<int>(std::min(chunk, batch - b0));
+    launch_adj_cols<R>(pd, static_cast<const Cx<R>*>(band) + b0 * nb, G.as<Cx<R>>(), nbat, st);
+    EpiArgs ep{};
+    ep.out = static_cast<Cx<R>*>(z) + b0 * nz;
+    launch_adj_rows<R>(pd, 0, G.as<Cx<R>>(), ep, nbat, st);
+  }
+}
+
+template <class R>
+void band_residual_dev(const pftg_plan* plan, const void* exit_wave, const void* dcrop, void* out,
+                       std::size_t batch, cudaStream_t st) {
+  const PftDev<R>& pd = plan_dev<R>(*plan);
+  const std::size_t chunk = std::min(batch, chunk_fields(pd));
+  const std::size_t gsz = (std::size_t)pd.p1 * pd.r1 * pd.M2;
+  Scratch G(sizeof(Cx<R>) * gsz * chunk, st), Gt(sizeof(Cx<R>) * gsz * chunk, st);
+  const std::size_t nz = (std::size_t)pd.n1 * pd.n2, nb = (std::size_t)pd.M1 * pd.M2;
+  for (std::size_t b0 = 0; b0 < batch; b0 += chunk) {
+    const int nbat = static_cast<int>(std::min(chunk, batch - b0));
+    Src<R> src{static_cast<const Cx<R>*>(exit_wave) + b0 * nz, pd.n2, (long long)nz, nullptr, nullptr};
+    launch_fwd_rows<R>(pd, src, G.as<Cx<R>>(), nbat, st);
+    launch_fwd_cols<R>(pd, 1, G.as<Cx<R>>(), nullptr, static_cast<const R*>(dcrop) + b0 * nb, (long long)nb,
+                       Gt.as<Cx<R>>(), nullptr, nbat, st);
+    EpiArgs ep{};
+    ep.out = static_cast<Cx<R>*>(out) + b0 * nz;
+    launch_adj_rows<R>(pd, 0, Gt.as<Cx<R>>(), ep, nbat, st);
+  }
+}
+
+// Host-buffer variants: chunks of the batch ping-pong between two streams so
+// H2D of chunk i+1, compute of chunk i and D2H of chunk i-1 overlap.
+template <class R, class Op>
+void host_pipeline(std::size_t batch, std::size_t in_elems, std::size_t out_elems, const void* in, void* out,
+                   std::size_t chunk, Op&& op) {
+  using C = Cx<R>;
+  cudaStream_t s[2];
+  PFTG_CUDA(cudaStreamCreateWithFlags(&s[0], cudaStreamNonBlocking));
+  PFTG_CUDA(cudaStreamCreateWithFlags(&s[1], cudaStreamNonBlocking));
+  C* din[2] = {nullptr, nullptr};
+  C* dout[2] = {nullptr, nullptr};
+  auto cleanup = [&] {
+    for (int k = 0; k < 2; ++k) {
+      if (din[k]) cudaFree(din[k]);
+      if (dout[k]) cudaFree(dout[k]);
+      cudaStreamDestroy(s[k]);
+    }
+  };
+  try {
+    for (int k = 0; k < 2; ++k) {
+      PFTG_CUDA(cudaMalloc(&din[k], sizeof(C) * in_elems * chunk));
+      PFTG_CUDA(cudaMalloc(&dout[k], sizeof(C) * out_elems * chunk));
+    }
+    int k = 0;
+    for (std::size_t b0 = 0; b0 < batch; b0 += chunk, k ^= 1) {
+      const std::size_t nb = std::min(chunk, batch - b0);
+      PFTG_CUDA(cudaMemcpyAsync(din[k], static_cast<const C*>(in) + b0 * in_elems, sizeof(C) * in_elems * nb,
+                                cudaMemcpyHostToDevice, s[k]));
+      op(din[k], dout[k], nb, s[k]);
+      PFTG_CUDA(cudaMemcpyAsync(static_cast<C*>(out) + b0 * out_elems, dout[k], sizeof(C) * out_elems * nb,
+                                cudaMemcpyDeviceToHost, s[k]));
+    }
+    PFTG_CUDA(cudaStreamSynchronize(s[0]));
+    PFTG_CUDA(cudaStreamSynchronize(s[1]));
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+
+std::size_t host_chunk(std::size_t batch, std::size_t bytes_per_field) {
+  // ~32 MiB per copy: large enough to run PCIe at full rate, small enough to overlap.
+  std::size_t c = (32u << 20) / std::max<std::size_t>(bytes_per_field, 1);
+  c = std::max<std::size_t>(1, c);
+  return std::min(c, std::max<std::size_t>(1, (batch + 1) / 2));
+}
+
+// ---- full transforms ----
+template <class R>
+void fft2_dev(const void* z, void* out, std::size_t rows, std::size_t cols, std::size_t batch, int inverse,
+              cudaStream_t st) {
+  check_fft_len(rows);
+  check_fft_len(cols);
+  const int n1 = (int)rows, n2 = (int)cols;
+  const long long n = (long long)n1 * n2;
+  const int sign = inverse ? +1 : -1;
+  const double scale = inverse ? 1.0 / static_cast<double>(n) : 1.0;
+  RowSrc<R> src{static_cast<const Cx<R>*>(z), n2, n, nullptr, nullptr};
+  RowEpiArgs ep{};
+  launch_fft_rows<R>(ROW_DIT_NATURAL, EPI_STORE, n1, n2, src, static_cast<Cx<R>*>(out), n, sign, scale, ep,
+                     (int)batch, st);
+  launch_fft_cols<R>(COL_NATURAL, n1, n2, static_cast<Cx<R>*>(out), n, nullptr, 0, nullptr, 0, sign, nullptr,
+                     (int)batch, st);
+}
+
+template <class R>
+void project_modulus_dev(const void* exit_wave, const void* d, void* out, std::size_t rows, std::size_t cols,
+                         std::size_t batch, cudaStream_t st) {
+  check_fft_len(rows);
+  check_fft_len(cols);
+  const int n1 = (int)rows, n2 = (int)cols;
+  const long long n = (long long)n1 * n2;
+  Scratch X(sizeof(Cx<R>) * n * batch, st);
+  RowSrc<R> src{static_cast<const Cx<R>*>(exit_wave), n2, n, nullptr, nullptr};
+  RowEpiArgs ep{};
+  launch_fft_rows<R>(ROW_DIF_STORE, EPI_STORE, n1, n2, src, X.as<Cx<R>>(), n, -1, 1.0, ep, (int)batch, st);
+  launch_fft_cols<R>(COL_PROJECT, n1, n2, X.as<Cx<R>>(), n, static_cast<const R*>(d), n, nullptr, 1, -1, nullptr,
+                     (int)batch, st);
+  ep.out = out;
+  ep.out_bstride = n;
+  launch_fft_rows<R>(ROW_DIT_PROJ, EPI_STORE, n1, n2, src, X.as<Cx<R>>(), n, +1, 1.0 / static_cast<double>(n),
+                     ep, (int)batch, st);
+}
+
+// ---- elementwise kernels ----
+template <class C>
+__global__ void k_window_slice(const C* __restrict__ frame, long long fc, C* __restrict__ out, int wr, int wc,
+                               const long long* __restrict__ offs, int npos) {
+  const long long per = (long long)wr * wc;
+  const long long tot = per * npos;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long j = i / per;
+    const int rem = (int)(i % per);
+    const int r = rem / wc, c = rem % wc;
+    out[i] = frame[offs[j] + (long long)r * fc + c];
+  }
+}
+
+template <class C>
+__global__ void k_set_window(C* __restrict__ frame, long long fc, const C* __restrict__ patch, int wr, int wc,
+                             long long off) {
+  const long long tot = (long long)wr * wc;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / wc), c = (int)(i % wc);
+    frame[off + (long long)r * fc + c] = patch[i];
+  }
+}
+
+// mode 0: zj -= s conj(P) (P zj - proj); mode 1: P -= s conj(zj) (P zj - proj)
+template <class C>
+__global__ void k_update(C* __restrict__ a, const C* __restrict__ b, const C* __restrict__ proj, long long n,
+                         double s, int mode) {
+  using R = typename RT<C>::R;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const C zj = mode == 0 ? a[i] : b[i];
+    const C pr = mode == 0 ? b[i] : a[i];
+    const C resid = csub(cmul(pr, zj), proj[i]);
+    const C g = mode == 0 ? cmulc(pr, resid) : cmulc(zj, resid);
+    C v = a[i];
+    v.x -= (R)s * g.x;
+    v.y -= (R)s * g.y;
+    a[i] = v;
+  }
+}
+
+template <class R>
+__global__ void k_crop(const R* __restrict__ spec, R* __restrict__ out, int rows, int cols, int mt1, int mt2,
+                       long long batch) {
+  const long long M = 4LL * mt1 * mt2;
+  const long long tot = M * batch;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long f = i / M;
+    const int rem = (int)(i % M);
+    const int a = rem / (2 * mt2), b = rem % (2 * mt2);
+    const int r = mod_nonneg(a - mt1, rows), c = mod_nonneg(b - mt2, cols);
+    out[i] = spec[f * rows * cols + (long long)r * cols + c];
+  }
+}
+
+int grid_for(long long n) {
+  long long g = (n + 255) / 256;
+  return (int)std::max<long long>(1, std::min<long long>(g, 148LL * 32));
+}
+
+// ---- evaluator ----
+template <class R>
+void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void* probe, std::size_t wr,
+                  std::size_t wc, const int64_t* offsets, std::size_t npos, std::size_t pb, std::size_t pe,
+                  const void* d, const pftg_plan* plan, const void* dcrop, double* fft_sum, double* band_sum,
+                  cudaStream_t st) {
+  check_fft_len(wr);
+  check_fft_len(wc);
+  if (pb > pe || pe > npos) throw std::out_of_range("scan: position index out of range");
+  const int n1 = (int)wr, n2 = (int)wc;
+  const long long n = (long long)n1 * n2;
+  const std::size_t count = pe - pb;
+  std::vector<long long> offs(count);
+  for (std::size_t j = 0; j < count; ++j) offs[j] = offsets[2 * (pb + j)] * (long long)fc + offsets[2 * (pb + j) + 1];
+  const PftDev<R>* pd = plan ? &plan_dev<R>(*plan) : nullptr;
+  if (pd && (pd->n1 != n1 || pd->n2 != n2))
+    throw std::invalid_argument("band_residual: plan does not match the window shape");
+  const std::size_t chunk = std::max<std::size_t>(1, std::min<std::size_t>(count, (64u << 20) / (sizeof(Cx<R>) * n)));
+  Scratch doffs(sizeof(long long) * std::max<std::size_t>(count, 1), st);
+  if (count) PFTG_CUDA(cudaMemcpyAsync(doffs.p, offs.data(), sizeof(long long) * count, cudaMemcpyHostToDevice, st));
+  Scratch X(sizeof(Cx<R>) * n * chunk, st);
+  const int nstrips = fft_cols_strips<R>(n2);
+  Scratch part(sizeof(double) * nstrips * std::max<std::size_t>(count, 1), st);
+  std::unique_ptr<Scratch> G, bpart;
+  int bstrips = 0;
+  if (pd) {
+    G.reset(new Scratch(sizeof(Cx<R>) * (std::size_t)pd->p1 * pd->r1 * pd->M2 * chunk, st));
+    bstrips = cols_strips<R>(*pd);
+    bpart.reset(new Scratch(sizeof(double) * bstrips * std::max<std::size_t>(count, 1), st));
+  }
+  for (std::size_t c0 = 0; c0 < count; c0 += chunk) {
+    const int nb = (int)std::min(chunk, count - c0);
+    const long long* o = doffs.as<long long>() + c0;
+    // full-FFT objective: rows (natural input, bitrev-gather + DIT) ...
+    RowSrc<R> src{static_cast<const Cx<R>*>(frame), (long long)fc, 0, o, static_cast<const Cx<R>*>(probe)};
+    RowEpiArgs ep{};
+    launch_fft_rows<R>(ROW_DIF_STORE, EPI_STORE, n1, n2, src, X.as<Cx<R>>(), n, -1, 1.0, ep, nb, st);
+    launch_fft_cols<R>(COL_EVAL, n1, n2, X.as<Cx<R>>(), n, static_cast<const R*>(d) + (pb + c0) * n, n, nullptr, 1,
+                       -1, part.as<double>() + c0 * nstrips, nb, st);
+    if (pd) {
+      Src<R> s2{static_cast<const Cx<R>*>(frame), (long long)fc, 0, o, static_cast<const Cx<R>*>(probe)};
+      launch_fwd_rows<R>(*pd, s2, G->as<Cx<R>>(), nb, st);
+      const long long mb = (long long)pd->M1 * pd->M2;
+      launch_fwd_cols<R>(*pd, 2, G->as<Cx<R>>(), nullptr, static_cast<const R*>(dcrop) + (pb + c0) * mb, mb,
+                         nullptr, bpart->as<double>() + c0 * bstrips, nb, st);
+    }
+  }
+  std::vector<double> h(nstrips * count), hb(bstrips * count);
+  if (count) PFTG_CUDA(cudaMemcpyAsync(h.data(), part.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+  if (pd && count)
+    PFTG_CUDA(cudaMemcpyAsync(hb.data(), bpart->p, sizeof(double) * hb.size(), cudaMemcpyDeviceToHost, st));
+  PFTG_CUDA(cudaStreamSynchronize(st));
+  // (1/n) sum_k (|X_k| - d_k)^2 = ||x - P_M(x)||^2 by Parseval (solver.cpp:89-102)
+  double s = 0.0;
+  for (std::size_t j = 0; j < count; ++j) {
+    double sj = 0.0;
+    for (int k = 0; k < nstrips; ++k) sj += h[j * nstrips + k];
+    s += sj / static_cast<double>(n);
+  }
+  *fft_sum = s;
+  if (pd && band_sum) {
+    double sb = 0.0;
+    for (std::size_t j = 0; j < count; ++j)
+      for (int k = 0; k < bstrips; ++k) sb += hb[j * bstrips + k];
+    *band_sum = sb;
+  }
+}
+
+}  // namespace
+}  // namespace pftg
+
+pftg_plan::~pftg_plan() {
+  if (dev32 >= 0) pftg::free_tables(t32);
+  if (dev64 >= 0) pftg::free_tables(t64);
+}
+
+// ------------------------------------------------------------------ C ABI
+using namespace pftg;
+
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PFTG_OK;
+  } catch (const cuda_error& e) {
+    set_error(e.what());
+    return PFTG_ECUDA;
+  } catch (const std::invalid_argument& e) {
+    set_error(std::string("invalid_argument: ") + e.what());
+    return PFTG_EINVAL;
+  } catch (const std::out_of_range& e) {
+    set_error(std::string("out_of_range: ") + e.what());
+    return PFTG_ERANGE;
+  } catch (const std::logic_error& e) {
+    set_error(std::string("logic_error: ") + e.what());
+    return PFTG_ELOGIC;
+  } catch (const std::exception& e) {
+    set_error(std::string("runtime_error: ") + e.what());
+    return PFTG_ERUNTIME;
+  }
+}
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+void check_dtype(int dtype) {
+  if (dtype != PFTG_C64 && dtype != PFTG_C128) throw std::invalid_argument("pftg: dtype must be PFTG_C64 or PFTG_C128");
+}
+
+void check_plan(const pftg_plan* p) {
+  if (!p) throw std::invalid_argument("pftg: null plan");
+}
+
+}  // namespace
+
+extern "C" {
+
+int pftg_version(void) { return 1; }
+
+int pftg_profile_begin(void) {
+  return guarded([&] {
+    ProfState& p = prof();
+    std::lock_guard<std::mutex> lock(p.mu);
+    for (auto& e : p.ev) {
+      cudaEventDestroy(e.second.first);
+      cudaEventDestroy(e.second.second);
+    }
+    p.ev.clear();
+    std::fill(p.launches, p.launches + K_NUM, 0);
+    p.on = true;
+  });
+}
+
+int pftg_profile_end(double* ms, int* count, int* launches) {
+  return guarded([&] {
+    ProfState& p = prof();
+    std::lock_guard<std::mutex> lock(p.mu);
+    p.on = false;
+    for (int k = 0; k < K_NUM; ++k) {
+      ms[k] = 0.0;
+      count[k] = 0;
+      if (launches) launches[k] = p.launches[k];
+    }
+    for (auto& e : p.ev) {
+      PFTG_CUDA(cudaEventSynchronize(e.second.second));
+      float t = 0.f;
+      PFTG_CUDA(cudaEventElapsedTime(&t, e.second.first, e.second.second));
+      ms[e.first] += t;
+      count[e.first] += 1;
+      cudaEventDestroy(e.second.first);
+      cudaEventDestroy(e.second.second);
+    }
+    p.ev.clear();
+  });
+}
+const char* pftg_last_error(void) { return g_err.c_str(); }
+
+int pftg_device_ok(void) {
+  try {
+    ensure_device();
+    return 1;
+  } catch (...) {
+    return 0;
+  }
+}
+
+int pftg_table_load(const char* path, pftg_table** out) {
+  return guarded([&] {
+    auto t = std::make_unique<pftg_table>();
+    t->t = table_load(path);
+    *out = t.release();
+  });
+}
+
+void pftg_table_free(pftg_table* t) { delete t; }
+
+int pftg_table_min_degree(const pftg_table* t, double eps, double target, int* r_out) {
+  return guarded([&] { *r_out = table_min_degree(t->t, eps, target); });
+}
+
+int pftg_plan_2d(const pftg_table* t, size_t n1, size_t n2, size_t mt1, size_t mt2, size_t p1, size_t p2,
+                 double eps, pftg_plan** out) {
+  return guarded([&] {
+    if (!t) throw std::invalid_argument("pftg_plan_2d: null scope table");
+    auto p = std::make_unique<pftg_plan>();
+    p->a1 = plan_1d(n1, mt1, p1, eps, t->t);
+    p->a2 = plan_1d(n2, mt2, p2, eps, t->t);
+    *out = p.release();
+  });
+}
+
+int pftg_plan_load(const char* path, pftg_plan** out) {
+  return guarded([&] {
+    auto p = std::make_unique<pftg_plan>();
+    plan_load(p->a1, p->a2, path);
+    *out = p.release();
+  });
+}
+
+int pftg_plan_save(const pftg_plan* plan, const char* path) {
+  return guarded([&] {
+    check_plan(plan);
+    plan_save(plan->a1, plan->a2, path);
+  });
+}
+
+void pftg_plan_free(pftg_plan* plan) { delete plan; }
+
+int pftg_plan_info(const pftg_plan* plan, int64_t* info) {
+  return guarded([&] {
+    check_plan(plan);
+    const Axis* ax[2] = {&plan->a1, &plan->a2};
+    for (int a = 0; a < 2; ++a) {
+      info[5 * a + 0] = (int64_t)ax[a]->n;
+      info[5 * a + 1] = (int64_t)ax[a]->p;
+      info[5 * a + 2] = (int64_t)ax[a]->q;
+      info[5 * a + 3] = (int64_t)ax[a]->mt;
+      info[5 * a + 4] = ax[a]->r;
+    }
+  });
+}
+
+int pftg_plan_tables(const pftg_plan* plan, int axis, double* B, double* W) {
+  return guarded([&] {
+    check_plan(plan);
+    if (axis != 1 && axis != 2) throw std::invalid_argument("pftg_plan_tables: axis must be 1 or 2");
+    const Axis& a = axis == 1 ? plan->a1 : plan->a2;
+    std::memcpy(B, a.B.data(), a.B.size() * sizeof(cd));
+    std::memcpy(W, a.W.data(), a.W.size() * sizeof(cd));
+  });
+}
+
+int pftg_apply_2d_dev(const pftg_plan* plan, int dtype, const void* z, void* band, size_t batch, void* stream) {
+  return guarded([&] {
+    check_plan(plan);
+    check_dtype(dtype);
+    if (batch == 0) return;
+    if (dtype == PFTG_C64) apply_dev<float>(plan, z, band, batch, S(stream));
+    else apply_dev<double>(plan, z, band, batch, S(stream));
+  });
+}
+
+int pftg_adjoint_2d_dev(const pftg_plan* plan, int dtype, const void* band, void* z, size_t batch, void* stream) {
+  return guarded([&] {
+    check_plan(plan);
+    check_dtype(dtype);
+    if (batch == 0) return;
+    if (dtype == PFTG_C64) adjoint_dev<float>(plan, band, z, batch, S(stream));
+    else adjoint_dev<double>(plan, band, z, batch, S(stream));
+  });
+}
+
+int pftg_apply_2d_host(const pftg_plan* plan, int dtype, const void* z, void* band, size_t batch) {
+  return guarded([&] {
+    check_plan(plan);
+    check_dtype(dtype);
+    if (batch == 0) return;
+    ensure_device();
+    const std::size_t nz = plan->a1.n * plan->a2.n, nb = 4 * plan->a1.mt * plan->a2.mt;
+    auto run = [&](auto tag) {
+      using R = decltype(tag);
+      const std::size_t chunk = host_chunk(batch, sizeof(Cx<R>) * nz);
+      host_pipeline<R>(batch, nz, nb, z, band, chunk, [&](Cx<R>* din, Cx<R>* dout, std::size_t nbat, cudaStream_t s) {
+        apply_dev<R>(plan, din, dout, nbat, s);
+      });
+    };
+    if (dtype == PFTG_C64) run(float{});
+    else run(double{});
+  });
+}
+
+int pftg_adjoint_2d_host(const pftg_plan* plan, int dtype, const void* band, void* z, size_t batch) {
+  return guarded([&] {
+    check_plan(plan);
+    check_dtype(dtype);
+    if (batch == 0) return;
+    ensure_device();
+    const std::size_t nz = plan->a1.n * plan->a2.n, nb = 4 * plan->a1.mt * plan->a2.mt;
+    auto run = [&](auto tag) {
+      using R = decltype(tag);
+      const std::size_t chunk = host_chunk(batch, sizeof(Cx<R>) * nz);
+      host_pipeline<R>(batch, nb, nz, band, z, chunk, [&](Cx<R>* din, Cx<R>* dout, std::size_t nbat, cudaStream_t s) {
+        adjoint_dev<R>(plan, din, dout, nbat, s);
+      });
+    };
+    if (dtype == PFTG_C64) run(float{});
+    else run(double{});
+  });
+}
+
+int pftg_band_residual_dev(const pftg_plan* plan, int dtype, const void* exit_wave, const void* dcrop, void* out,
+                           size_t batch, void* stream) {
+  return guarded([&] {
+    check_plan(plan);
+    check_dtype(dtype);
+    if (batch == 0) return;
+    if (dtype == PFTG_C64) band_residual_dev<float>(plan, exit_wave, dcrop, out, batch, S(stream));
+    else band_residual_dev<double>(plan, exit_wave, dcrop, out, batch, S(stream));
+  });
+}
+
+int pftg_fft2_dev(int dtype, const void* z, void* out, size_t rows, size_t cols, size_t batch, int inverse,
+                  void* stream) {
+  return guarded([&] {
+    check_dtype(dtype);
+    if (rows == 0 || cols == 0) throw std::invalid_argument("fast_fft2: empty field");
+    if (batch == 0) return;
+    ensure_device();
+    if (dtype == PFTG_C64) fft2_dev<float>(z, out, rows, cols, batch, inverse, S(stream));
+    else fft2_dev<double>(z, out, rows, cols, batch, inverse, S(stream));
+  });
+}
+
+int pftg_project_modulus_dev(int dtype, const void* exit_wave, const void* d, void* out, size_t rows, size_t cols,
+                             size_t batch, void* stream) {
+  return guarded([&] {
+    check_dtype(dtype);
+    if (batch == 0) return;
+    ensure_device();
+    if (dtype == PFTG_C64) project_modulus_dev<float>(exit_wave, d, out, rows, cols, batch, S(stream));
+    else project_modulus_dev<double>(exit_wave, d, out, rows, cols, batch, S(stream));
+  });
+}
+
+int pftg_crop_centered_dev(int dtype, const void* spectrum, void* out, size_t rows, size_t cols, size_t mt1,
+                           size_t mt2, size_t batch, void* stream) {
+  return guarded([&] {
+    check_dtype(dtype);
+    if (mt1 == 0 || mt2 == 0) throw std::invalid_argument("crop_centered: mt must be >= 1");
+    if (2 * mt1 > rows || 2 * mt2 > cols) throw std::invalid_argument("crop_centered: band exceeds spectrum shape");
+    if (batch == 0) return;
+    ensure_device();
+    const long long tot = 4LL * mt1 * mt2 * batch;
+    if (dtype == PFTG_C64)
+      k_crop<float><<<grid_for(tot), 256, 0, S(stream)>>>(static_cast<const float*>(spectrum), static_cast<float*>(out),
+                                                          (int)rows, (int)cols, (int)mt1, (int)mt2, (long long)batch);
+    else
+      k_crop<double><<<grid_for(tot), 256, 0, S(stream)>>>(static_cast<const double*>(spectrum),
+                                                           static_cast<double*>(out), (int)rows, (int)cols, (int)mt1,
+                                                           (int)mt2, (long long)batch);
+    PFTG_LAUNCH_CHECK();
+  });
+}
+
+int pftg_window_slice_dev(int dtype, const void* frame, size_t fr, size_t fc, void* patches, size_t wr, size_t wc,
+                          const int64_t* offsets, size_t npos, void* stream) {
+  return guarded([&] {
+    check_dtype(dtype);
+    (void)fr;
+    if (npos == 0) return;
+    ensure_device();
+    std::vector<long long> offs(npos);
+    for (size_t j = 0; j < npos; ++j) offs[j] = offsets[2 * j] * (long long)fc + offsets[2 * j + 1];
+    Scratch d(sizeof(long long) * npos, S(stream));
+    PFTG_CUDA(cudaMemcpyAsync(d.p, offs.data(), sizeof(long long) * npos, cudaMemcpyHostToDevice, S(stream)));
+    const long long tot = (long long)wr * wc * npos;
+    if (dtype == PFTG_C64)
+      k_window_slice<float2><<<grid_for(tot), 256, 0, S(stream)>>>(static_cast<const float2*>(frame), (long long)fc,
+                                                                   static_cast<float2*>(patches), (int)wr, (int)wc,
+                                                                   d.as<long long>(), (int)npos);
+    else
+      k_window_slice<double2><<<grid_for(tot), 256, 0, S(stream)>>>(static_cast<const double2*>(frame),
+                                                                    (long long)fc, static_cast<double2*>(patches),
+                                                                    (int)wr, (int)wc, d.as<long long>(), (int)npos);
+    PFTG_LAUNCH_CHECK();
+    // keep the offsets alive until the kernel has consumed them
+    PFTG_CUDA(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int pftg_set_window_dev(int dtype, void* frame, size_t fr, size_t fc, const void* patch, size_t wr, size_t wc,
+                        int64_t r0, int64_t c0, void* stream) {
+  return guarded([&] {
+    check_dtype(dtype);
+    (void)fr;
+    ensure_device();
+    const long long off = r0 * (long long)fc + c0;
+    const long long tot = (long long)wr * wc;
+    if (dtype == PFTG_C64)
+      k_set_window<float2><<<grid_for(tot), 256, 0, S(stream)>>>(static_cast<float2*>(frame), (long long)fc,
+                                                                 static_cast<const float2*>(patch), (int)wr, (int)wc,
+                                                                 off);
+    else
+      k_set_window<double2><<<grid_for(tot), 256, 0, S(stream)>>>(static_cast<double2*>(frame), (long long)fc,
+                                                                  static_cast<const double2*>(patch), (int)wr,
+                                                                  (int)wc, off);
+    PFTG_LAUNCH_CHECK();
+  });
+}
+
+int pftg_pie_object_update_dev(int dtype, void* zj, const void* probe, const void* proj, size_t n, double beta,
+                               void* stream) {
+  return guarded([&] {
+    check_dtype(dtype);
+    ensure_device();
+    if (dtype == PFTG_C64)
+      k_update<float2><<<grid_for(n), 256, 0, S(stream)>>>(static_cast<float2*>(zj), static_cast<const float2*>(probe),
+                                                           static_cast<const float2*>(proj), (long long)n, beta, 0);
+    else
+      k_update<double2><<<grid_for(n), 256, 0, S(stream)>>>(static_cast<double2*>(zj),
+                                                            static_cast<const double2*>(probe),
+                                                            static_cast<const double2*>(proj), (long long)n, beta, 0);
+    PFTG_LAUNCH_CHECK();
+  });
+}
+
+int pftg_epie_probe_update_dev(int dtype, void* probe, const void* zj, const void* proj, size_t n, double gamma,
+                               int blind, void* stream) {
+  return guarded([&] {
+    check_dtype(dtype);
+    if (!blind) throw std::logic_error("epie_probe_update: probe updates need blind mode");
+    ensure_device();
+    if (dtype == PFTG_C64)
+      k_update<float2><<<grid_for(n), 256, 0, S(stream)>>>(static_cast<float2*>(probe), static_cast<const float2*>(zj),
+                                                           static_cast<const float2*>(proj), (long long)n, gamma, 1);
+    else
+      k_update<double2><<<grid_for(n), 256, 0, S(stream)>>>(static_cast<double2*>(probe),
+                                                            static_cast<const double2*>(zj),
+                                                            static_cast<const double2*>(proj), (long long)n, gamma, 1);
+    PFTG_LAUNCH_CHECK();
+  });
+}
+
+int pftg_evaluate_dev(int dtype, const void* frame, size_t fr, size_t fc, const void* probe, size_t wr, size_t wc,
+                      const int64_t* offsets, size_t npos, size_t pos_begin, size_t pos_end, const void* d,
+                      const pftg_plan* plan, const void* dcrop, double* fft_sum, double* band_sum, void* stream) {
+  return guarded([&] {
+    check_dtype(dtype);
+    (void)fr;
+    ensure_device();
+    if (dtype == PFTG_C64)
+      evaluate_dev<float>(frame, fr, fc, probe, wr, wc, offsets, npos, pos_begin, pos_end, d, plan, dcrop, fft_sum,
+                          band_sum, S(stream));
+    else
+      evaluate_dev<double>(frame, fr, fc, probe, wr, wc, offsets, npos, pos_begin, pos_end, d, plan, dcrop, fft_sum,
+                           band_sum, S(stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,211 @@
+// Shared device helpers for the B200 PFT / ePIE kernels (sm_100a).
+//
+// Complex values are float2 (complex64) or double2 (complex128), interleaved
+// (re, im) exactly like the reference ComplexField storage
+// (/root/reference/proj/core/include/ptycho/field.hpp:37-65).
+//
+// Short FFTs run in registers across a "lane group": a transform of length
+// P*S is held by P lanes (P = min(len, 32)) with S slots each; element index
+// i = slot*P + lane. Stages whose butterfly distance h >= P pair two slots of
+// the same thread; stages with h < P pair lanes via __shfl_xor_sync. Every
+// thread carries a batch of NB independent transforms (e.g. all r
+// polynomial-coefficient columns) so each shuffle stage has NB-way ILP.
+//   fft_dif: natural-order input  -> bit-reversed output
+//   fft_dit: bit-reversed input   -> natural-order output
+// Both are unnormalized; sign = -1 forward, +1 backward (FFTW convention used by
+// the reference, /root/reference/proj/core/src/fft_internal.hpp:25-26).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace pftg {
+
+template <class R>
+struct CT;
+template <>
+struct CT<float> {
+  using C = float2;
+  static __host__ __device__ __forceinline__ float2 mk(float x, float y) { return make_float2(x, y); }
+};
+template <>
+struct CT<double> {
+  using C = double2;
+  static __host__ __device__ __forceinline__ double2 mk(double x, double y) { return make_double2(x, y); }
+};
+
+template <class C>
+struct RT;
+template <>
+struct RT<float2> { using R = float; };
+template <>
+struct RT<double2> { using R = double; };
+
+template <class C>
+__device__ __forceinline__ C cadd(C a, C b) { a.x += b.x; a.y += b.y; return a; }
+template <class C>
+__device__ __forceinline__ C csub(C a, C b) { a.x -= b.x; a.y -= b.y; return a; }
+template <class C>
+__device__ __forceinline__ C cmul(C a, C b) {
+  C r;
+  r.x = a.x * b.x - a.y * b.y;
+  r.y = a.x * b.y + a.y * b.x;
+  return r;
+}
+// conj(a) * b
+template <class C>
+__device__ __forceinline__ C cmulc(C a, C b) {
+  C r;
+  r.x = a.x * b.x + a.y * b.y;
+  r.y = a.x * b.y - a.y * b.x;
+  return r;
+}
+// acc += a * b
+template <class C>
+__device__ __forceinline__ void cmac(C& acc, C a, C b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+// acc += conj(a) * b
+template <class C>
+__device__ __forceinline__ void cmacc(C& acc, C a, C b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+// acc += B * z where B is the plan's B[l][j] entry, which is purely real for
+// even j and purely imaginary for odd j (/root/reference/proj/core/src/minimax.cpp:326-330,
+// pft.cpp:52-61); bv holds its nonzero part. 2 FMA per complex MAC.
+template <class C, class R>
+__device__ __forceinline__ void bmac(C& acc, R bv, C z, bool odd) {
+  if (!odd) {
+    acc.x = fma(bv, z.x, acc.x);
+    acc.y = fma(bv, z.y, acc.y);
+  } else {
+    acc.x = fma(-bv, z.y, acc.x);
+    acc.y = fma(bv, z.x, acc.y);
+  }
+}
+// acc += conj(B) * z
+template <class C, class R>
+__device__ __forceinline__ void bmacc(C& acc, R bv, C z, bool odd) {
+  if (!odd) {
+    acc.x = fma(bv, z.x, acc.x);
+    acc.y = fma(bv, z.y, acc.y);
+  } else {
+    acc.x = fma(bv, z.y, acc.x);
+    acc.y = fma(-bv, z.x, acc.y);
+  }
+}
+
+template <class C>
+__device__ __forceinline__ C czero() { C r; r.x = 0; r.y = 0; return r; }
+
+template <class C>
+__device__ __forceinline__ C shfl_xor(C v, int m) {
+  v.x = __shfl_xor_sync(0xffffffffu, v.x, m);
+  v.y = __shfl_xor_sync(0xffffffffu, v.y, m);
+  return v;
+}
+
+__host__ __device__ __forceinline__ int ilog2(int n) {
+  int l = 0;
+  while ((1 << l) < n) ++l;
+  return l;
+}
+
+__device__ __forceinline__ int bitrev(int i, int bits) { return static_cast<int>(__brev(static_cast<unsigned>(i)) >> (32 - bits)) & ((1 << bits) - 1); }
+
+// Twiddle lookup: tw[k] = exp(-2*pi*i*k/len) for k < len/2 (forward); sign=+1 conjugates.
+template <class C>
+__device__ __forceinline__ C twiddle(const C* tw, int k, int sign) {
+  C w = tw[k];
+  if (sign > 0) w.y = -w.y;
+  return w;
+}
+
+// DIF over the lane group. x[s][b]: slot s, batch b. len = P*S, P <= 32 lanes
+// (lanes of a group are lane_in_group = lane & (P-1); groups are P-aligned).
+// tw: table for length len.
+template <int S, int NB, class C>
+__device__ __forceinline__ void fft_dif(C (&x)[S][NB], int len, int P, int lig, const C* tw,
+                                        int sign) {
+  // in-thread stages: h = len/2 ... P   (pairs slot s and s + h/P)
+#pragma unroll
+  for (int hs = S / 2; hs >= 1; hs >>= 1) {
+    const int h = hs * P;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      if ((s & hs) == 0) {
+        const int i = s * P + lig;
+        const C w = twiddle(tw, (i & (h - 1)) * (len / (2 * h)), sign);
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const C a = x[s][b], c = x[s + hs][b];
+          x[s][b] = cadd(a, c);
+          x[s + hs][b] = cmul(csub(a, c), w);
+        }
+      }
+    }
+  }
+  // cross-lane stages: h = P/2 ... 1
+  for (int h = P / 2; h >= 1; h >>= 1) {
+    const bool upper = (lig & h) != 0;
+    const C w = twiddle(tw, (lig & (h - 1)) * (len / (2 * h)), sign);
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const C o = shfl_xor(x[s][b], h);
+        x[s][b] = upper ? cmul(csub(o, x[s][b]), w) : cadd(x[s][b], o);
+      }
+  }
+}
+
+// DIT over the lane group: bit-reversed input -> natural output.
+template <int S, int NB, class C>
+__device__ __forceinline__ void fft_dit(C (&x)[S][NB], int len, int P, int lig, const C* tw,
+                                        int sign) {
+  for (int h = 1; h < P; h <<= 1) {
+    const bool upper = (lig & h) != 0;
+    const C w = twiddle(tw, (lig & (h - 1)) * (len / (2 * h)), sign);
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        // lower: a + w*c ; upper: a - w*c, where c is the upper element
+        const C mine = upper ? cmul(x[s][b], w) : x[s][b];
+        const C o = shfl_xor(mine, h);
+        x[s][b] = upper ? csub(o, mine) : cadd(mine, o);
+      }
+  }
+#pragma unroll
+  for (int hs = 1; hs < S; hs <<= 1) {
+    const int h = hs * P;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      if ((s & hs) == 0) {
+        const int i = s * P + lig;
+        const C w = twiddle(tw, (i & (h - 1)) * (len / (2 * h)), sign);
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const C a = x[s][b];
+          const C t = cmul(x[s + hs][b], w);
+          x[s][b] = cadd(a, t);
+          x[s + hs][b] = csub(a, t);
+        }
+      }
+    }
+  }
+}
+
+// Non-negative t mod p (/root/reference/proj/core/src/pft.cpp:25-29).
+__host__ __device__ __forceinline__ int mod_nonneg(int t, int p) {
+  int m = t % p;
+  return m < 0 ? m + p : m;
+}
+
+}  // namespace pftg

@@ -1,0 +1,144 @@
+// Launchers for the full 2-D FFT passes; included once per precision by
+// fft_launch_f32.cu / fft_launch_f64.cu (PFTG_REAL = float | double).
+#include <cmath>
+#include <mutex>
+#include <type_traits>
+
+#include "internal.hpp"
+
+namespace pftg {
+
+namespace {
+
+template <int V>
+using IC = std::integral_constant<int, V>;
+
+template <class F>
+void dispatch_slots(int S, F&& f) {
+  switch (S) {
+    case 1: f(IC<1>{}); break;
+    case 2: f(IC<2>{}); break;
+    case 4: f(IC<4>{}); break;
+    case 8: f(IC<8>{}); break;
+    case 16: f(IC<16>{}); break;
+    case 32: f(IC<32>{}); break;
+    default: throw std::invalid_argument("pftg: FFT length out of range");
+  }
+}
+
+template <class K>
+void allow_smem_fft(K kernel) {
+  PFTG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+}
+
+int slots_for(int n) { return n <= 32 ? 1 : n / 32; }
+
+}  // namespace
+
+using R_ = PFTG_REAL;
+using C_ = typename CT<R_>::C;
+
+template <>
+const C_* fft_twiddles<R_>(int n) {
+  // One device table per (device, length); built once, never freed (tiny).
+  static std::mutex mu;
+  static C_* tabs[64][11] = {};
+  int dev = 0;
+  PFTG_CUDA(cudaGetDevice(&dev));
+  const int lg = ilog2(n);
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev >= 64) throw std::runtime_error("pftg: device index out of range");
+  if (!tabs[dev][lg]) {
+    const int h = n / 2 > 0 ? n / 2 : 1;
+    std::vector<C_> host(static_cast<size_t>(h));
+    for (int k = 0; k < h; ++k) {
+      const double a = -2.0 * M_PI * static_cast<double>(k) / static_cast<double>(n);
+      host[k] = CT<R_>::mk(static_cast<R_>(std::cos(a)), static_cast<R_>(std::sin(a)));
+    }
+    C_* d = nullptr;
+    PFTG_CUDA(cudaMalloc(&d, sizeof(C_) * h));
+    PFTG_CUDA(cudaMemcpy(d, host.data(), sizeof(C_) * h, cudaMemcpyHostToDevice));
+    tabs[dev][lg] = d;
+  }
+  return tabs[dev][lg];
+}
+
+template <>
+void launch_fft_rows<R_>(int mode, int epi, int n1, int n2, const RowSrc<R_>& src, C_* X, long long x_bstride,
+                         int sign, double scale, const RowEpiArgs& ep, int batch, cudaStream_t st) {
+  const C_* tw = fft_twiddles<R_>(n2);
+  const int S = slots_for(n2);
+  const int P = n2 / S;
+  const int rows_per_cta = 8 * (32 / P);
+  const dim3 grid((n1 + rows_per_cta - 1) / rows_per_cta, batch);
+  const size_t smem = sizeof(C_) * (n2 / 2 + 1);
+  ProfScope prof(st, K_FFT_ROWS);
+  dispatch_slots(S, [&](auto s) {
+    constexpr int SS = decltype(s)::value;
+    if (mode == ROW_DIF_STORE) {
+      k_fft_rows<R_, SS, ROW_DIF_STORE, EPI_STORE><<<grid, 256, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
+                                                                           x_bstride, sign, scale, ep);
+    } else if (mode == ROW_DIT_NATURAL) {
+      k_fft_rows<R_, SS, ROW_DIT_NATURAL, EPI_STORE><<<grid, 256, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
+                                                                             x_bstride, sign, scale, ep);
+    } else if (epi == EPI_STORE) {
+      k_fft_rows<R_, SS, ROW_DIT_PROJ, EPI_STORE><<<grid, 256, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
+                                                                          x_bstride, sign, scale, ep);
+    } else if (epi == EPI_OBJ) {
+      k_fft_rows<R_, SS, ROW_DIT_PROJ, EPI_OBJ><<<grid, 256, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
+                                                                        x_bstride, sign, scale, ep);
+    } else {
+      k_fft_rows<R_, SS, ROW_DIT_PROJ, EPI_PROBE><<<grid, 256, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
+                                                                          x_bstride, sign, scale, ep);
+    }
+  });
+  PFTG_LAUNCH_CHECK();
+}
+
+template <>
+int fft_cols_strips<R_>(int n2) {
+  const int nc0 = sizeof(R_) == 4 ? 16 : 8;
+  const int nc = n2 < nc0 ? n2 : nc0;
+  return n2 / nc;
+}
+
+template <>
+void launch_fft_cols<R_>(int mode, int n1, int n2, C_* X, long long x_bstride, const R_* d, long long d_bstride,
+                         const long long* d_index, int dmode, int sign, double* partial, int batch,
+                         cudaStream_t st) {
+  const C_* tw = fft_twiddles<R_>(n1);
+  const int S = slots_for(n1);
+  const int nc0 = sizeof(R_) == 4 ? 16 : 8;
+  const int nc = n2 < nc0 ? n2 : nc0;
+  const dim3 grid(n2 / nc, batch);
+  size_t smem = sizeof(C_) * ((size_t)n1 * (nc + 1) + n1 / 2 + 1);
+  if (mode != COL_NATURAL && dmode == 0) smem += sizeof(R_) * (size_t)n1 * nc;
+  smem = (smem + 15) & ~size_t(15);
+  if (smem < 64 * sizeof(double)) smem = 64 * sizeof(double);
+  ProfScope prof(st, K_FFT_COLS);
+  dispatch_slots(S, [&](auto s) {
+    constexpr int SS = decltype(s)::value;
+    if (mode == COL_PROJECT) {
+      auto k = k_fft_cols<R_, SS, COL_PROJECT>;
+      static bool once = (allow_smem_fft(k), true);
+      (void)once;
+      k<<<grid, 256, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
+                                 dmode, sign, partial);
+    } else if (mode == COL_EVAL) {
+      auto k = k_fft_cols<R_, SS, COL_EVAL>;
+      static bool once = (allow_smem_fft(k), true);
+      (void)once;
+      k<<<grid, 256, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
+                                 dmode, sign, partial);
+    } else {
+      auto k = k_fft_cols<R_, SS, COL_NATURAL>;
+      static bool once = (allow_smem_fft(k), true);
+      (void)once;
+      k<<<grid, 256, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
+                                 dmode, sign, partial);
+    }
+  });
+  PFTG_LAUNCH_CHECK();
+}
+
+}  // namespace pftg

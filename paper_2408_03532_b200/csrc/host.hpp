@@ -1,0 +1,45 @@
+// Host-only (no CUDA) pieces of the offline phase: scope table and plan
+// tables. See plan.cpp.
+#pragma once
+
+#include <complex>
+#include <cstddef>
+#include <string>
+#include <vector>
+
+namespace pftg {
+
+using cd = std::complex<double>;
+
+// minimax::ScopeRecord (minimax.hpp:35-41)
+struct Record {
+  double eps = 0.0;
+  int r = 0;
+  double xi = 0.0;
+  double achieved_error = 0.0;
+  std::vector<cd> coeff;
+};
+
+// minimax::ScopeTable (minimax.hpp:45-70)
+struct Table {
+  int max_r = 0;
+  std::vector<Record> records;
+};
+
+// pft::PftPlan1D (pft.hpp:25-31)
+struct Axis {
+  std::size_t n = 0, p = 0, q = 0, mt = 0;
+  int r = 0;
+  double eps = 0.0;
+  std::vector<cd> B;  // q x r
+  std::vector<cd> W;  // (2mt+1) x r
+};
+
+Table table_load(const std::string& path);
+const Record* table_find(const Table& t, double eps, int r);
+int table_min_degree(const Table& t, double eps, double target);
+Axis plan_1d(std::size_t n, std::size_t mt, std::size_t p, double eps, const Table& table);
+void plan_save(const Axis& a1, const Axis& a2, const std::string& path);
+void plan_load(Axis& a1, Axis& a2, const std::string& path);
+
+}  // namespace pftg

@@ -1,0 +1,127 @@
+// Host-side internals shared by the CUDA translation units of libpftg.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <complex>
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "fft_kernels.cuh"
+#include "host.hpp"
+#include "pft_kernels.cuh"
+
+namespace pftg {
+
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
+#define PFTG_CUDA(x)                                                        \
+  do {                                                                      \
+    cudaError_t e_ = (x);                                                   \
+    if (e_ != cudaSuccess) ::pftg::throw_cuda(e_, #x, __FILE__, __LINE__);  \
+  } while (0)
+#define PFTG_LAUNCH_CHECK() PFTG_CUDA(cudaGetLastError())
+
+template <class R>
+struct DevTables {
+  R* Bv1 = nullptr;
+  R* Bv2 = nullptr;
+  typename CT<R>::C* W1t = nullptr;
+  typename CT<R>::C* W2t = nullptr;
+  typename CT<R>::C* tw1 = nullptr;
+  typename CT<R>::C* tw2 = nullptr;
+};
+
+}  // namespace pftg
+
+// pft::PftPlan2D (pft.hpp:44-47): host tables + lazily uploaded device tables.
+struct pftg_plan {
+  pftg::Axis a1, a2;
+  mutable std::mutex mu;
+  mutable int dev32 = -1, dev64 = -1;  // device the tables live on (-1 = not uploaded)
+  mutable pftg::DevTables<float> t32;
+  mutable pftg::DevTables<double> t64;
+  mutable pftg::PftDev<float> pd32{};
+  mutable pftg::PftDev<double> pd64{};
+  ~pftg_plan();
+};
+
+struct pftg_table {
+  pftg::Table t;
+};
+
+namespace pftg {
+
+// Validates the GPU constraints and returns the device descriptor (uploads
+// the tables on first use).
+template <class R>
+const PftDev<R>& plan_dev(const pftg_plan& p);
+
+// ---- PFT building blocks (pft_launch_*.cu); all stream-ordered ----
+template <class R>
+void launch_fwd_rows(const PftDev<R>& pd, const Src<R>& src, typename CT<R>::C* G, int batch,
+                     cudaStream_t st);
+// mode 0: band out; 1: residual -> Gout; 2: evaluator partials [batch][cols_strips]
+template <class R>
+void launch_fwd_cols(const PftDev<R>& pd, int mode, const typename CT<R>::C* G, typename CT<R>::C* band,
+                     const R* dcrop, long long dstride, typename CT<R>::C* Gout, double* partial, int batch,
+                     cudaStream_t st);
+template <class R>
+int cols_strips(const PftDev<R>& pd);
+template <class R>
+void launch_adj_cols(const PftDev<R>& pd, const typename CT<R>::C* band, typename CT<R>::C* Gt, int batch,
+                     cudaStream_t st);
+template <class R>
+void launch_adj_rows(const PftDev<R>& pd, int epi, const typename CT<R>::C* Gt, const EpiArgs& ep,
+                     int batch, cudaStream_t st);
+
+// ---- full FFT building blocks (fft_launch_*.cu) ----
+template <class R>
+const typename CT<R>::C* fft_twiddles(int n);  // device table exp(-2 pi i k/n), k < n/2
+template <class R>
+void launch_fft_rows(int mode, int epi, int n1, int n2, const RowSrc<R>& src, typename CT<R>::C* X,
+                     long long x_bstride, int sign, double scale, const RowEpiArgs& ep, int batch,
+                     cudaStream_t st);
+template <class R>
+void launch_fft_cols(int mode, int n1, int n2, typename CT<R>::C* X, long long x_bstride, const R* d,
+                     long long d_bstride, const long long* d_index, int dmode, int sign,
+                     double* partial, int batch, cudaStream_t st);
+template <class R>
+int fft_cols_strips(int n2);
+
+// Stream-ordered scratch allocation (cudaMallocAsync on the default pool).
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  Scratch() = default;
+  Scratch(std::size_t bytes, cudaStream_t s);
+  ~Scratch();
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+void ensure_device();
+void check_fft_len(std::size_t n);
+
+// Optional per-kernel timing (pftg_profile_*): CUDA events recorded around
+// each launch on its own stream while profiling is on (never inside a graph
+// capture). Kernel ids:
+enum KernelId { K_FWD_ROWS = 0, K_FWD_COLS, K_ADJ_COLS, K_ADJ_ROWS, K_FFT_ROWS, K_FFT_COLS, K_NUM };
+struct ProfScope {
+  int kid;
+  cudaStream_t st;
+  cudaEvent_t e0 = nullptr;
+  ProfScope(cudaStream_t s, int k);
+  ~ProfScope();
+};
+
+}  // namespace pftg

@@ -1,0 +1,496 @@
+// Device-resident hybrid_solve (PFT-warm-started ePIE).
+//
+// Reference: /root/reference/proj/core/src/solver.cpp:173-302. Semantics kept:
+//  - positions visited in list order, or shuffled per sweep with the
+//    reference's mt19937_64 Fisher-Yates stream (solver.cpp:164-169, 223, 236);
+//  - stage = band iff sweep <= pft_sweeps (233); band plan defaults
+//    mt = window/8, p = mt (195-198); dcrop = crop_centered(d) (202-208);
+//  - band stage per position: resid = band_residual(P z_j); z_j -= beta_pft
+//    conj(P) resid; blind: resid2 from the updated z_j, P -= gamma_pft conj(z_j)
+//    resid2 (243-251);
+//  - FFT stage: pie_object_update then (blind) epie_probe_update with the
+//    projection of the updated exit wave (253-259);
+//  - per sweep: objective over all positions (287), divergence guards
+//    (291-295) and the relative-change stop (296-299).
+// TV smoothing (264-279) is not on the BASELINE path and is rejected if asked.
+//
+// Each position is 3 (non-blind) or 5 (blind) kernel launches that keep the
+// patch, spectrum and PFT intermediates in L2; a whole sweep is captured once
+// into a CUDA graph (sequential order) and replayed.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <random>
+#include <stdexcept>
+#include <vector>
+
+#include "../../include/pftg.h"
+#include "internal.hpp"
+
+namespace pftg {
+void set_error(const std::string& m);
+}
+
+using namespace pftg;
+
+namespace {
+
+template <class R>
+__global__ void k_norm_finite(const typename CT<R>::C* __restrict__ a, long long n, double* __restrict__ out) {
+  // out[0] += sum |a|^2 per CTA partial (written to out[blockIdx.x]); out[gridDim.x + blockIdx.x] = nonfinite count
+  double s = 0.0, bad = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const auto v = a[i];
+    if (!isfinite(v.x) || !isfinite(v.y)) bad += 1.0;
+    s += (double)v.x * v.x + (double)v.y * v.y;
+  }
+  __shared__ double sh[2][32];
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][threadIdx.x >> 5] = s;
+    sh[1][threadIdx.x >> 5] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ts = 0, tb = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      ts += sh[0][w];
+      tb += sh[1][w];
+    }
+    out[blockIdx.x] = ts;
+    out[gridDim.x + blockIdx.x] = tb;
+  }
+}
+
+template <class R>
+__global__ void k_diff_norm(const typename CT<R>::C* __restrict__ a, const typename CT<R>::C* __restrict__ b,
+                            long long n, double* __restrict__ out) {
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double dx = (double)a[i].x - b[i].x, dy = (double)a[i].y - b[i].y;
+    s += dx * dx + dy * dy;
+  }
+  __shared__ double sh[32];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    out[blockIdx.x] = t;
+  }
+}
+
+template <class R>
+__global__ void k_crop_real(const R* __restrict__ d, R* __restrict__ out, int w1, int w2, int mt1, int mt2,
+                            long long count) {
+  const long long M = 4LL * mt1 * mt2;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < M * count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long f = i / M;
+    const int rem = (int)(i % M);
+    const int a = rem / (2 * mt2), b = rem % (2 * mt2);
+    out[i] = d[f * (long long)w1 * w2 + (long long)mod_nonneg(a - mt1, w1) * w2 + mod_nonneg(b - mt2, w2)];
+  }
+}
+
+constexpr int kRedBlocks = 296;
+
+}  // namespace
+
+struct pftg_solver {
+  int dtype = PFTG_C64;
+  std::size_t fr = 0, fc = 0, wr = 0, wc = 0, npos = 0;
+  pftg_solver_config cfg{};
+  std::vector<long long> offs;  // linear offsets r0*fc + c0, reference list order
+  std::vector<std::size_t> order;
+  std::mt19937_64 shuffle_rng;
+  std::unique_ptr<pftg_plan> plan;
+  cudaStream_t st = nullptr;
+  void* frame = nullptr;
+  void* probe = nullptr;
+  void* prev = nullptr;
+  void* d = nullptr;
+  void* dperm = nullptr;
+  void* dcrop = nullptr;
+  long long* doffs = nullptr;  // per list position
+  void* G = nullptr;
+  void* Gt = nullptr;
+  void* X = nullptr;
+  void* X2 = nullptr;
+  void* Xe = nullptr;  // evaluator chunk
+  double* part = nullptr;
+  double* red = nullptr;
+  std::size_t eval_chunk = 1;
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};  // [band, fft]
+  std::vector<double> objective, wall;
+  int sweeps_run = 0;
+  int flags = 0;
+  double frame_guard = 0, probe_guard = 0;
+  double t_accum = 0;
+
+  ~pftg_solver() {
+    for (auto& g : graph)
+      if (g) cudaGraphExecDestroy(g);
+    void* bufs[] = {frame, probe, prev, d, dperm, dcrop, doffs, G, Gt, X, X2, Xe, part, red};
+    for (void* b : bufs)
+      if (b) cudaFree(b);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+namespace {
+
+template <class R>
+using Cx = typename CT<R>::C;
+
+template <class R>
+void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
+  const cudaStream_t st = s.st;
+  const int n1 = (int)s.wr, n2 = (int)s.wc;
+  const long long n = (long long)n1 * n2;
+  Cx<R>* frame = static_cast<Cx<R>*>(s.frame);
+  Cx<R>* probe = static_cast<Cx<R>*>(s.probe);
+  const long long* doff = s.doffs + j;
+  const bool blind = s.cfg.blind != 0;
+  if (band) {
+    const PftDev<R>& pd = plan_dev<R>(*s.plan);
+    const long long mb = (long long)pd.M1 * pd.M2;
+    const R* dc = static_cast<const R*>(s.dcrop) + (long long)j * mb;
+    Src<R> src{frame, (long long)s.fc, 0, doff, probe};
+    launch_fwd_rows<R>(pd, src, static_cast<Cx<R>*>(s.G), 1, st);
+    launch_fwd_cols<R>(pd, 1, static_cast<Cx<R>*>(s.G), nullptr, dc, mb, static_cast<Cx<R>*>(s.Gt), nullptr, 1, st);
+    EpiArgs ep{};
+    ep.obj = frame;
+    ep.obj_ld = (long long)s.fc;
+    ep.obj_off = s.offs[j];
+    ep.probe = probe;
+    ep.step = s.cfg.beta_pft;
+    ep.G2 = blind ? s.G : nullptr;
+    launch_adj_rows<R>(pd, 1, static_cast<Cx<R>*>(s.Gt), ep, 1, st);
+    if (blind) {
+      launch_fwd_cols<R>(pd, 1, static_cast<Cx<R>*>(s.G), nullptr, dc, mb, static_cast<Cx<R>*>(s.Gt), nullptr, 1,
+                         st);
+      ep.step = s.cfg.gamma_pft;
+      ep.G2 = nullptr;
+      launch_adj_rows<R>(pd, 2, static_cast<Cx<R>*>(s.Gt), ep, 1, st);
+    }
+    return;
+  }
+  const R* dp = static_cast<const R*>(s.dperm) + (long long)j * n;
+  RowSrc<R> src{frame, (long long)s.fc, 0, doff, probe};
+  RowEpiArgs ep{};
+  launch_fft_rows<R>(ROW_DIF_STORE, EPI_STORE, n1, n2, src, static_cast<Cx<R>*>(s.X), n, -1, 1.0, ep, 1, st);
+  launch_fft_cols<R>(COL_PROJECT, n1, n2, static_cast<Cx<R>*>(s.X), n, dp, n, nullptr, 0, -1, nullptr, 1, st);
+  ep.obj = frame;
+  ep.obj_ld = (long long)s.fc;
+  ep.obj_offs = doff;
+  ep.probe = probe;
+  ep.step = s.cfg.beta;
+  ep.out = s.X2;
+  ep.out_bstride = n;
+  ep.fuse_next = blind ? 1 : 0;
+  const double scale = 1.0 / static_cast<double>(n);
+  launch_fft_rows<R>(ROW_DIT_PROJ, EPI_OBJ, n1, n2, src, static_cast<Cx<R>*>(s.X), n, +1, scale, ep, 1, st);
+  if (blind) {
+    launch_fft_cols<R>(COL_PROJECT, n1, n2, static_cast<Cx<R>*>(s.X2), n, dp, n, nullptr, 0, -1, nullptr, 1, st);
+    ep.step = s.cfg.gamma;
+    ep.fuse_next = 0;
+    launch_fft_rows<R>(ROW_DIT_PROJ, EPI_PROBE, n1, n2, src, static_cast<Cx<R>*>(s.X2), n, +1, scale, ep, 1, st);
+  }
+}
+
+template <class R>
+void enqueue_sweep(pftg_solver& s, bool band) {
+  for (std::size_t t = 0; t < s.npos; ++t) enqueue_position<R>(s, s.order[t], band);
+}
+
+template <class R>
+double objective(pftg_solver& s) {
+  // (1/N) sum_j (1/n) sum_k (|X_jk| - d_jk)^2  (Parseval form of solver.cpp:89-102)
+  const int n1 = (int)s.wr, n2 = (int)s.wc;
+  const long long n = (long long)n1 * n2;
+  const int strips = fft_cols_strips<R>(n2);
+  for (std::size_t c0 = 0; c0 < s.npos; c0 += s.eval_chunk) {
+    const int nb = (int)std::min(s.eval_chunk, s.npos - c0);
+    RowSrc<R> src{static_cast<const Cx<R>*>(s.frame), (long long)s.fc, 0, s.doffs + c0,
+                  static_cast<const Cx<R>*>(s.probe)};
+    RowEpiArgs ep{};
+    launch_fft_rows<R>(ROW_DIF_STORE, EPI_STORE, n1, n2, src, static_cast<Cx<R>*>(s.Xe), n, -1, 1.0, ep, nb, s.st);
+    launch_fft_cols<R>(COL_EVAL, n1, n2, static_cast<Cx<R>*>(s.Xe), n, static_cast<const R*>(s.dperm) + c0 * n, n,
+                       nullptr, 0, -1, s.part + c0 * strips, nb, s.st);
+  }
+  std::vector<double> h(s.npos * strips);
+  PFTG_CUDA(cudaMemcpyAsync(h.data(), s.part, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s.st));
+  PFTG_CUDA(cudaStreamSynchronize(s.st));
+  double acc = 0.0;
+  for (std::size_t j = 0; j < s.npos; ++j) {
+    double sj = 0.0;
+    for (int k = 0; k < strips; ++k) sj += h[j * strips + k];
+    acc += sj / static_cast<double>(n);
+  }
+  return acc / static_cast<double>(s.npos);
+}
+
+template <class R>
+void norm_finite(pftg_solver& s, const void* a, long long n, double* norm, bool* finite) {
+  k_norm_finite<R><<<kRedBlocks, 256, 0, s.st>>>(static_cast<const Cx<R>*>(a), n, s.red);
+  PFTG_LAUNCH_CHECK();
+  std::vector<double> h(2 * kRedBlocks);
+  PFTG_CUDA(cudaMemcpyAsync(h.data(), s.red, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s.st));
+  PFTG_CUDA(cudaStreamSynchronize(s.st));
+  double t = 0, bad = 0;
+  for (int i = 0; i < kRedBlocks; ++i) {
+    t += h[i];
+    bad += h[kRedBlocks + i];
+  }
+  *norm = std::sqrt(t);
+  *finite = bad == 0.0;
+}
+
+template <class R>
+void run(pftg_solver& s, int max_sweeps) {
+  const int total = s.cfg.pft_sweeps + s.cfg.fft_sweeps;
+  int done = 0;
+  const long long fn = (long long)s.fr * s.fc, pn = (long long)s.wr * s.wc;
+  while (s.sweeps_run < total && (s.flags & 3) == 0 && (max_sweeps <= 0 || done < max_sweeps)) {
+    const int sweep = s.sweeps_run + 1;
+    const bool band = sweep <= s.cfg.pft_sweeps;
+    const auto t0 = std::chrono::steady_clock::now();
+    if (s.cfg.tol > 0.0)
+      PFTG_CUDA(cudaMemcpyAsync(s.prev, s.frame, sizeof(Cx<R>) * fn, cudaMemcpyDeviceToDevice, s.st));
+    if (s.cfg.shuffled) {
+      // Fisher-Yates with explicit modulo draws (solver.cpp:164-169)
+      for (std::size_t i = s.order.size(); i > 1; --i) {
+        const std::size_t j = static_cast<std::size_t>(s.shuffle_rng() % i);
+        std::swap(s.order[i - 1], s.order[j]);
+      }
+      enqueue_sweep<R>(s, band);
+    } else {
+      cudaGraphExec_t& g = s.graph[band ? 0 : 1];
+      if (!g) {
+        cudaGraph_t graph;
+        PFTG_CUDA(cudaStreamBeginCapture(s.st, cudaStreamCaptureModeThreadLocal));
+        try {
+          enqueue_sweep<R>(s, band);
+        } catch (...) {
+          cudaStreamEndCapture(s.st, &graph);
+          throw;
+        }
+        PFTG_CUDA(cudaStreamEndCapture(s.st, &graph));
+        PFTG_CUDA(cudaGraphInstantiate(&g, graph, 0));
+        cudaGraphDestroy(graph);
+      }
+      PFTG_CUDA(cudaGraphLaunch(g, s.st));
+    }
+    PFTG_CUDA(cudaStreamSynchronize(s.st));
+    s.sweeps_run = sweep;
+    ++done;
+    s.t_accum += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    s.wall.push_back(s.t_accum);
+    const auto t1 = std::chrono::steady_clock::now();
+    const bool eval = s.cfg.objective_every <= 1 || (sweep % s.cfg.objective_every) == 0 || sweep == total;
+    s.objective.push_back(eval ? objective<R>(s) : std::nan(""));
+    double fnrm, pnrm;
+    bool ffin, pfin;
+    norm_finite<R>(s, s.frame, fn, &fnrm, &ffin);
+    norm_finite<R>(s, s.probe, pn, &pnrm, &pfin);
+    bool stop_tol = false;
+    if (ffin && pfin && fnrm <= s.frame_guard && pnrm <= s.probe_guard && s.cfg.tol > 0.0) {
+      double pv;
+      bool pf;
+      norm_finite<R>(s, s.prev, fn, &pv, &pf);
+      if (pv == 0.0) {
+        std::fprintf(stderr, "relative_change_below: zero reference norm, not stopping\n");
+      } else {
+        k_diff_norm<R><<<kRedBlocks, 256, 0, s.st>>>(static_cast<const Cx<R>*>(s.frame),
+                                                     static_cast<const Cx<R>*>(s.prev), fn, s.red);
+        PFTG_LAUNCH_CHECK();
+        std::vector<double> h(kRedBlocks);
+        PFTG_CUDA(cudaMemcpyAsync(h.data(), s.red, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s.st));
+        PFTG_CUDA(cudaStreamSynchronize(s.st));
+        double num = 0;
+        for (double v : h) num += v;
+        stop_tol = std::sqrt(num) / pv <= s.cfg.tol;
+      }
+    }
+    // objective + guards are part of the reference's per-sweep cost (solver.cpp:286-299)
+    s.t_accum += std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+    if (!ffin || !pfin || fnrm > s.frame_guard || pnrm > s.probe_guard) {
+      s.flags |= 1;
+      break;
+    }
+    if (stop_tol) {
+      s.flags |= 2;
+      break;
+    }
+  }
+}
+
+template <class R>
+void create(pftg_solver& s, const void* frame, const void* probe, const int64_t* offsets, const void* d,
+            const pftg_table* table) {
+  const long long fn = (long long)s.fr * s.fc, pn = (long long)s.wr * s.wc;
+  check_fft_len(s.wr);
+  check_fft_len(s.wc);
+  for (std::size_t j = 0; j < s.npos; ++j) {
+    const long long r0 = offsets[2 * j], c0 = offsets[2 * j + 1];
+    // The reference does not bounds-check offsets (scan.cpp:14-22); reading
+    // out of the device frame would fault, so reject it here instead.
+    if (r0 < 0 || c0 < 0 || r0 + (long long)s.wr > (long long)s.fr || c0 + (long long)s.wc > (long long)s.fc)
+      throw std::out_of_range("scan: window outside the frame");
+    s.offs.push_back(r0 * (long long)s.fc + c0);
+  }
+  s.order.resize(s.npos);
+  std::iota(s.order.begin(), s.order.end(), std::size_t{0});
+  s.shuffle_rng.seed(s.cfg.seed);
+  PFTG_CUDA(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+  PFTG_CUDA(cudaMalloc(&s.frame, sizeof(Cx<R>) * fn));
+  PFTG_CUDA(cudaMalloc(&s.probe, sizeof(Cx<R>) * pn));
+  PFTG_CUDA(cudaMemcpy(s.frame, frame, sizeof(Cx<R>) * fn, cudaMemcpyHostToDevice));
+  PFTG_CUDA(cudaMemcpy(s.probe, probe, sizeof(Cx<R>) * pn, cudaMemcpyHostToDevice));
+  if (s.cfg.tol > 0.0) PFTG_CUDA(cudaMalloc(&s.prev, sizeof(Cx<R>) * fn));
+  PFTG_CUDA(cudaMalloc(&s.d, sizeof(R) * pn * s.npos));
+  PFTG_CUDA(cudaMemcpy(s.d, d, sizeof(R) * pn * s.npos, cudaMemcpyHostToDevice));
+  PFTG_CUDA(cudaMalloc(&s.dperm, sizeof(R) * pn * s.npos));
+  k_permute_d<R><<<148 * 16, 256, 0, s.st>>>(static_cast<const R*>(s.d), static_cast<R*>(s.dperm), (int)s.wr,
+                                             (int)s.wc, ilog2((int)s.wr), ilog2((int)s.wc), (long long)s.npos);
+  PFTG_LAUNCH_CHECK();
+  PFTG_CUDA(cudaMalloc(&s.doffs, sizeof(long long) * std::max<std::size_t>(s.npos, 1)));
+  PFTG_CUDA(cudaMemcpy(s.doffs, s.offs.data(), sizeof(long long) * s.npos, cudaMemcpyHostToDevice));
+  PFTG_CUDA(cudaMalloc(&s.X, sizeof(Cx<R>) * pn));
+  PFTG_CUDA(cudaMalloc(&s.X2, sizeof(Cx<R>) * pn));
+  s.eval_chunk = std::max<std::size_t>(1, std::min<std::size_t>(s.npos, (64u << 20) / (sizeof(Cx<R>) * pn)));
+  PFTG_CUDA(cudaMalloc(&s.Xe, sizeof(Cx<R>) * pn * s.eval_chunk));
+  PFTG_CUDA(cudaMalloc(&s.part, sizeof(double) * fft_cols_strips<R>((int)s.wc) * std::max<std::size_t>(s.npos, 1)));
+  PFTG_CUDA(cudaMalloc(&s.red, sizeof(double) * 2 * kRedBlocks));
+  (void)fft_twiddles<R>((int)s.wr);
+  (void)fft_twiddles<R>((int)s.wc);
+  if (s.cfg.pft_sweeps > 0) {
+    // solver.cpp:194-209
+    const std::size_t mt1 = s.cfg.mt1 ? (std::size_t)s.cfg.mt1 : s.wr / 8;
+    const std::size_t mt2 = s.cfg.mt2 ? (std::size_t)s.cfg.mt2 : s.wc / 8;
+    const std::size_t p1 = s.cfg.p1 ? (std::size_t)s.cfg.p1 : mt1;
+    const std::size_t p2 = s.cfg.p2 ? (std::size_t)s.cfg.p2 : mt2;
+    if (!table) throw std::invalid_argument("hybrid_solve: band stage needs a scope table");
+    s.plan = std::make_unique<pftg_plan>();
+    s.plan->a1 = plan_1d(s.wr, mt1, p1, s.cfg.eps_pft, table->t);
+    s.plan->a2 = plan_1d(s.wc, mt2, p2, s.cfg.eps_pft, table->t);
+    const PftDev<R>& pd = plan_dev<R>(*s.plan);
+    const long long mb = 4LL * mt1 * mt2;
+    PFTG_CUDA(cudaMalloc(&s.dcrop, sizeof(R) * mb * s.npos));
+    k_crop_real<R><<<148 * 16, 256, 0, s.st>>>(static_cast<const R*>(s.d), static_cast<R*>(s.dcrop), (int)s.wr,
+                                               (int)s.wc, (int)mt1, (int)mt2, (long long)s.npos);
+    PFTG_LAUNCH_CHECK();
+    const std::size_t gsz = (std::size_t)pd.p1 * pd.r1 * pd.M2;
+    PFTG_CUDA(cudaMalloc(&s.G, sizeof(Cx<R>) * gsz));
+    PFTG_CUDA(cudaMalloc(&s.Gt, sizeof(Cx<R>) * gsz));
+  }
+  double fnrm, pnrm;
+  bool f1, f2;
+  norm_finite<R>(s, s.frame, fn, &fnrm, &f1);
+  norm_finite<R>(s, s.probe, pn, &pnrm, &f2);
+  // solver.cpp:227-228
+  s.probe_guard = 1e6 * std::max(pnrm, 1e-300);
+  s.frame_guard = 1e6 * std::max(fnrm, 1e-300);
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PFTG_OK;
+  } catch (const cuda_error& e) {
+    set_error(e.what());
+    return PFTG_ECUDA;
+  } catch (const std::invalid_argument& e) {
+    set_error(std::string("invalid_argument: ") + e.what());
+    return PFTG_EINVAL;
+  } catch (const std::out_of_range& e) {
+    set_error(std::string("out_of_range: ") + e.what());
+    return PFTG_ERANGE;
+  } catch (const std::logic_error& e) {
+    set_error(std::string("logic_error: ") + e.what());
+    return PFTG_ELOGIC;
+  } catch (const std::exception& e) {
+    set_error(std::string("runtime_error: ") + e.what());
+    return PFTG_ERUNTIME;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int pftg_solver_create(int dtype, const void* frame, size_t fr, size_t fc, const void* probe, size_t wr, size_t wc,
+                       const int64_t* offsets, size_t npos, const void* d, const pftg_solver_config* cfg,
+                       const pftg_table* table, pftg_solver** out) {
+  return guarded([&] {
+    if (dtype != PFTG_C64 && dtype != PFTG_C128) throw std::invalid_argument("pftg: bad dtype");
+    if (!cfg) throw std::invalid_argument("hybrid_solve: null config");
+    if (cfg->pft_sweeps < 0 || cfg->fft_sweeps < 0) throw std::invalid_argument("hybrid_solve: negative sweep budget");
+    if (npos == 0) throw std::invalid_argument("hybrid_solve: no scan positions");
+    if (wr > fr || wc > fc) throw std::invalid_argument("hybrid_solve: window larger than frame");
+    ensure_device();
+    auto s = std::make_unique<pftg_solver>();
+    s->dtype = dtype;
+    s->fr = fr;
+    s->fc = fc;
+    s->wr = wr;
+    s->wc = wc;
+    s->npos = npos;
+    s->cfg = *cfg;
+    if (dtype == PFTG_C64) create<float>(*s, frame, probe, offsets, d, table);
+    else create<double>(*s, frame, probe, offsets, d, table);
+    *out = s.release();
+  });
+}
+
+int pftg_solver_run(pftg_solver* s, int max_sweeps) {
+  return guarded([&] {
+    if (!s) throw std::invalid_argument("pftg: null solver");
+    if (s->dtype == PFTG_C64) run<float>(*s, max_sweeps);
+    else run<double>(*s, max_sweeps);
+  });
+}
+
+int pftg_solver_trace(const pftg_solver* s, double* objective, double* wall_s, int* sweeps_run, int* flags) {
+  return guarded([&] {
+    if (!s) throw std::invalid_argument("pftg: null solver");
+    for (std::size_t i = 0; i < s->objective.size(); ++i) {
+      if (objective) objective[i] = s->objective[i];
+      if (wall_s) wall_s[i] = s->wall[i];
+    }
+    if (sweeps_run) *sweeps_run = s->sweeps_run;
+    if (flags) *flags = s->flags;
+  });
+}
+
+int pftg_solver_result(const pftg_solver* s, void* frame, void* probe) {
+  return guarded([&] {
+    if (!s) throw std::invalid_argument("pftg: null solver");
+    const std::size_t cs = s->dtype == PFTG_C64 ? 8 : 16;
+    PFTG_CUDA(cudaStreamSynchronize(s->st));
+    if (frame) PFTG_CUDA(cudaMemcpy(frame, s->frame, cs * s->fr * s->fc, cudaMemcpyDeviceToHost));
+    if (probe) PFTG_CUDA(cudaMemcpy(probe, s->probe, cs * s->wr * s->wc, cudaMemcpyDeviceToHost));
+  });
+}
+
+int pftg_solver_device_state(const pftg_solver* s, void** frame, void** probe) {
+  return guarded([&] {
+    if (!s) throw std::invalid_argument("pftg: null solver");
+    if (frame) *frame = s->frame;
+    if (probe) *probe = s->probe;
+  });
+}
+
+void pftg_solver_free(pftg_solver* s) { delete s; }
+
+}  // extern "C"

@@ -1,0 +1,237 @@
+"""Python mirror of the reference's ``ptycho::pft`` / ``ptycho`` transform API
+over libpftg (include/pftg.h).
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/core/include/ptycho/{pft,fft,minimax}.hpp:
+
+=========================  ====================================================
+reference                  here
+=========================  ====================================================
+minimax::ScopeTable::load  ``ScopeTable.load(path)``            (minimax.hpp:50)
+ScopeTable::min_degree     ``ScopeTable.min_degree(eps, xi)``   (minimax.hpp:59)
+pft::pft_plan_2d           ``pft_plan_2d(n1, n2, mt1, mt2, p1, p2, eps, table)`` (pft.hpp:49)
+pft::load_plan_2d/save     ``PftPlan2D.load(path)`` / ``plan.save(path)`` (pft.hpp:60-63)
+pft::pft_apply_2d          ``pft_apply_2d(plan, z)``            (pft.hpp:53)
+pft::pft_adjoint_2d        ``pft_adjoint_2d(plan, band)``       (pft.hpp:57)
+fast_fft2 / fast_ifft2     ``fast_fft2(z)`` / ``fast_ifft2(z)`` (fft.hpp:18-19)
+crop_centered              ``crop_centered(d, mt1, mt2)``       (fft.hpp:30)
+=========================  ====================================================
+
+Arrays are ``torch`` tensors on a CUDA device (complex64 or complex128; the
+dtype selects the kernel precision) with optional leading batch dimensions;
+``pft_apply_2d`` / ``pft_adjoint_2d`` additionally accept host numpy arrays
+(routed through the pipelined host-buffer C-ABI entry points). Shape errors
+raise ValueError, like the reference's std::invalid_argument.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import PFTG_C64, PFTG_C128, check, lib
+
+DATA = Path(__file__).resolve().parent / "data"
+DEFAULT_TABLE = DATA / "scope_table_v1.txt"
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dtype_code(t) -> int:
+    if t.dtype in (torch.complex64, np.complex64):
+        return PFTG_C64
+    if t.dtype in (torch.complex128, np.complex128):
+        return PFTG_C128
+    raise TypeError(f"expected complex64 or complex128, got {t.dtype}")
+
+
+def _real_of(t: torch.Tensor) -> torch.dtype:
+    return torch.float32 if t.dtype == torch.complex64 else torch.float64
+
+
+def _dev(t):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("expected a CUDA torch tensor")
+    return t.contiguous()
+
+
+def _ptr(t: torch.Tensor):
+    return C.c_void_p(t.data_ptr())
+
+
+class ScopeTable:
+    """minimax::ScopeTable loaded from the ``pft-scope-table v1`` text format."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle)
+
+    @classmethod
+    def load(cls, path=DEFAULT_TABLE) -> "ScopeTable":
+        h = C.c_void_p()
+        check(lib().pftg_table_load(str(path).encode(), C.byref(h)))
+        return cls(h.value)
+
+    def min_degree(self, eps: float, target_scope: float) -> int:
+        r = C.c_int()
+        check(lib().pftg_table_min_degree(self._h, eps, target_scope, C.byref(r)))
+        return r.value
+
+    def __del__(self):
+        try:
+            lib().pftg_table_free(self._h)
+        except Exception:
+            pass
+
+
+class PftPlan2D:
+    """pft::PftPlan2D: immutable plan; device tables are uploaded on first use."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle)
+        info = np.zeros(10, np.int64)
+        check(lib().pftg_plan_info(self._h, info.ctypes.data_as(C.POINTER(C.c_int64))))
+        (self.n1, self.p1, self.q1, self.mt1, self.r1,
+         self.n2, self.p2, self.q2, self.mt2, self.r2) = (int(v) for v in info)
+
+    @property
+    def band_shape(self):
+        return (2 * self.mt1, 2 * self.mt2)
+
+    @property
+    def field_shape(self):
+        return (self.n1, self.n2)
+
+    @classmethod
+    def load(cls, path) -> "PftPlan2D":
+        h = C.c_void_p()
+        check(lib().pftg_plan_load(str(path).encode(), C.byref(h)))
+        return cls(h.value)
+
+    def save(self, path) -> None:
+        check(lib().pftg_plan_save(self._h, str(path).encode()))
+
+    def tables(self, axis: int):
+        """(B, W) of one axis as complex128 numpy arrays (pft.hpp:29-30)."""
+        q, r, mt = (self.q1, self.r1, self.mt1) if axis == 1 else (self.q2, self.r2, self.mt2)
+        B = np.zeros((q, r), np.complex128)
+        W = np.zeros((2 * mt + 1, r), np.complex128)
+        check(lib().pftg_plan_tables(self._h, axis, B.ctypes.data_as(C.POINTER(C.c_double)),
+                                     W.ctypes.data_as(C.POINTER(C.c_double))))
+        return B, W
+
+    def __del__(self):
+        try:
+            lib().pftg_plan_free(self._h)
+        except Exception:
+            pass
+
+
+def pft_plan_2d(n1, n2, mt1, mt2, p1, p2, eps, table: ScopeTable | None = None) -> PftPlan2D:
+    """pft::pft_plan_2d (pft.hpp:49-51; pft.cpp:33-76,103-112)."""
+    table = table or ScopeTable.load()
+    h = C.c_void_p()
+    check(lib().pftg_plan_2d(table._h, n1, n2, mt1, mt2, p1, p2, eps, C.byref(h)))
+    return PftPlan2D(h.value)
+
+
+def _batch(x, tail):
+    if tuple(x.shape[-2:]) != tuple(tail):
+        raise ValueError(f"shape must end in {tuple(tail)}, got {tuple(x.shape)}")
+    b = 1
+    for s in x.shape[:-2]:
+        b *= int(s)
+    return b
+
+
+def pft_apply_2d(plan: PftPlan2D, z):
+    """pft::pft_apply_2d: band of the 2-D DFT, DC at (mt1, mt2) (pft.hpp:53)."""
+    if isinstance(z, np.ndarray):
+        if tuple(z.shape[-2:]) != plan.field_shape:
+            raise ValueError("pft_apply_2d: z shape must match the plan")
+        z = np.ascontiguousarray(z)
+        b = _batch(z, plan.field_shape)
+        out = np.empty(z.shape[:-2] + plan.band_shape, z.dtype)
+        check(lib().pftg_apply_2d_host(plan._h, _dtype_code(z), z.ctypes.data, out.ctypes.data, b))
+        return out
+    z = _dev(z)
+    if tuple(z.shape[-2:]) != plan.field_shape:
+        raise ValueError("pft_apply_2d: z shape must match the plan")
+    b = _batch(z, plan.field_shape)
+    out = torch.empty(z.shape[:-2] + plan.band_shape, dtype=z.dtype, device=z.device)
+    check(lib().pftg_apply_2d_dev(plan._h, _dtype_code(z), _ptr(z), _ptr(out), b, _stream()))
+    return out
+
+
+def pft_adjoint_2d(plan: PftPlan2D, band):
+    """pft::pft_adjoint_2d: exact adjoint of pft_apply_2d (pft.hpp:57)."""
+    if isinstance(band, np.ndarray):
+        if tuple(band.shape[-2:]) != plan.band_shape:
+            raise ValueError("pft_adjoint_2d: band shape must match the plan")
+        band = np.ascontiguousarray(band)
+        b = _batch(band, plan.band_shape)
+        out = np.empty(band.shape[:-2] + plan.field_shape, band.dtype)
+        check(lib().pftg_adjoint_2d_host(plan._h, _dtype_code(band), band.ctypes.data,
+                                         out.ctypes.data, b))
+        return out
+    band = _dev(band)
+    if tuple(band.shape[-2:]) != plan.band_shape:
+        raise ValueError("pft_adjoint_2d: band shape must match the plan")
+    b = _batch(band, plan.band_shape)
+    out = torch.empty(band.shape[:-2] + plan.field_shape, dtype=band.dtype, device=band.device)
+    check(lib().pftg_adjoint_2d_dev(plan._h, _dtype_code(band), _ptr(band), _ptr(out), b,
+                                    _stream()))
+    return out
+
+
+def band_residual(plan: PftPlan2D, exit_wave, d_crop):
+    """ptycho::band_residual (solver.hpp:63): A*(A x - d .* exp(i arg(A x)))."""
+    x = _dev(exit_wave)
+    if tuple(x.shape[-2:]) != plan.field_shape:
+        raise ValueError("pft_apply_2d: z shape must match the plan")
+    d = _dev(d_crop).to(_real_of(x))
+    if tuple(d.shape[-2:]) != plan.band_shape or d.numel() // (4 * plan.mt1 * plan.mt2) != \
+            _batch(x, plan.field_shape):
+        raise ValueError("band_residual: cropped measurement shape mismatch")
+    out = torch.empty_like(x)
+    check(lib().pftg_band_residual_dev(plan._h, _dtype_code(x), _ptr(x), _ptr(d), _ptr(out),
+                                       _batch(x, plan.field_shape), _stream()))
+    return out
+
+
+def _fft2(z, inverse):
+    z = _dev(z)
+    if z.dim() < 2 or z.numel() == 0:
+        raise ValueError("fast_fft2: empty field")
+    rows, cols = z.shape[-2:]
+    out = torch.empty_like(z)
+    check(lib().pftg_fft2_dev(_dtype_code(z), _ptr(z), _ptr(out), rows, cols,
+                              _batch(z, (rows, cols)), int(inverse), _stream()))
+    return out
+
+
+def fast_fft2(z):
+    """fast_fft2 (fft.hpp:18): unnormalized forward 2-D DFT."""
+    return _fft2(z, False)
+
+
+def fast_ifft2(z):
+    """fast_ifft2 (fft.hpp:19): inverse 2-D DFT with the 1/n factor."""
+    return _fft2(z, True)
+
+
+def crop_centered(spectrum, mt1, mt2):
+    """crop_centered(RealField) (fft.hpp:30; fft.cpp:206-232)."""
+    s = _dev(spectrum)
+    rows, cols = s.shape[-2:]
+    out = torch.empty(s.shape[:-2] + (2 * mt1, 2 * mt2), dtype=s.dtype, device=s.device)
+    code = PFTG_C64 if s.dtype == torch.float32 else PFTG_C128
+    if s.dtype not in (torch.float32, torch.float64):
+        raise TypeError("crop_centered: real float32/float64 spectrum expected")
+    check(lib().pftg_crop_centered_dev(code, _ptr(s), _ptr(out), rows, cols, mt1, mt2,
+                                       _batch(s, (rows, cols)), _stream()))
+    return out

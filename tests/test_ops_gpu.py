@@ -1,0 +1,166 @@
+"""GPU parity of the full-FFT / projection / update / solver operators against
+the reference (oracle/_ref: verbatim fft.cpp, solver.cpp, scan.cpp, simulate.cpp)."""
+import numpy as np
+import pytest
+
+from conftest import DATA, cnormal, rel_l2
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+P = pytest.importorskip("paper_2408_03532_b200")
+
+
+@pytest.mark.parametrize("shape", [(64, 64), (256, 256), (512, 512), (32, 128), (8, 16)])
+def test_fft2_ifft2_c128(ref, shape):
+    rng = np.random.default_rng(11)
+    z = cnormal(rng, (2,) + shape)
+    f = P.fast_fft2(torch.from_numpy(z).cuda()).cpu().numpy()
+    fi = P.fast_ifft2(torch.from_numpy(z).cuda()).cpu().numpy()
+    for b in range(2):
+        assert rel_l2(f[b], ref.fast_fft2(z[b])) <= 1e-13
+        assert rel_l2(fi[b], ref.fast_ifft2(z[b])) <= 1e-13
+
+
+def test_fft2_c64():
+    rng = np.random.default_rng(12)
+    z = cnormal(rng, (3, 512, 512), np.complex64)
+    f = P.fast_fft2(torch.from_numpy(z).cuda()).cpu().numpy()
+    assert rel_l2(f, np.fft.fft2(z.astype(np.complex128))) <= 1e-6
+
+
+def test_fft_known_answers():
+    z = np.zeros((4, 4), np.complex128)
+    z[0, 0] = 1
+    assert np.allclose(P.fast_fft2(torch.from_numpy(z).cuda()).cpu().numpy(), 1)
+    c = np.full((4, 4), 2.5 + 0j)
+    f = P.fast_fft2(torch.from_numpy(c).cuda()).cpu().numpy()
+    assert abs(f[0, 0] - 40) < 1e-12 and np.abs(f.ravel()[1:]).max() < 1e-12
+
+
+@pytest.mark.parametrize("dtype,tol", [(np.complex128, 1e-12), (np.complex64, 1e-5)])
+def test_project_modulus(ref, dtype, tol):
+    rng = np.random.default_rng(13)
+    x = cnormal(rng, (256, 256), dtype)
+    d = np.abs(cnormal(rng, (256, 256))) * 10
+    d = d.astype(np.float64 if dtype == np.complex128 else np.float32)
+    got = P.project_modulus(torch.from_numpy(x).cuda(), torch.from_numpy(d).cuda()).cpu().numpy()
+    want = ref.project_modulus(x.astype(np.complex128), d.astype(np.float64))
+    assert rel_l2(got, want) <= tol
+
+
+def test_project_modulus_fixed_point_and_zero():
+    rng = np.random.default_rng(14)
+    x = cnormal(rng, (64, 64))
+    d = np.abs(np.fft.fft2(x))
+    got = P.project_modulus(torch.from_numpy(x).cuda(), torch.from_numpy(d).cuda()).cpu().numpy()
+    assert rel_l2(got, x) <= 1e-10
+    z = np.zeros((64, 64), np.complex128)
+    got0 = P.project_modulus(torch.from_numpy(z).cuda(), torch.from_numpy(d).cuda()).cpu().numpy()
+    assert rel_l2(got0, np.fft.ifft2(d)) <= 1e-12
+
+
+@pytest.mark.parametrize("dtype,tol", [(np.complex128, 1e-10), (np.complex64, 1e-5)])
+def test_band_residual(ref, dtype, tol):
+    g = P.pft_plan_2d(256, 256, 32, 32, 32, 32, 1e-3)
+    r = ref.RefPlan.create(DATA / "scope_table_v1.txt", 256, 256, 32, 32, 32, 32, 1e-3)
+    rng = np.random.default_rng(15)
+    x = cnormal(rng, (256, 256), dtype)
+    dcrop = (np.abs(cnormal(rng, (64, 64))) * 50).astype(np.float64)
+    got = P.band_residual(g, torch.from_numpy(x).cuda(), torch.from_numpy(dcrop).cuda())
+    want = r.band_residual(x.astype(np.complex128), dcrop.astype(np.float32 if dtype == np.complex64 else np.float64))
+    assert rel_l2(got.cpu().numpy(), want) <= tol
+
+
+def test_updates_and_windows(ref):
+    rng = np.random.default_rng(16)
+    z, pr, pj = (cnormal(rng, (32, 32)) for _ in range(3))
+    zt = torch.from_numpy(z.copy()).cuda()
+    P.pie_object_update(zt, torch.from_numpy(pr).cuda(), torch.from_numpy(pj).cuda(), 0.7)
+    assert rel_l2(zt.cpu().numpy(), ref.pie_object_update(z, pr, pj, 0.7)) <= 1e-15
+    pt = torch.from_numpy(pr.copy()).cuda()
+    P.epie_probe_update(pt, torch.from_numpy(z).cuda(), torch.from_numpy(pj).cuda(), 0.3, True)
+    assert rel_l2(pt.cpu().numpy(), ref.epie_probe_update(pr, z, pj, 0.3)) <= 1e-15
+    with pytest.raises(RuntimeError):
+        P.epie_probe_update(pt, torch.from_numpy(z).cuda(), torch.from_numpy(pj).cuda(), 0.3, False)
+    frame = cnormal(rng, (100, 90))
+    offs = np.array([[0, 0], [3, 7], [68, 58]])
+    pat = P.window_slice(torch.from_numpy(frame).cuda(), offs, 32, 32).cpu().numpy()
+    for k, (r0, c0) in enumerate(offs):
+        assert np.array_equal(pat[k], frame[r0:r0 + 32, c0:c0 + 32])
+    ft = torch.from_numpy(frame.copy()).cuda()
+    P.set_window(ft, (3, 7), torch.from_numpy(z).cuda())
+    f2 = frame.copy()
+    f2[3:35, 7:39] = z
+    assert np.array_equal(ft.cpu().numpy(), f2)
+
+
+def test_objective_value(ref):
+    rng = np.random.default_rng(17)
+    frame = cnormal(rng, (160, 160))
+    probe = cnormal(rng, (64, 64))
+    offs = np.array([[r, c] for r in (0, 48, 96) for c in (0, 48, 96)])
+    d = np.abs(cnormal(rng, (9, 64, 64))) * 30
+    got = P.objective_value(torch.from_numpy(frame).cuda(), torch.from_numpy(probe).cuda(), offs,
+                            torch.from_numpy(d).cuda())
+    want = ref.objective_value(frame, probe, offs, d)
+    assert abs(got - want) / want <= 1e-12
+
+
+def _small_problem(rng, n=128, w=64, npos=9):
+    obj = (0.5 + 0.5 * rng.random((n, n))) * np.exp(1j * rng.uniform(-1, 1, (n, n)))
+    yy, xx = np.mgrid[0:w, 0:w] - (w - 1) / 2
+    probe = np.exp(-(xx ** 2 + yy ** 2) / (2 * (w / 5) ** 2)) * np.exp(1j * 0.3 * (xx ** 2 + yy ** 2) / w ** 2)
+    k = int(round(np.sqrt(npos)))
+    pos = np.linspace(0, n - w, k).round().astype(int)
+    offs = np.array([[r, c] for r in pos for c in pos], np.int64)
+    return obj.astype(np.complex128), probe.astype(np.complex128), offs
+
+
+@pytest.mark.parametrize("blind", [False, True])
+def test_hybrid_solve_c128_matches_reference(ref, blind):
+    rng = np.random.default_rng(18)
+    obj, probe, offs = _small_problem(rng)
+    d = ref.simulate(obj, probe, offs)
+    init = np.exp(1j * 0.1 * rng.standard_normal(obj.shape)) * 0.8
+    pinit = probe * 0.9
+    kw = dict(pft_sweeps=2, fft_sweeps=2, beta=1.0, gamma=1.0, beta_pft=1.0 / 64 ** 2,
+              gamma_pft=1.0 / 64 ** 2, eps_pft=1e-3, blind=blind)
+    f_ref, p_ref, obj_ref, _, _ = ref.hybrid_solve(init, pinit, offs, d, table_path=DATA / "scope_table_v1.txt",
+                                                   **kw)
+    cfg = P.SolverConfig(**kw)
+    res = P.hybrid_solve(d, offs, pinit, init, cfg, dtype=np.complex128)
+    assert res.sweeps_run == 4
+    assert rel_l2(res.frame, f_ref) <= 1e-9
+    assert rel_l2(res.probe, p_ref) <= 1e-9
+    assert np.allclose(res.objective, obj_ref, rtol=1e-8)
+
+
+def test_hybrid_solve_c64_tracks_reference(ref):
+    rng = np.random.default_rng(19)
+    obj, probe, offs = _small_problem(rng)
+    d = ref.simulate(obj, probe, offs)
+    init = np.exp(1j * 0.1 * rng.standard_normal(obj.shape)) * 0.8
+    kw = dict(pft_sweeps=2, fft_sweeps=3, beta=1.0, gamma=1.0, beta_pft=1.0 / 64 ** 2,
+              gamma_pft=1.0 / 64 ** 2, eps_pft=1e-3, blind=True)
+    f_ref, p_ref, obj_ref, _, _ = ref.hybrid_solve(init, probe, offs, d, table_path=DATA / "scope_table_v1.txt",
+                                                   **kw)
+    res = P.hybrid_solve(d, offs, probe, init, P.SolverConfig(**kw), dtype=np.complex64)
+    assert rel_l2(res.frame, f_ref) <= 1e-4
+    assert rel_l2(res.probe, p_ref) <= 1e-4
+
+
+def test_evaluator_band_and_fft(ref):
+    rng = np.random.default_rng(20)
+    obj, probe, offs = _small_problem(rng, n=160, w=64, npos=9)
+    d = ref.simulate(obj, probe, offs)
+    g = P.pft_plan_2d(64, 64, 8, 8, 8, 8, 1e-3)
+    r = ref.RefPlan.create(DATA / "scope_table_v1.txt", 64, 64, 8, 8, 8, 8, 1e-3)
+    dcrop = np.stack([ref.crop_centered(dj, 8, 8) for dj in d])
+    fs, bs = P.evaluate(torch.from_numpy(obj).cuda(), torch.from_numpy(probe).cuda(), offs,
+                        torch.from_numpy(d).cuda(), plan=g, d_crop=torch.from_numpy(dcrop).cuda())
+    assert abs(fs / 9 - ref.objective_value(obj, probe, offs, d)) <= 1e-10 * max(1.0, fs)
+    want_b = 0.0
+    for j, (r0, c0) in enumerate(offs):
+        ex = probe * obj[r0:r0 + 64, c0:c0 + 64]
+        want_b += np.sum((np.abs(r.apply(ex)) - dcrop[j]) ** 2)
+    assert abs(bs - want_b) <= 1e-9 * max(want_b, 1e-30) + 1e-18
