@@ -198,6 +198,13 @@ void upload(const pftg_plan& p, DevTables<R>& t, PftDev<R>& pd) {
   pd.W2t = t.W2t;
   pd.tw1 = t.tw1;
   pd.tw2 = t.tw2;
+  pd.nb = choose_nb(pd);
+  if (p.hbv1.empty()) {
+    p.hbv1 = b_values<double>(p.a1);
+    p.hbv2 = b_values<double>(p.a2);
+  }
+  pd.hBv1 = p.hbv1.data();
+  pd.hBv2 = p.hbv2.data();
 }
 
 template <class R>
@@ -247,6 +254,11 @@ namespace {
 template <class R>
 using Cx = typename CT<R>::C;
 
+// 16-byte column pairs are safe: 16-byte aligned base, even row length and batch stride.
+bool vec_ok(const void* p, long long ld, long long bstride) {
+  return (reinterpret_cast<std::uintptr_t>(p) % 16 == 0) && ld % 2 == 0 && bstride % 2 == 0;
+}
+
 // Fields per chunk so the chunk's G workspace (~p1*r1*M2 complex per field)
 // stays well inside L2 between the rows and cols passes.
 template <class R>
@@ -265,7 +277,8 @@ void apply_dev(const pftg_plan* plan, const void* z, void* band, std::size_t bat
   const std::size_t nz = (std::size_t)pd.n1 * pd.n2, nb = (std::size_t)pd.M1 * pd.M2;
   for (std::size_t b0 = 0; b0 < batch; b0 += chunk) {
     const int nbat = static_cast<int>(std::min(chunk, batch - b0));
-    Src<R> src{static_cast<const Cx<R>*>(z) + b0 * nz, pd.n2, (long long)nz, nullptr, nullptr};
+    Src<R> src{static_cast<const Cx<R>*>(z) + b0 * nz, pd.n2, (long long)nz, nullptr, nullptr,
+               vec_ok(z, pd.n2, nz)};
     launch_fwd_rows<R>(pd, src, G.as<Cx<R>>(), nbat, st);
     launch_fwd_cols<R>(pd, 0, G.as<Cx<R>>(), static_cast<Cx<R>*>(band) + b0 * nb, nullptr, 0, nullptr, nullptr,
                        nbat, st);
@@ -284,6 +297,7 @@ void adjoint_dev(const pftg_plan* plan, const void* band, void* z, std::size_t b
     launch_adj_cols<R>(pd, static_cast<const Cx<R>*>(band) + b0 * nb, G.as<Cx<R>>(), nbat, st);
     EpiArgs ep{};
     ep.out = static_cast<Cx<R>*>(z) + b0 * nz;
+    ep.vec_ok = vec_ok(z, pd.n2, nz);
     launch_adj_rows<R>(pd, 0, G.as<Cx<R>>(), ep, nbat, st);
   }
 }
@@ -298,12 +312,14 @@ void band_residual_dev(const pftg_plan* plan, const void* exit_wave, const void*
   const std::size_t nz = (std::size_t)pd.n1 * pd.n2, nb = (std::size_t)pd.M1 * pd.M2;
   for (std::size_t b0 = 0; b0 < batch; b0 += chunk) {
     const int nbat = static_cast<int>(std::min(chunk, batch - b0));
-    Src<R> src{static_cast<const Cx<R>*>(exit_wave) + b0 * nz, pd.n2, (long long)nz, nullptr, nullptr};
+    Src<R> src{static_cast<const Cx<R>*>(exit_wave) + b0 * nz, pd.n2, (long long)nz, nullptr, nullptr,
+               vec_ok(exit_wave, pd.n2, nz)};
     launch_fwd_rows<R>(pd, src, G.as<Cx<R>>(), nbat, st);
     launch_fwd_cols<R>(pd, 1, G.as<Cx<R>>(), nullptr, static_cast<const R*>(dcrop) + b0 * nb, (long long)nb,
                        Gt.as<Cx<R>>(), nullptr, nbat, st);
     EpiArgs ep{};
     ep.out = static_cast<Cx<R>*>(out) + b0 * nz;
+    ep.vec_ok = vec_ok(out, pd.n2, nz);
     launch_adj_rows<R>(pd, 0, Gt.as<Cx<R>>(), ep, nbat, st);
   }
 }
@@ -497,7 +513,9 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
     launch_fft_cols<R>(COL_EVAL, n1, n2, X.as<Cx<R>>(), n, static_cast<const R*>(d) + (pb + c0) * n, n, nullptr, 1,
                        -1, part.as<double>() + c0 * nstrips, nb, st);
     if (pd) {
-      Src<R> s2{static_cast<const Cx<R>*>(frame), (long long)fc, 0, o, static_cast<const Cx<R>*>(probe)};
+      bool evec = vec_ok(frame, (long long)fc, 0) && vec_ok(probe, n2, 0);
+      for (std::size_t j = c0; j < c0 + nb; ++j) evec = evec && (offs[j] % 2 == 0);
+      Src<R> s2{static_cast<const Cx<R>*>(frame), (long long)fc, 0, o, static_cast<const Cx<R>*>(probe), evec};
       launch_fwd_rows<R>(*pd, s2, G->as<Cx<R>>(), nb, st);
       const long long mb = (long long)pd->M1 * pd->M2;
       launch_fwd_cols<R>(*pd, 2, G->as<Cx<R>>(), nullptr, static_cast<const R*>(dcrop) + (pb + c0) * mb, mb,

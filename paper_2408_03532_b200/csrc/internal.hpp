@@ -50,6 +50,7 @@ struct pftg_plan {
   mutable pftg::DevTables<double> t64;
   mutable pftg::PftDev<float> pd32{};
   mutable pftg::PftDev<double> pd64{};
+  mutable std::vector<double> hbv1, hbv2;  // nonzero parts of B1, B2 (host; kernel-parameter tables)
   ~pftg_plan();
 };
 

@@ -34,12 +34,15 @@ struct PftDev {
   using C = typename CT<R>::C;
   int n1, n2, p1, p2, q1, q2, mt1, mt2, r1, r2, M1, M2;
   int lp1, lp2;             // log2 p
+  int nb;                   // band columns per cols-pass CTA (fits shared memory)
   const R* Bv1;             // [q1][r1] nonzero part of B1 (pft.cpp:52-61)
   const R* Bv2;             // [q2][r2]
   const C* W1t;             // [r1][M1] = W1[a][j1] for a < 2*mt1 (pft.cpp:63-74)
   const C* W2t;             // [r2][M2]
   const C* tw1;             // exp(-2 pi i k / p1), k < p1/2
   const C* tw2;
+  const double* hBv1;       // HOST copies of Bv1/Bv2 (kernel-parameter B tables of the
+  const double* hBv2;       // specialized kernels, pft_fast.cuh); never dereferenced on device
 };
 
 // Where the rows pass reads its field: base + off(f) + l*ld + c, optionally
@@ -53,6 +56,7 @@ struct Src {
   long long bstride;
   const long long* offs;
   const C* probe;
+  int vec_ok;  // host-verified: base, ld, offsets and probe allow 16-byte column pairs
 };
 
 // ---------------------------------------------------------------- smem sizes
@@ -66,16 +70,12 @@ __host__ inline size_t rows_smem_bytes(const PftDev<R>& p) {
   b += sizeof(C) * (size_t)p.r2 * p.M2;                // W2t
   b += sizeof(C) * (size_t)(p.p2 / 2 + 1);             // tw2
   b += sizeof(R) * (size_t)(p.q1 * p.r1 + p.q2 * p.r2);  // Bv1, Bv2
-  b += sizeof(C) * (size_t)p.r1 * p.M2;                // Gk (adjoint input block)
   return (b + 15) & ~size_t(15);
 }
 
-__host__ __device__ inline int strip_nb(int M2) { return M2 < 16 ? M2 : 16; }
-
 template <class R>
-__host__ inline size_t cols_smem_bytes(const PftDev<R>& p) {
+__host__ inline size_t cols_smem_bytes(const PftDev<R>& p, int nb) {
   using C = typename CT<R>::C;
-  const int nb = strip_nb(p.M2);
   size_t b = 0;
   b += sizeof(C) * (size_t)p.r1 * nb * (p.p1 + 1);  // Gs
   b += sizeof(C) * (size_t)p.M1 * (nb + 1);        // band strip
@@ -83,6 +83,19 @@ __host__ inline size_t cols_smem_bytes(const PftDev<R>& p) {
   b += sizeof(C) * (size_t)(p.p1 / 2 + 1);         // tw1
   b += sizeof(double) * 64;                        // reduction scratch
   return (b + 15) & ~size_t(15);
+}
+
+template <class R>
+__host__ inline size_t cols_smem_bytes(const PftDev<R>& p) {
+  return cols_smem_bytes(p, p.nb);
+}
+
+// Widest strip (<= 16 band columns) whose working set fits in shared memory.
+template <class R>
+__host__ inline int choose_nb(const PftDev<R>& p) {
+  int nb = p.M2 < 16 ? p.M2 : 16;
+  while (nb > 1 && cols_smem_bytes(p, nb) > 200 * 1024) nb /= 2;
+  return nb;
 }
 
 // ------------------------------------------------------------ rows pass core
@@ -154,7 +167,6 @@ struct RowsSmem {
   C* tw2s;
   R* Bv1s;
   R* Bv2s;
-  C* Gk;
   __device__ RowsSmem(unsigned char* raw, const PftDev<R>& pl) {
     C* c = reinterpret_cast<C*>(raw);
     T = c;
@@ -163,8 +175,6 @@ struct RowsSmem {
     c += (size_t)pl.r2 * pl.M2;
     tw2s = c;
     c += pl.p2 / 2 + 1;
-    Gk = c;
-    c += (size_t)pl.r1 * pl.M2;
     Bv1s = reinterpret_cast<R*>(c);
     Bv2s = Bv1s + pl.q1 * pl.r1;
   }
@@ -264,17 +274,25 @@ __device__ __forceinline__ void cols_load_tables(const PftDev<R>& pl, ColsSmem<R
 }
 
 // Gs <- G[f][k1][j1][b0 + bb] for bb < nbv (coalesced along bb).
+// One thread per (j1, k1) row segment of the strip, k1 fastest across threads:
+// each thread reads its nb contiguous values (full 128-byte segments), and the
+// shared-memory writes of a warp hit consecutive k1 (conflict-free). nb <= 16.
 template <class R>
 __device__ __forceinline__ void cols_load_g(const PftDev<R>& pl, ColsSmem<R>& sm,
                                             const typename CT<R>::C* Gf, int b0, int nb, int nbv) {
-  const int total = pl.p1 * pl.r1 * nb;
-  for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    const int bb = i % nb;
-    const int kj = i / nb;  // k1 * r1 + j1
-    const int j1 = kj % pl.r1, k1 = kj / pl.r1;
-    typename CT<R>::C v = czero<typename CT<R>::C>();
-    if (bb < nbv) v = Gf[(size_t)kj * pl.M2 + b0 + bb];
-    sm.Gs[((size_t)j1 * nb + bb) * (pl.p1 + 1) + k1] = v;
+  using C = typename CT<R>::C;
+  const int rows = pl.p1 * pl.r1;
+  const int ld = pl.p1 + 1;
+  for (int t = threadIdx.x; t < rows; t += blockDim.x) {
+    const int k1 = t & (pl.p1 - 1), j1 = t >> pl.lp1;
+    const C* src = Gf + ((size_t)k1 * pl.r1 + j1) * pl.M2 + b0;
+    C* dst = sm.Gs + (size_t)j1 * nb * ld + k1;
+    C v[16];
+#pragma unroll
+    for (int bb = 0; bb < 16; ++bb) v[bb] = (bb < nbv) ? src[bb] : czero<C>();
+#pragma unroll
+    for (int bb = 0; bb < 16; ++bb)
+      if (bb < nb) dst[(size_t)bb * ld] = v[bb];
   }
 }
 
@@ -358,26 +376,37 @@ __device__ __forceinline__ void cols_adjoint(const PftDev<R>& pl, ColsSmem<R>& s
 template <class R>
 __device__ __forceinline__ void cols_store_g(const PftDev<R>& pl, ColsSmem<R>& sm,
                                              typename CT<R>::C* Gf, int b0, int nb, int nbv) {
-  const int total = pl.p1 * pl.r1 * nb;
-  for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    const int bb = i % nb;
-    const int kj = i / nb;
-    const int j1 = kj % pl.r1, k1 = kj / pl.r1;
-    if (bb < nbv) Gf[(size_t)kj * pl.M2 + b0 + bb] = sm.Gs[((size_t)j1 * nb + bb) * (pl.p1 + 1) + k1];
+  using C = typename CT<R>::C;
+  const int rows = pl.p1 * pl.r1;
+  const int ld = pl.p1 + 1;
+  for (int t = threadIdx.x; t < rows; t += blockDim.x) {
+    const int k1 = t & (pl.p1 - 1), j1 = t >> pl.lp1;
+    C* dst = Gf + ((size_t)k1 * pl.r1 + j1) * pl.M2 + b0;
+    const C* src = sm.Gs + (size_t)j1 * nb * ld + k1;
+#pragma unroll
+    for (int bb = 0; bb < 16; ++bb)
+      if (bb < nbv) dst[bb] = src[(size_t)bb * ld];
   }
 }
 
 // Band projection residual in place on the strip (solver.cpp:61-69 with
 // phase_unit solver.cpp:21-24): y <- y - d * y/|y|  (|y| == 0 -> phase 1).
 // Optionally accumulates sum (|y| - d)^2 into *acc (evaluator).
+// Visit every (a, bb) of an M1 x nb strip; one division per thread, not per element.
+template <class F>
+__device__ __forceinline__ void strip_for(int M1, int nb, F&& f) {
+  const int step = blockDim.x / nb;
+  if ((int)threadIdx.x >= step * nb) return;
+  const int bb = threadIdx.x % nb;
+  for (int a = threadIdx.x / nb; a < M1; a += step) f(a, bb);
+}
+
 template <class R>
 __device__ __forceinline__ void project_strip(const PftDev<R>& pl, ColsSmem<R>& sm, int nb, int nbv,
                                               const R* dc, int b0, bool residual, double* acc) {
-  const int tot = pl.M1 * nb;
   double local = 0.0;
-  for (int i = threadIdx.x; i < tot; i += blockDim.x) {
-    const int a = i / nb, bb = i % nb;
-    if (bb >= nbv) continue;
+  strip_for(pl.M1, nb, [&](int a, int bb) {
+    if (bb >= nbv) return;
     auto& y = sm.Ys[(size_t)a * (nb + 1) + bb];
     const R d = dc[(size_t)a * pl.M2 + b0 + bb];
     const R mag = hypot(y.x, y.y);
@@ -387,14 +416,14 @@ __device__ __forceinline__ void project_strip(const PftDev<R>& pl, ColsSmem<R>& 
     }
     if (residual) {
       if (mag > R(0)) {
-        const R s = d / mag;
-        y.x -= s * y.x;
-        y.y -= s * y.y;
+        const R ux = y.x / mag, uy = y.y / mag;  // phase_unit = v / |v|
+        y.x -= d * ux;
+        y.y -= d * uy;
       } else {
         y.x -= d;
       }
     }
-  }
+  });
   if (acc) *acc += local;
 }
 
@@ -424,7 +453,7 @@ __global__ void __launch_bounds__(256) k_fwd_cols(PftDev<R> pl, const typename C
                                                   double* __restrict__ partial) {
   using C = typename CT<R>::C;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int nb = strip_nb(pl.M2);
+  const int nb = pl.nb;
   ColsSmem<R> sm(smem_raw, pl, nb);
   const int f = blockIdx.y, b0 = blockIdx.x * nb;
   const int nbv = min(nb, pl.M2 - b0);
@@ -436,10 +465,9 @@ __global__ void __launch_bounds__(256) k_fwd_cols(PftDev<R> pl, const typename C
   __syncthreads();
   if (band) {
     C* bf = band + (size_t)f * pl.M1 * pl.M2;
-    for (int i = threadIdx.x; i < pl.M1 * nb; i += blockDim.x) {
-      const int a = i / nb, bb = i % nb;
+    strip_for(pl.M1, nb, [&](int a, int bb) {
       if (bb < nbv) bf[(size_t)a * pl.M2 + b0 + bb] = sm.Ys[(size_t)a * (nb + 1) + bb];
-    }
+    });
   }
   if (MODE == 0) return;
   const R* dc = dcrop + (size_t)f * dstride;
@@ -462,16 +490,15 @@ __global__ void __launch_bounds__(256) k_adj_cols(PftDev<R> pl, const typename C
                                                   typename CT<R>::C* __restrict__ Gt) {
   using C = typename CT<R>::C;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int nb = strip_nb(pl.M2);
+  const int nb = pl.nb;
   ColsSmem<R> sm(smem_raw, pl, nb);
   const int f = blockIdx.y, b0 = blockIdx.x * nb;
   const int nbv = min(nb, pl.M2 - b0);
   cols_load_tables(pl, sm);
   const C* bf = band + (size_t)f * pl.M1 * pl.M2;
-  for (int i = threadIdx.x; i < pl.M1 * nb; i += blockDim.x) {
-    const int a = i / nb, bb = i % nb;
+  strip_for(pl.M1, nb, [&](int a, int bb) {
     sm.Ys[(size_t)a * (nb + 1) + bb] = bb < nbv ? bf[(size_t)a * pl.M2 + b0 + bb] : czero<C>();
-  }
+  });
   __syncthreads();
   cols_adjoint<R, S1, RB>(pl, sm, nb);
   __syncthreads();
@@ -495,6 +522,7 @@ struct EpiArgs {
   void* probe;             // [n1][n2]
   double step;             // beta_pft or gamma_pft
   void* G2;                // EPI 1: fused forward output (may be null)
+  int vec_ok;              // host-verified 16-byte alignment of out / obj window / probe rows
 };
 
 template <class R, int S2, int RB, int EPI>
@@ -505,8 +533,9 @@ __global__ void __launch_bounds__(sizeof(R) == 4 ? 512 : 256) k_adj_rows(PftDev<
   RowsSmem<R> sm(smem_raw, pl);
   const int k1 = blockIdx.x, f = blockIdx.y;
   rows_load_tables(pl, sm.Bv1s, sm.Bv2s, sm.W2s, sm.tw2s);
+  // this row block's r1 x M2 slice of the adjoint intermediate; each element is
+  // read by exactly one lane (coalesced across the lanes' consecutive b)
   const C* Gblk = Gt + ((size_t)f * pl.p1 + k1) * pl.r1 * pl.M2;
-  for (int i = threadIdx.x; i < pl.r1 * pl.M2; i += blockDim.x) sm.Gk[i] = Gblk[i];
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -525,7 +554,7 @@ __global__ void __launch_bounds__(sizeof(R) == 4 ? 512 : 256) k_adj_rows(PftDev<
       if (valid) {
         const int u2 = s * P2 + lig;
         for (int b = mod_nonneg(u2 + pl.mt2, pl.p2); b < M2; b += pl.p2) {
-          const C g = sm.Gk[(size_t)j1 * M2 + b];
+          const C g = Gblk[(size_t)j1 * M2 + b];
 #pragma unroll
           for (int j = 0; j < RB; ++j)
             if (j < r2) cmacc(x[s][j], sm.W2s[j * M2 + b], g);

@@ -1,9 +1,16 @@
 // Launchers for the PFT kernels; included once per precision by
 // pft_launch_f32.cu / pft_launch_f64.cu (PFTG_REAL = float | double) so the two
 // precisions compile in parallel.
+#include <mutex>
+#include <set>
 #include <type_traits>
+#include <utility>
+
+#include <cstdlib>
 
 #include "internal.hpp"
+#include "pft_fast.cuh"
+#include "pft_tma.cuh"
 
 namespace pftg {
 
@@ -46,23 +53,156 @@ void dispatch_sr(int S, int RB, F&& f) {
 
 template <class K>
 void allow_smem(K kernel) {
-  // one-time opt-in to the full 227 KB of dynamic shared memory per CTA
-  PFTG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  // one-time (per kernel and device) opt-in to the full 227 KB of dynamic shared memory per CTA
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  PFTG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.insert({reinterpret_cast<const void*>(kernel), dev}).second)
+    PFTG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
 }
 
 template <class R>
 constexpr int rows_threads() { return sizeof(R) == 4 ? 512 : 256; }
 
+// ---- specialized rows kernels (pft_fast.cuh) for the hot-path plan shapes ----
+template <class R, int Q, int RR>
+BPar<R, Q, RR> make_bpar(const PftDev<R>& pd) {
+  BPar<R, Q, RR> b;
+  for (int l = 0; l <= Q / 2; ++l)
+    for (int j = 0; j < RR; ++j) {
+      b.b1[l][j] = static_cast<R>(pd.hBv1[l * RR + j]);
+      b.b2[l][j] = static_cast<R>(pd.hBv2[l * RR + j]);
+    }
+  return b;
+}
+
+// Calls f(IC<Q>, IC<RR>, IC<P>) when the (square) plan matches a specialized shape.
+template <class R, class F>
+bool dispatch_fast(const PftDev<R>& pd, F&& f) {
+  if (pd.n1 != pd.n2 || pd.p1 != pd.p2 || pd.r1 != pd.r2 || pd.mt1 != pd.mt2 || pd.q1 != pd.q2) return false;
+  const int q = pd.q1, r = pd.r1, p = pd.p1;
+#define PFTG_FAST(QQ, RRR, PP)                      \
+  if (q == QQ && r == RRR && p == PP) {             \
+    f(IC<QQ>{}, IC<RRR>{}, IC<PP>{});               \
+    return true;                                    \
+  }
+  if constexpr (sizeof(R) == 4) {
+    PFTG_FAST(32, 10, 32)  // BASELINE cfg2 literal
+    PFTG_FAST(8, 9, 32)    // cfg3 band (w=256, mt=p=32, eps 1e-3)
+    PFTG_FAST(8, 9, 64)    // cfg4/5 band (w=512, mt=p=64)
+    PFTG_FAST(8, 13, 64)   // scope-1 companion of cfg1 (eps 1e-7)
+    PFTG_FAST(8, 13, 128)  // scope-1 companion of cfg2
+  } else {
+    PFTG_FAST(32, 12, 16)  // BASELINE cfg1 literal
+    PFTG_FAST(32, 10, 32)  // cfg2 literal in complex128
+    PFTG_FAST(8, 13, 64)   // scope-1 companion of cfg1
+    PFTG_FAST(8, 9, 32)    // cfg3 band in complex128
+    PFTG_FAST(8, 13, 8)    // SPEC ACC-4 dot-test shape (64^2, m~=p=8)
+  }
+#undef PFTG_FAST
+  return false;
+}
+
 }  // namespace
 
 using R_ = PFTG_REAL;
 
+namespace {
+
+bool fast_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* G, int batch, cudaStream_t st) {
+  return dispatch_fast(pd, [&](auto q, auto r, auto p) {
+    constexpr int Q = decltype(q)::value, RR = decltype(r)::value, P = decltype(p)::value;
+    const size_t smem = fast_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P);
+    if (smem > 227 * 1024) throw std::invalid_argument("pftg: plan too large for the rows pass (smem)");
+    const auto bp = make_bpar<R_, Q, RR>(pd);
+    const bool vec = sizeof(R_) == 4 && src.vec_ok && (pd.n2 % 2 == 0);
+    constexpr int NT = fast_nt<RR, P>();
+    if (vec) {
+      auto k = kf_fwd_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
+      allow_smem(k);
+      k<<<dim3(pd.p1, batch), NT, smem, st>>>(pd, bp, src, G);
+    } else {
+      auto k = kf_fwd_rows<R_, Q, RR, P, 1>;
+      allow_smem(k);
+      k<<<dim3(pd.p1, batch), NT, smem, st>>>(pd, bp, src, G);
+    }
+  });
+}
+
+// Persistent TMA-fed rows pass (pft_tma.cuh) for plain batched fields whose
+// rows are whole 16-byte multiples and span exactly 512 x {1,2} columns.
+bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* G, int batch, cudaStream_t st) {
+  if (src.offs || src.probe || !src.vec_ok) return false;
+  if (std::getenv("PFTG_NO_TMA")) return false;
+  int vc = 0;
+  if (pd.n2 == kTmaConsumers) vc = 1;
+  else if (sizeof(R_) == 4 && pd.n2 == 2 * kTmaConsumers) vc = 2;
+  if (!vc || (src.ld % 2) || (src.bstride % 2)) return false;
+  return dispatch_fast(pd, [&](auto q, auto r, auto p) {
+    constexpr int Q = decltype(q)::value, RR = decltype(r)::value, P = decltype(p)::value;
+    int ns = 8;
+    while (ns > 2 && tma_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns) > 227 * 1024) --ns;
+    const size_t smem = tma_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns);
+    if (smem > 227 * 1024) throw std::invalid_argument("pftg: plan too large for the TMA rows pass");
+    const auto bp = make_bpar<R_, Q, RR>(pd);
+    int dev = 0, nsm = 148;
+    PFTG_CUDA(cudaGetDevice(&dev));
+    PFTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int ntiles = pd.p1 * batch;
+    const int grid = ntiles < nsm ? ntiles : nsm;
+    if (vc == 2) {
+      auto k = kt_fwd_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
+      allow_smem(k);
+      k<<<grid, kTmaConsumers + 32, smem, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns, G);
+    } else {
+      auto k = kt_fwd_rows<R_, Q, RR, P, 1>;
+      allow_smem(k);
+      k<<<grid, kTmaConsumers + 32, smem, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns, G);
+    }
+  });
+}
+
+bool fast_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, const EpiArgs& ep, int batch,
+                   cudaStream_t st) {
+  return dispatch_fast(pd, [&](auto q, auto r, auto p) {
+    constexpr int Q = decltype(q)::value, RR = decltype(r)::value, P = decltype(p)::value;
+    constexpr int VV = sizeof(R_) == 4 ? 2 : 1;
+    const size_t smem = fast_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P);
+    if (smem > 227 * 1024) throw std::invalid_argument("pftg: plan too large for the rows pass (smem)");
+    const auto bp = make_bpar<R_, Q, RR>(pd);
+    const bool vec = sizeof(R_) == 4 && ep.vec_ok && (pd.n2 % 2 == 0);
+    const dim3 grid(pd.p1, batch);
+    auto go = [&](auto kern) {
+      allow_smem(kern);
+      kern<<<grid, fast_nt<RR, P>(), smem, st>>>(pd, bp, Gt, ep);
+    };
+    if (epi == 0) {
+      if (vec) go(kf_adj_rows<R_, Q, RR, P, VV, 0>);
+      else go(kf_adj_rows<R_, Q, RR, P, 1, 0>);
+    } else if (epi == 1) {
+      if (vec) go(kf_adj_rows<R_, Q, RR, P, VV, 1>);
+      else go(kf_adj_rows<R_, Q, RR, P, 1, 1>);
+    } else {
+      if (vec) go(kf_adj_rows<R_, Q, RR, P, VV, 2>);
+      else go(kf_adj_rows<R_, Q, RR, P, 1, 2>);
+    }
+  });
+}
+
+}  // namespace
+
 template <>
 void launch_fwd_rows<R_>(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* G, int batch,
                          cudaStream_t st) {
+  ProfScope prof(st, K_FWD_ROWS);
+  if (tma_fwd_rows(pd, src, G, batch, st) || fast_fwd_rows(pd, src, G, batch, st)) {
+    PFTG_LAUNCH_CHECK();
+    return;
+  }
   const size_t smem = rows_smem_bytes(pd);
   if (smem > 227 * 1024) throw std::invalid_argument("pftg: plan too large for the rows pass (smem)");
-  ProfScope prof(st, K_FWD_ROWS);
   dispatch_sr(slots_of(pd.p2), rb_of(std::max(pd.r1, pd.r2)), [&](auto s, auto rb) {
     auto k = k_fwd_rows<R_, decltype(s)::value, decltype(rb)::value>;
     static bool once = (allow_smem(k), true);
@@ -74,8 +214,7 @@ void launch_fwd_rows<R_>(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R
 
 template <>
 int cols_strips<R_>(const PftDev<R_>& pd) {
-  const int nb = strip_nb(pd.M2);
-  return (pd.M2 + nb - 1) / nb;
+  return (pd.M2 + pd.nb - 1) / pd.nb;
 }
 
 template <>
@@ -127,9 +266,13 @@ void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, t
 template <>
 void launch_adj_rows<R_>(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, const EpiArgs& ep,
                          int batch, cudaStream_t st) {
+  ProfScope prof(st, K_ADJ_ROWS);
+  if (fast_adj_rows(pd, epi, Gt, ep, batch, st)) {
+    PFTG_LAUNCH_CHECK();
+    return;
+  }
   const size_t smem = rows_smem_bytes(pd);
   if (smem > 227 * 1024) throw std::invalid_argument("pftg: plan too large for the rows pass (smem)");
-  ProfScope prof(st, K_ADJ_ROWS);
   dispatch_sr(slots_of(pd.p2), rb_of(std::max(pd.r1, pd.r2)), [&](auto s, auto rb) {
     constexpr int S = decltype(s)::value, RB = decltype(rb)::value;
     const dim3 grid(pd.p1, batch);

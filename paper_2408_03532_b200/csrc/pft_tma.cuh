@@ -1,0 +1,141 @@
+// Persistent, TMA-fed forward rows pass for the batched PFT (the hot kernel of
+// BASELINE configs[1]): one CTA per SM loops over (field, k1) row blocks.
+//
+//  * A producer warp streams the row block through a ring of NS shared-memory
+//    slots with 1-D bulk copies (cp.async.bulk -> UBLKCP). Each slot holds the
+//    symmetric row pair (l, q-l) (or (0, q/2)), so the node-symmetry pairing of
+//    stage A (pft_fast.cuh) needs no register staging. The producer runs ahead
+//    across block boundaries: while the consumers do stage B / FFT / band of
+//    block t, the first NS pairs of block t+1 are already in flight, so HBM
+//    never idles behind the compute phase.
+//  * 512 consumer threads own 512*VC columns each for the whole block
+//    (accumulators stay in registers across all q rows), then write T to
+//    shared memory and run the same stage-B/FFT/band code as kf_fwd_rows.
+// Math identical to kf_fwd_rows / pft.cpp:119-172 (see pft_kernels.cuh).
+#pragma once
+
+#include "pft_fast.cuh"
+#include "tma.cuh"
+
+namespace pftg {
+
+constexpr int kTmaConsumers = 512;
+
+template <class R>
+__host__ __device__ inline size_t tma_rows_smem(int n2, int q, int r, int M2, int p, int ns) {
+  using C = typename CT<R>::C;
+  size_t b = sizeof(C) * ((size_t)ns * 2 * n2 + (size_t)r * ldT_of(n2, q) + (size_t)r * M2 + p / 2 + 1);
+  b = (b + 15) & ~size_t(15);
+  return b + 2 * ns * sizeof(uint64_t);
+}
+
+template <class R, int Q, int RR, int P, int VC>
+__global__ void __launch_bounds__(kTmaConsumers + 32, 1)
+    kt_fwd_rows(PftDev<R> pl, BPar<R, Q, RR> bp, const typename CT<R>::C* __restrict__ z, long long ld,
+                long long bstride, int ntiles, int NS, typename CT<R>::C* __restrict__ G) {
+  using C = typename CT<R>::C;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int n2 = pl.n2;
+  C* ring = reinterpret_cast<C*>(smem_raw);
+  C* T = ring + (size_t)NS * 2 * n2;
+  const int ldT = ldT_of(n2, Q);
+  C* W2s = T + (size_t)RR * ldT;
+  C* tw2s = W2s + (size_t)RR * pl.M2;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(tw2s + P / 2 + 1) + 15) & ~uintptr_t(15));
+  uint64_t* full = bars;
+  uint64_t* empty = bars + NS;
+
+  fast_load_tables(pl, W2s, tw2s);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmaConsumers / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const uint32_t row_bytes = (uint32_t)(n2 * sizeof(C));
+  if (threadIdx.x >= kTmaConsumers) {
+    // ---------------- producer warp ----------------
+    if (threadIdx.x != kTmaConsumers) return;
+    uint32_t seq = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int f = t / pl.p1, k1 = t % pl.p1;
+      const C* base = z + (long long)f * bstride + (long long)k1 * Q * ld;
+      for (int pi = 0; pi < Q / 2; ++pi, ++seq) {
+        const int s = seq % NS;
+        if (seq >= NS) mbar_wait(&empty[s], ((seq / NS) - 1) & 1);
+        const int la = pi == 0 ? 0 : pi, lb = pi == 0 ? Q / 2 : Q - pi;
+        mbar_arrive_expect_tx(&full[s], 2 * row_bytes);
+        C* slot = ring + (size_t)s * 2 * n2;
+        bulk_g2s(slot, base + (long long)la * ld, row_bytes, &full[s]);
+        bulk_g2s(slot + n2, base + (long long)lb * ld, row_bytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int lane = threadIdx.x & 31;
+  const int c0 = threadIdx.x * VC;
+  uint32_t seq = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int f = t / pl.p1, k1 = t % pl.p1;
+    C acc[VC][RR];
+#pragma unroll
+    for (int v = 0; v < VC; ++v)
+#pragma unroll
+      for (int j = 0; j < RR; ++j) acc[v][j] = czero<C>();
+#pragma unroll
+    for (int pi = 0; pi < Q / 2; ++pi, ++seq) {
+      const int s = seq % NS;
+      mbar_wait(&full[s], (seq / NS) & 1);
+      const C* slot = ring + (size_t)s * 2 * n2;
+      C a[VC], b[VC];
+      if constexpr (VC == 2 && sizeof(C) == 8) {
+        const float4 ta = *reinterpret_cast<const float4*>(slot + c0);
+        const float4 tb = *reinterpret_cast<const float4*>(slot + n2 + c0);
+        a[0] = CT<R>::mk(ta.x, ta.y);
+        a[VC - 1] = CT<R>::mk(ta.z, ta.w);
+        b[0] = CT<R>::mk(tb.x, tb.y);
+        b[VC - 1] = CT<R>::mk(tb.z, tb.w);
+      } else {
+#pragma unroll
+        for (int v = 0; v < VC; ++v) {
+          a[v] = slot[c0 + v];
+          b[v] = slot[n2 + c0 + v];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+      for (int v = 0; v < VC; ++v) {
+        if (pi == 0) {
+#pragma unroll
+          for (int j = 0; j < RR; ++j) bmac(acc[v][j], bp.b1[0][j], a[v], j & 1);
+          bmac(acc[v][0], bp.b1[Q / 2][0], b[v], false);
+        } else {
+          const C sp = cadd(a[v], b[v]), dm = csub(a[v], b[v]);
+#pragma unroll
+          for (int j = 0; j < RR; ++j) bmac(acc[v][j], bp.b1[pi][j], (j & 1) ? dm : sp, j & 1);
+        }
+      }
+    }
+    // all consumers are past stage B of the previous block: T may be overwritten
+    named_sync(1, kTmaConsumers);
+#pragma unroll
+    for (int v = 0; v < VC; ++v) {
+      const int c = c0 + v;
+      const int tc = c + c / Q;
+#pragma unroll
+      for (int j = 0; j < RR; ++j) T[(size_t)j * ldT + tc] = acc[v][j];
+    }
+    named_sync(1, kTmaConsumers);
+    C* Gblk = G + ((size_t)f * pl.p1 + k1) * RR * pl.M2;
+    fast_stage_b_to_g<R, Q, RR, P>(pl, bp, T, W2s, tw2s, Gblk, kTmaConsumers / 32);
+  }
+}
+
+}  // namespace pftg

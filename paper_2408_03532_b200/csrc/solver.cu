@@ -164,7 +164,9 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
     const PftDev<R>& pd = plan_dev<R>(*s.plan);
     const long long mb = (long long)pd.M1 * pd.M2;
     const R* dc = static_cast<const R*>(s.dcrop) + (long long)j * mb;
-    Src<R> src{frame, (long long)s.fc, 0, doff, probe};
+    // 16-byte column pairs when the window starts on an even column of an even-width frame
+    const int vec = (s.offs[j] % 2 == 0) && (s.fc % 2 == 0) && (s.wc % 2 == 0);
+    Src<R> src{frame, (long long)s.fc, 0, doff, probe, vec};
     launch_fwd_rows<R>(pd, src, static_cast<Cx<R>*>(s.G), 1, st);
     launch_fwd_cols<R>(pd, 1, static_cast<Cx<R>*>(s.G), nullptr, dc, mb, static_cast<Cx<R>*>(s.Gt), nullptr, 1, st);
     EpiArgs ep{};
@@ -174,6 +176,7 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
     ep.probe = probe;
     ep.step = s.cfg.beta_pft;
     ep.G2 = blind ? s.G : nullptr;
+    ep.vec_ok = vec;
     launch_adj_rows<R>(pd, 1, static_cast<Cx<R>*>(s.Gt), ep, 1, st);
     if (blind) {
       launch_fwd_cols<R>(pd, 1, static_cast<Cx<R>*>(s.G), nullptr, dc, mb, static_cast<Cx<R>*>(s.Gt), nullptr, 1,

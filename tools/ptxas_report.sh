@@ -1,6 +1,6 @@
 #!/bin/bash
 # usage: tools_ptxas_report.sh file.cu  -> kernel, regs, spills (demangled)
-nvcc -std=c++17 -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -Xcompiler -fPIC -Xptxas -v -c "$1" -o /tmp/ptxas_report.o 2>&1 | python3 -c '
+nvcc -std=c++17 -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --expt-relaxed-constexpr -Xcompiler -fPIC -Xptxas -v -c "$1" -o /tmp/ptxas_report.o 2>&1 | python3 -c '
 import sys, re, subprocess
 lines = sys.stdin.read().splitlines()
 cur = None
