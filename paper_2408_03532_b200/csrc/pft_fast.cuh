@@ -222,12 +222,8 @@ __device__ __forceinline__ void fast_stage_b_to_g(const PftDev<R>& pl, const BPa
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int u2 = bitrev(s * PL + lig, LP);
-      for (int b = (u2 + mt2) & (P - 1); b < M2; b += P) {
-        C acc = czero<C>();
-#pragma unroll
-        for (int j = 0; j < RR; ++j) cmac(acc, x[s][j], W2s[j * M2 + b]);
-        Gblk[(size_t)j1 * M2 + b] = acc;
-      }
+      band_contract<RR>(W2s, M2, (u2 + mt2) & (P - 1), P, RR, x[s],
+                        [&](int b, C v) { Gblk[(size_t)j1 * M2 + b] = v; });
     }
   }
 }

@@ -79,7 +79,6 @@ __host__ inline size_t cols_smem_bytes(const PftDev<R>& p, int nb) {
   size_t b = 0;
   b += sizeof(C) * (size_t)p.r1 * nb * (p.p1 + 1);  // Gs
   b += sizeof(C) * (size_t)p.M1 * (nb + 1);        // band strip
-  b += sizeof(C) * (size_t)p.r1 * p.M1;            // W1t
   b += sizeof(C) * (size_t)(p.p1 / 2 + 1);         // tw1
   b += sizeof(double) * 64;                        // reduction scratch
   return (b + 15) & ~size_t(15);
@@ -91,11 +90,36 @@ __host__ inline size_t cols_smem_bytes(const PftDev<R>& p) {
 }
 
 // Widest strip (<= 16 band columns) whose working set fits in shared memory.
+// 8 band columns per CTA keeps several CTAs resident per SM (the cols pass is
+// latency-bound); fewer only when the strip does not fit.
 template <class R>
 __host__ inline int choose_nb(const PftDev<R>& p) {
-  int nb = p.M2 < 16 ? p.M2 : 16;
-  while (nb > 1 && cols_smem_bytes(p, nb) > 200 * 1024) nb /= 2;
+  int nb = p.M2 < 8 ? p.M2 : 8;
+  while (nb > 1 && cols_smem_bytes(p, nb) > 100 * 1024) nb /= 2;
   return nb;
+}
+
+// out[m] = sum_j W[j*M + a0 + m*step] * x[j] for the M/step band indices of one
+// FFT output (4 independent accumulation chains at a time). emit(a, value).
+template <int RB, class C, class Emit>
+__device__ __forceinline__ void band_contract(const C* __restrict__ W, int M, int a0, int step, int r,
+                                              const C (&x)[RB], Emit&& emit) {
+  for (int a = a0; a < M; a += 4 * step) {
+    C acc[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) acc[m] = czero<C>();
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      if (j < r) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          if (a + m * step < M) cmac(acc[m], W[j * M + a + m * step], x[j]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (a + m * step < M) emit(a + m * step, acc[m]);
+  }
 }
 
 // ------------------------------------------------------------ rows pass core
@@ -138,13 +162,8 @@ __device__ __forceinline__ void rows_stage_b_to_g(const PftDev<R>& pl, const typ
 #pragma unroll
     for (int s = 0; s < S2; ++s) {
       const int u2 = bitrev(s * P2 + lig, pl.lp2);
-      for (int b = mod_nonneg(u2 + pl.mt2, pl.p2); b < M2; b += pl.p2) {
-        C acc = czero<C>();
-#pragma unroll
-        for (int j = 0; j < RB; ++j)
-          if (j < r2) cmac(acc, x[s][j], W2t[j * M2 + b]);
-        Gblk[(size_t)j1 * M2 + b] = acc;
-      }
+      band_contract<RB>(W2t, M2, mod_nonneg(u2 + pl.mt2, pl.p2), pl.p2, r2, x[s],
+                        [&](int b, C v) { Gblk[(size_t)j1 * M2 + b] = v; });
     }
   }
 }
@@ -250,7 +269,7 @@ struct ColsSmem {
   using C = typename CT<R>::C;
   C* Gs;   // [r1][nb][p1+1]
   C* Ys;   // [M1][nb+1]  band strip
-  C* W1s;  // [r1][M1]
+  const C* W1s;  // [r1][M1], read through L1 (shared by all CTAs; no per-CTA copy)
   C* tw1s;
   double* red;
   __device__ ColsSmem(unsigned char* raw, const PftDev<R>& pl, int nb) {
@@ -259,8 +278,7 @@ struct ColsSmem {
     c += (size_t)pl.r1 * nb * (pl.p1 + 1);
     Ys = c;
     c += (size_t)pl.M1 * (nb + 1);
-    W1s = c;
-    c += (size_t)pl.r1 * pl.M1;
+    W1s = pl.W1t;
     tw1s = c;
     c += pl.p1 / 2 + 1;
     red = reinterpret_cast<double*>(c);
@@ -269,7 +287,6 @@ struct ColsSmem {
 
 template <class R>
 __device__ __forceinline__ void cols_load_tables(const PftDev<R>& pl, ColsSmem<R>& sm) {
-  for (int i = threadIdx.x; i < pl.r1 * pl.M1; i += blockDim.x) sm.W1s[i] = pl.W1t[i];
   for (int i = threadIdx.x; i < pl.p1 / 2; i += blockDim.x) sm.tw1s[i] = pl.tw1[i];
 }
 
@@ -322,13 +339,8 @@ __device__ __forceinline__ void cols_forward(const PftDev<R>& pl, ColsSmem<R>& s
 #pragma unroll
     for (int s = 0; s < S1; ++s) {
       const int u1 = bitrev(s * P1 + lig, pl.lp1);
-      for (int a = mod_nonneg(u1 + pl.mt1, pl.p1); a < M1; a += pl.p1) {
-        C acc = czero<C>();
-#pragma unroll
-        for (int j = 0; j < RB; ++j)
-          if (j < r1) cmac(acc, sm.W1s[j * M1 + a], x[s][j]);
-        sm.Ys[(size_t)a * (nb + 1) + bb] = acc;
-      }
+      band_contract<RB>(sm.W1s, M1, mod_nonneg(u1 + pl.mt1, pl.p1), pl.p1, r1, x[s],
+                        [&](int a, C v) { sm.Ys[(size_t)a * (nb + 1) + bb] = v; });
     }
   }
 }
@@ -357,7 +369,7 @@ __device__ __forceinline__ void cols_adjoint(const PftDev<R>& pl, ColsSmem<R>& s
           const C y = sm.Ys[(size_t)a * (nb + 1) + bb];
 #pragma unroll
           for (int j = 0; j < RB; ++j)
-            if (j < r1) cmacc(x[s][j], sm.W1s[j * M1 + a], y);
+            if (j < r1) cmacc(x[s][j], __ldg(sm.W1s + j * M1 + a), y);
         }
       }
     }
@@ -446,7 +458,7 @@ __device__ __forceinline__ void block_sum_store(double v, double* scratch, doubl
 // MODE 2: forward cols -> sum (|band| - dcrop)^2 per CTA into partial.
 // grid = (ceil(M2/nb), batch).
 template <class R, int S1, int RB, int MODE>
-__global__ void __launch_bounds__(256) k_fwd_cols(PftDev<R> pl, const typename CT<R>::C* __restrict__ G,
+__global__ void __launch_bounds__(256, 3) k_fwd_cols(PftDev<R> pl, const typename CT<R>::C* __restrict__ G,
                                                   typename CT<R>::C* __restrict__ band,
                                                   const R* __restrict__ dcrop, long long dstride,
                                                   typename CT<R>::C* __restrict__ Gout,
@@ -486,7 +498,7 @@ __global__ void __launch_bounds__(256) k_fwd_cols(PftDev<R> pl, const typename C
 
 // Adjoint cols: band -> Gt. grid = (ceil(M2/nb), batch).
 template <class R, int S1, int RB>
-__global__ void __launch_bounds__(256) k_adj_cols(PftDev<R> pl, const typename CT<R>::C* __restrict__ band,
+__global__ void __launch_bounds__(256, 3) k_adj_cols(PftDev<R> pl, const typename CT<R>::C* __restrict__ band,
                                                   typename CT<R>::C* __restrict__ Gt) {
   using C = typename CT<R>::C;
   extern __shared__ __align__(16) unsigned char smem_raw[];

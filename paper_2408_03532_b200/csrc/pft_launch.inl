@@ -152,14 +152,17 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
     PFTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     const int ntiles = pd.p1 * batch;
     const int grid = ntiles < nsm ? ntiles : nsm;
+    const char* dv = std::getenv("PFTG_DEBUG_TMA");
+    const int dbg = dv ? std::atoi(dv) : 0;
+    if (const char* e = std::getenv("PFTG_TMA_NS")) ns = std::min(ns, std::atoi(e));
     if (vc == 2) {
       auto k = kt_fwd_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
       allow_smem(k);
-      k<<<grid, kTmaConsumers + 32, smem, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns, G);
+      k<<<grid, kTmaConsumers + 32, smem, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns, G, dbg);
     } else {
       auto k = kt_fwd_rows<R_, Q, RR, P, 1>;
       allow_smem(k);
-      k<<<grid, kTmaConsumers + 32, smem, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns, G);
+      k<<<grid, kTmaConsumers + 32, smem, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns, G, dbg);
     }
   });
 }

@@ -32,7 +32,7 @@ __host__ __device__ inline size_t tma_rows_smem(int n2, int q, int r, int M2, in
 template <class R, int Q, int RR, int P, int VC>
 __global__ void __launch_bounds__(kTmaConsumers + 32, 1)
     kt_fwd_rows(PftDev<R> pl, BPar<R, Q, RR> bp, const typename CT<R>::C* __restrict__ z, long long ld,
-                long long bstride, int ntiles, int NS, typename CT<R>::C* __restrict__ G) {
+                long long bstride, int ntiles, int NS, typename CT<R>::C* __restrict__ G, int dbg) {
   using C = typename CT<R>::C;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int n2 = pl.n2;
@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1)
       for (int j = 0; j < RR; ++j) T[(size_t)j * ldT + tc] = acc[v][j];
     }
     named_sync(1, kTmaConsumers);
+    if (dbg & 1) continue;  // profiling experiment: streaming + stage A only
     C* Gblk = G + ((size_t)f * pl.p1 + k1) * RR * pl.M2;
     fast_stage_b_to_g<R, Q, RR, P>(pl, bp, T, W2s, tw2s, Gblk, kTmaConsumers / 32);
   }
