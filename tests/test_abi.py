@@ -1,0 +1,112 @@
+"""CPU tests of the drop-in boundary: libpftg.so loads and exports every symbol
+include/pftg.h declares; the host-side offline phase (scope table, plans,
+plan files) mirrors the reference bit-for-bit; compute entry points fail loudly
+(no CPU fallback) when no GPU is present; error codes map onto the
+reference's exception types."""
+import ctypes as C
+import re
+
+import numpy as np
+import pytest
+
+from conftest import DATA, GOLDEN, ROOT
+
+torch = pytest.importorskip("torch")
+P = pytest.importorskip("paper_2408_03532_b200")
+from paper_2408_03532_b200 import _lib  # noqa: E402
+
+HEADER = ROOT / "include" / "pftg.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(pftg_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = declared_symbols()
+    assert len(syms) >= 30
+    lib = C.CDLL(str(_lib.LIB_PATH))
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert sorted(_lib.EXPORTS) == syms
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_scope_table_and_min_degree_mirror_reference():
+    t = P.ScopeTable.load()
+    assert t.min_degree(1e-7, 1.0) == 13
+    assert t.min_degree(1e-3, 1.0) == 9
+    with pytest.raises(ValueError, match="infeasible"):
+        t.min_degree(1e-7, 4.0)
+    with pytest.raises(OSError):
+        P.ScopeTable.load(ROOT / "README.md")
+
+
+def test_plan_tables_bit_identical_to_reference_golden():
+    g = np.load(GOLDEN / "pft_small.npz")
+    pl = P.pft_plan_2d(64, 64, 8, 8, 8, 8, 1e-7)
+    B, W = pl.tables(1)
+    assert (pl.r1, pl.r2) == (13, 13)
+    assert np.array_equal(B, g["B"]) and np.array_equal(W, g["W"])
+
+
+def test_plan_validation_errors_mirror_reference():
+    t = P.ScopeTable.load()
+    with pytest.raises(ValueError, match="p must divide n"):
+        P.pft_plan_2d(16, 16, 1, 1, 5, 5, 1e-1, t)
+    with pytest.raises(ValueError, match="2\\*mt <= n"):
+        P.pft_plan_2d(16, 16, 9, 9, 4, 4, 1e-1, t)
+    with pytest.raises(ValueError, match="q = n/p >= 2"):
+        P.pft_plan_2d(16, 16, 4, 4, 16, 16, 1e-1, t)
+
+
+def test_plan_file_roundtrip_matches_reference(tmp_path, ref):
+    pl = P.pft_plan_2d(256, 256, 32, 32, 32, 32, 1e-3)
+    pl.save(tmp_path / "ours.plan")
+    rp = ref.RefPlan.create(DATA / "scope_table_v1.txt", 256, 256, 32, 32, 32, 32, 1e-3)
+    rp.save(tmp_path / "ref.plan")
+    assert (tmp_path / "ours.plan").read_bytes() == (tmp_path / "ref.plan").read_bytes()
+    back = P.PftPlan2D.load(tmp_path / "ref.plan")
+    assert np.array_equal(back.tables(2)[1], rp.tables(2)[1])
+    # the reference loads our file too
+    rp2 = ref.RefPlan.load(tmp_path / "ours.plan")
+    assert (rp2.n1, rp2.p1, rp2.r1) == (256, 32, 9)
+
+
+def test_plan_file_errors(tmp_path):
+    bad = tmp_path / "bad.plan"
+    bad.write_text("not a plan\n")
+    with pytest.raises(OSError, match="pft-plan-2d"):
+        P.PftPlan2D.load(bad)
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_compute_fails_loudly_without_gpu():
+    pl = P.pft_plan_2d(64, 64, 8, 8, 8, 8, 1e-7)
+    with pytest.raises(P.CudaError, match="no CPU fallback"):
+        P.pft_apply_2d(pl, np.zeros((64, 64), np.complex128))
+    lib = _lib.lib()
+    assert lib.pftg_device_ok() == 0
+
+
+def test_solver_config_defaults_mirror_reference():
+    """SolverConfig defaults (solver.hpp:21-37)."""
+    c = P.SolverConfig()
+    assert (c.pft_sweeps, c.fft_sweeps, c.beta, c.gamma, c.beta_pft, c.gamma_pft, c.eps_pft) == \
+        (0, 50, 1.0, 1.0, 1e-3, 1e-3, 1e-3)
+    assert (c.mt1, c.p1, c.tol, c.blind, c.shuffled, c.seed) == (0, 0, 0.0, False, False, 0)
+
+
+def test_tv_is_rejected_not_ignored():
+    with pytest.raises(ValueError, match="TV"):
+        P.Solver(np.zeros((1, 32, 32)), [[0, 0]], np.ones((32, 32)), np.ones((32, 32)),
+                 P.SolverConfig(tv_lambda_mag=1e-3))
