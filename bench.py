@@ -320,17 +320,178 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _sync_time(fn):
+    import torch
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = fn()
+    torch.cuda.synchronize()
+    return out, time.perf_counter() - t0
+
+
+def run_epie(args):
+    """BASELINE configs[2] / [3]: PFT-warm-started blind ePIE, complex64, one GPU
+    (the sweep does not shard: every position updates the shared probe)."""
+    import torch
+
+    import paper_2408_03532_b200 as P
+    from paper_2408_03532_b200 import problems as PR
+    from paper_2408_03532_b200._lib import KernelProfile
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    n, w, K, sph, spr, photons, pft_sweeps, fft_sweeps, mt = PR.CONFIGS[args.workload]
+    prob = PR.make_problem(args.workload, seed=0)
+    npos = len(prob.offsets)
+    rng = np.random.default_rng(1)
+    # random_object (solver.cpp:115-124): |z| ~ U[0,1], arg z ~ U[0, pi/2]
+    init = (rng.random((n, n)) * np.exp(1j * rng.random((n, n)) * np.pi / 2)).astype(np.complex64)
+    pinit = PR.make_probe(w, 1.2 * spr, "cuda").abs().to(torch.complex64).cpu().numpy()
+    # Step sizes (DESIGN.md §ePIE): the reference's unnormalized updates with
+    # beta = gamma = 1 diverge on this problem in the reference itself (NaN at
+    # sweep 2); beta = 0.5, gamma = 0.05, beta_pft = 0.25 / w^2, gamma_pft =
+    # gamma * beta_pft were the most accurate stable setting of a small grid.
+    beta, gamma, bp = 0.5, 0.05, 0.25 / (w * w)
+    cfg = P.SolverConfig(pft_sweeps=pft_sweeps, fft_sweeps=fft_sweeps, beta=beta, gamma=gamma,
+                         beta_pft=bp, gamma_pft=gamma * bp, eps_pft=1e-3, mt1=mt, mt2=mt, blind=True)
+    d = prob.d.cpu().numpy()
+    # warm-up: a 1+1-sweep solve on the first positions builds the plan, graphs, twiddles
+    wcfg = P.SolverConfig(**{**cfg.__dict__, "pft_sweeps": 1, "fft_sweeps": 1})
+    P.Solver(d[:4], prob.offsets[:4], pinit, init, wcfg).run()
+    s = P.Solver(d, prob.offsets, pinit, init, cfg)
+    with KernelProfile() as prof:
+        _, t_band = _sync_time(lambda: s.run(pft_sweeps))
+        _, t_fft = _sync_time(lambda: s.run())
+    res = s.result()
+    truth = prob.obj.cpu().numpy()
+    err = PR.relative_error_aligned(res.frame, truth)
+    total_updates = npos * (pft_sweeps + fft_sweeps)
+    value = total_updates / (t_band + t_fft)
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            from oracle import ref
+            d64 = d.astype(np.float64)
+            t0 = time.perf_counter()
+            ref.hybrid_solve(init.astype(np.complex128), pinit.astype(np.complex128), prob.offsets, d64,
+                             pft_sweeps=1, fft_sweeps=1, beta=beta, gamma=gamma, beta_pft=bp,
+                             gamma_pft=gamma * bp, eps_pft=1e-3, mt=mt, blind=True,
+                             table_path=DATA / "scope_table_v1.txt")
+            tc = time.perf_counter() - t0
+            cpu = {"value": 2 * npos / tc, "unit": "scan-updates/s", "cores": 1, "kind": "reference",
+                   "sample": f"1 band sweep + 1 FFT sweep ({2 * npos} updates, per-sweep objective "
+                             "included) of the same problem, unmodified proj/core hybrid_solve "
+                             "(complex128), 1 thread"}
+        except Exception as exc:
+            cpu = {"value": None, "unit": "scan-updates/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+    line = {
+        "metric": "epie_scan_updates_per_sec", "value": value, "unit": "scan-updates/s", "n_gpus": 1,
+        "steps": 1, "warmup": 1, "ms_per_step": 1e3 * (t_band + t_fft), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, see problems.py)",
+        "config": {"workload": args.workload, "object": n, "window": w, "positions": npos,
+                   "pft_sweeps": pft_sweeps, "fft_sweeps": fft_sweeps, "band_M": 2 * mt,
+                   "parallelism": "single GPU (sequential scan order; replicas only)"},
+        "band_updates_per_s": npos * pft_sweeps / t_band, "fft_updates_per_s": npos * fft_sweeps / t_fft,
+        "final_objective": float(res.objective[-1]), "final_rel_err_aligned": err,
+        "objective_trace": [float(v) for v in res.objective],
+        "kernel_ms": prof.ms, "gpu_launches": sum(prof.launches.values()),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_evaluator(args):
+    """BASELINE configs[4]: forward-model/residual evaluation of the cfg4 problem
+    (1600 positions of 512^2 c64, PFT band M=128 + full FFT), positions sharded
+    over the ranks, one NCCL all-reduce of the scalar residuals."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2408_03532_b200 as P
+    from paper_2408_03532_b200 import problems as PR
+    from paper_2408_03532_b200._lib import KernelProfile
+    from paper_2408_03532_b200.dist import evaluate_sharded
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    prob = PR.make_problem("cfg4", seed=0)
+    w = prob.probe.shape[0]
+    mt = 64
+    plan = P.pft_plan_2d(w, w, mt, mt, mt, mt, 1e-3)
+    dcrop = P.crop_centered(prob.d.cuda(), mt, mt)
+    npos = len(prob.offsets)
+
+    def step():
+        return evaluate_sharded(prob.obj, prob.probe, prob.offsets, prob.d, plan, dcrop)
+
+    for _ in range(max(args.warmup, 3)):
+        phi = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier(device_ids=[local])
+    clk = ClockSampler(local).__enter__()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with KernelProfile() as prof:
+        e0.record()
+        for _ in range(args.steps):
+            phi = step()
+        e1.record()
+        torch.cuda.synchronize()
+    t_end = time.perf_counter() + 1.0
+    while time.perf_counter() < t_end:
+        step()
+    clk.__exit__(None, None, None)
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = npos * args.steps / (ms / 1e3)
+    hbm, peak_kind = peaks()
+    kname = max(prof.ms, key=lambda k: prof.ms[k])
+    # algorithmic bytes per position (SURVEY §8(d) D3): patch w^2*8 + d w^2*4 + dcrop M^2*4
+    from paper_2408_03532_b200.dist import shard_range
+    pb, pe = shard_range(npos, rank, world)
+    alg = (pe - pb) * (w * w * 8 + w * w * 4 + (2 * mt) ** 2 * 4) * args.steps
+    achieved_step = alg / (ms / 1e3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": "evaluator_positions_per_sec", "value": value, "unit": "positions/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded cfg4 problem, see problems.py)",
+            "config": {"workload": "cfg5", "positions": npos, "window": w, "band_M": 2 * mt,
+                       "parallelism": f"positions sharded x{world}, scalar NCCL all-reduce"},
+            "phi_fft": phi[0], "phi_band": phi[1],
+            "roofline": {"bound": "hbm", "kernel": "whole step (per-rank algorithmic bytes)",
+                         "achieved": achieved_step, "peak": hbm, "unit": "GB/s", "frac": achieved_step / hbm,
+                         "traffic": None, "peak_kind": peak_kind, "dominant_kernel": kname,
+                         "kernel_ms": prof.ms},
+            "gpu_launches": sum(prof.launches.values()), "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="cfg2")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS) + ("cfg3", "cfg4", "cfg5"), default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload in ("cfg3", "cfg4"):
+        run_epie(args)
+    elif args.workload == "cfg5":
+        run_evaluator(args)
     else:
         run_ours(args)
 

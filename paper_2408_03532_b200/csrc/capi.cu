@@ -38,10 +38,21 @@ void ensure_device() {
   }
   int dev = 0;
   PFTG_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static bool checked[64] = {};
+  if (dev < 64 && checked[dev]) return;
+  std::lock_guard<std::mutex> lock(mu);
   int major = 0;
   PFTG_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
   if (major != 10) throw cuda_error("pftg: built for sm_100a (B200); device has compute capability major " +
                                     std::to_string(major));
+  // Scratch buffers come from the stream-ordered default pool; keep freed
+  // memory cached instead of returning it to the driver at every sync.
+  cudaMemPool_t pool;
+  PFTG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  std::uint64_t keep = ~std::uint64_t(0);
+  PFTG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  if (dev < 64) checked[dev] = true;
 }
 
 void check_fft_len(std::size_t n) {
@@ -330,23 +341,20 @@ template <class R, class Op>
 void host_pipeline(std::size_t batch, std::size_t in_elems, std::size_t out_elems, const void* in, void* out,
                    std::size_t chunk, Op&& op) {
   using C = Cx<R>;
-  cudaStream_t s[2];
-  PFTG_CUDA(cudaStreamCreateWithFlags(&s[0], cudaStreamNonBlocking));
-  PFTG_CUDA(cudaStreamCreateWithFlags(&s[1], cudaStreamNonBlocking));
-  C* din[2] = {nullptr, nullptr};
-  C* dout[2] = {nullptr, nullptr};
-  auto cleanup = [&] {
-    for (int k = 0; k < 2; ++k) {
-      if (din[k]) cudaFree(din[k]);
-      if (dout[k]) cudaFree(dout[k]);
-      cudaStreamDestroy(s[k]);
-    }
-  };
-  try {
-    for (int k = 0; k < 2; ++k) {
-      PFTG_CUDA(cudaMalloc(&din[k], sizeof(C) * in_elems * chunk));
-      PFTG_CUDA(cudaMalloc(&dout[k], sizeof(C) * out_elems * chunk));
-    }
+  // two non-blocking streams per (host thread, device), created once
+  thread_local cudaStream_t streams[64][2] = {};
+  int dev = 0;
+  PFTG_CUDA(cudaGetDevice(&dev));
+  if (dev >= 64) throw std::runtime_error("pftg: device index out of range");
+  cudaStream_t* s = streams[dev];
+  for (int k = 0; k < 2; ++k)
+    if (!s[k]) PFTG_CUDA(cudaStreamCreateWithFlags(&s[k], cudaStreamNonBlocking));
+  {
+    // buffers from the stream-ordered pool (released on the stream that used them)
+    Scratch din0(sizeof(C) * in_elems * chunk, s[0]), dout0(sizeof(C) * out_elems * chunk, s[0]);
+    Scratch din1(sizeof(C) * in_elems * chunk, s[1]), dout1(sizeof(C) * out_elems * chunk, s[1]);
+    C* din[2] = {din0.as<C>(), din1.as<C>()};
+    C* dout[2] = {dout0.as<C>(), dout1.as<C>()};
     int k = 0;
     for (std::size_t b0 = 0; b0 < batch; b0 += chunk, k ^= 1) {
       const std::size_t nb = std::min(chunk, batch - b0);
@@ -356,13 +364,9 @@ void host_pipeline(std::size_t batch, std::size_t in_elems, std::size_t out_elem
       PFTG_CUDA(cudaMemcpyAsync(static_cast<C*>(out) + b0 * out_elems, dout[k], sizeof(C) * out_elems * nb,
                                 cudaMemcpyDeviceToHost, s[k]));
     }
-    PFTG_CUDA(cudaStreamSynchronize(s[0]));
-    PFTG_CUDA(cudaStreamSynchronize(s[1]));
-  } catch (...) {
-    cleanup();
-    throw;
   }
-  cleanup();
+  PFTG_CUDA(cudaStreamSynchronize(s[0]));
+  PFTG_CUDA(cudaStreamSynchronize(s[1]));
 }
 
 std::size_t host_chunk(std::size_t batch, std::size_t bytes_per_field) {
@@ -509,9 +513,11 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
     // full-FFT objective: rows (natural input, bitrev-gather + DIT) ...
     RowSrc<R> src{static_cast<const Cx<R>*>(frame), (long long)fc, 0, o, static_cast<const Cx<R>*>(probe)};
     RowEpiArgs ep{};
-    launch_fft_rows<R>(ROW_DIF_STORE, EPI_STORE, n1, n2, src, X.as<Cx<R>>(), n, -1, 1.0, ep, nb, st);
-    launch_fft_cols<R>(COL_EVAL, n1, n2, X.as<Cx<R>>(), n, static_cast<const R*>(d) + (pb + c0) * n, n, nullptr, 1,
-                       -1, part.as<double>() + c0 * nstrips, nb, st);
+    // natural-order spectrum (bit-reversed gathers stay on-chip) so the measured
+    // magnitudes are read as coalesced strips
+    launch_fft_rows<R>(ROW_DIT_NATURAL, EPI_STORE, n1, n2, src, X.as<Cx<R>>(), n, -1, 1.0, ep, nb, st);
+    launch_fft_cols<R>(COL_EVAL_NAT, n1, n2, X.as<Cx<R>>(), n, static_cast<const R*>(d) + (pb + c0) * n, n,
+                       nullptr, 0, -1, part.as<double>() + c0 * nstrips, nb, st);
     if (pd) {
       bool evec = vec_ok(frame, (long long)fc, 0) && vec_ok(probe, n2, 0);
       for (std::size_t j = c0; j < c0 + nb; ++j) evec = evec && (offs[j] % 2 == 0);

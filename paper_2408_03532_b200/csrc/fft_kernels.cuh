@@ -197,6 +197,7 @@ enum ColMode {
   COL_PROJECT = 0,     // DIF (natural rows) -> modulus projection -> DIT ; in place
   COL_EVAL = 1,        // DIF -> sum (|X| - d)^2 per CTA
   COL_NATURAL = 2,     // bitrev gather -> DIT -> natural (API fft2/ifft2)
+  COL_EVAL_NAT = 3,    // rows already natural: bitrev gather -> DIT -> sum (|X| - d)^2, d natural
 };
 
 // grid = (n2 / nc, batch), block 256. Strip of nc columns x n1 rows in smem.
@@ -254,6 +255,22 @@ __global__ void __launch_bounds__(256) k_fft_cols(int n1, int n2, int lg1, int l
       }
       continue;
     }
+    if (MODE == COL_EVAL_NAT) {
+      // natural-order spectrum column vs the natural measured magnitudes (coalesced d strip)
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        x[s][0] = valid ? strip[(size_t)bitrev(s * P + lig, lg1) * ld + cc] : czero<C>();
+      fft_dit<S, 1>(x, n1, P, lig, tws, -1);
+      if (valid) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const C v = x[s][0];
+          const double e = (double)hypot(v.x, v.y) - (double)ds[(size_t)(s * P + lig) * nc + cc];
+          local += e * e;
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int s = 0; s < S; ++s) x[s][0] = valid ? strip[(size_t)(s * P + lig) * ld + cc] : czero<C>();
     fft_dif<S, 1>(x, n1, P, lig, tws, -1);
@@ -292,7 +309,7 @@ __global__ void __launch_bounds__(256) k_fft_cols(int n1, int n2, int lg1, int l
       for (int s = 0; s < S; ++s) strip[(size_t)(s * P + lig) * ld + cc] = x[s][0];
     }
   }
-  if (MODE == COL_EVAL) {
+  if (MODE == COL_EVAL || MODE == COL_EVAL_NAT) {
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
     __syncthreads();
     if (lane == 0) red[warp] = local;

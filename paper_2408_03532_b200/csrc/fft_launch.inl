@@ -130,6 +130,12 @@ void launch_fft_cols<R_>(int mode, int n1, int n2, C_* X, long long x_bstride, c
       (void)once;
       k<<<grid, 256, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
                                  dmode, sign, partial);
+    } else if (mode == COL_EVAL_NAT) {
+      auto k = k_fft_cols<R_, SS, COL_EVAL_NAT>;
+      static bool once = (allow_smem_fft(k), true);
+      (void)once;
+      k<<<grid, 256, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
+                                 dmode, sign, partial);
     } else {
       auto k = k_fft_cols<R_, SS, COL_NATURAL>;
       static bool once = (allow_smem_fft(k), true);

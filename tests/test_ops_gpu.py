@@ -164,3 +164,28 @@ def test_evaluator_band_and_fft(ref):
         ex = probe * obj[r0:r0 + 64, c0:c0 + 64]
         want_b += np.sum((np.abs(r.apply(ex)) - dcrop[j]) ** 2)
     assert abs(bs - want_b) <= 1e-9 * max(want_b, 1e-30) + 1e-18
+
+
+def test_cfg3_full_problem_one_band_one_fft_sweep(ref):
+    """BASELINE configs[2] problem (1024^2 object, 400 positions of 256^2, M=64),
+    blind, stable steps: GPU c128 == reference hybrid_solve to 1e-10 after one
+    PFT sweep + one FFT sweep; c64 within 1e-3 (float rounding through 800
+    sequential dependent updates)."""
+    from paper_2408_03532_b200 import problems as PR
+    prob = PR.make_problem("cfg3", seed=0)
+    n, w = prob.obj.shape[0], prob.probe.shape[0]
+    rng = np.random.default_rng(1)
+    init = rng.random((n, n)) * np.exp(1j * rng.random((n, n)) * np.pi / 2)
+    pinit = PR.make_probe(w, 48.0, "cuda").abs().to(torch.complex128).cpu().numpy()
+    d = prob.d.cpu().numpy().astype(np.float64)
+    kw = dict(pft_sweeps=1, fft_sweeps=1, beta=0.5, gamma=0.05, beta_pft=0.25 / w ** 2,
+              gamma_pft=0.25 * 0.05 / w ** 2, eps_pft=1e-3, blind=True)
+    fr, pr, objr, _, flags = ref.hybrid_solve(init, pinit, prob.offsets, d, mt=32,
+                                              table_path=DATA / "scope_table_v1.txt", **kw)
+    assert flags == 0
+    r128 = P.hybrid_solve(d, prob.offsets, pinit, init, P.SolverConfig(mt1=32, mt2=32, **kw),
+                          dtype=np.complex128)
+    assert rel_l2(r128.frame, fr) <= 1e-10 and rel_l2(r128.probe, pr) <= 1e-10
+    assert np.allclose(r128.objective, objr, rtol=1e-10)
+    r64 = P.hybrid_solve(d, prob.offsets, pinit, init, P.SolverConfig(mt1=32, mt2=32, **kw))
+    assert rel_l2(r64.frame, fr) <= 1e-3 and rel_l2(r64.probe, pr) <= 1e-3
