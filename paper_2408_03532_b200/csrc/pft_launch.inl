@@ -167,6 +167,36 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
   });
 }
 
+bool tma_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, const EpiArgs& ep, int batch,
+                  cudaStream_t st) {
+  if (epi != 0 || !ep.vec_ok || std::getenv("PFTG_NO_TMA")) return false;
+  int vc = 0;
+  if (pd.n2 == kTmaConsumers) vc = 1;
+  else if (sizeof(R_) == 4 && pd.n2 == 2 * kTmaConsumers) vc = 2;
+  if (!vc) return false;
+  return dispatch_fast(pd, [&](auto q, auto r, auto p) {
+    constexpr int Q = decltype(q)::value, RR = decltype(r)::value, P = decltype(p)::value;
+    const size_t smem = tma_adj_smem<R_>(pd.n2, Q, RR, pd.M2, P);
+    if (smem > 227 * 1024) throw std::invalid_argument("pftg: plan too large for the TMA adjoint rows pass");
+    const auto bp = make_bpar<R_, Q, RR>(pd);
+    int dev = 0, nsm = 148;
+    PFTG_CUDA(cudaGetDevice(&dev));
+    PFTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int ntiles = pd.p1 * batch;
+    const int grid = ntiles < nsm ? ntiles : nsm;
+    auto* out = reinterpret_cast<typename CT<R_>::C*>(ep.out);
+    if (vc == 2) {
+      auto k = kt_adj_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
+      allow_smem(k);
+      k<<<grid, kTmaConsumers + 32, smem, st>>>(pd, bp, Gt, out, ntiles);
+    } else {
+      auto k = kt_adj_rows<R_, Q, RR, P, 1>;
+      allow_smem(k);
+      k<<<grid, kTmaConsumers + 32, smem, st>>>(pd, bp, Gt, out, ntiles);
+    }
+  });
+}
+
 bool fast_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, const EpiArgs& ep, int batch,
                    cudaStream_t st) {
   return dispatch_fast(pd, [&](auto q, auto r, auto p) {
@@ -270,7 +300,7 @@ template <>
 void launch_adj_rows<R_>(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, const EpiArgs& ep,
                          int batch, cudaStream_t st) {
   ProfScope prof(st, K_ADJ_ROWS);
-  if (fast_adj_rows(pd, epi, Gt, ep, batch, st)) {
+  if (tma_adj_rows(pd, epi, Gt, ep, batch, st) || fast_adj_rows(pd, epi, Gt, ep, batch, st)) {
     PFTG_LAUNCH_CHECK();
     return;
   }

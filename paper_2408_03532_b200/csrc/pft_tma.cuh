@@ -110,6 +110,10 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (dbg & 2) {  // profiling experiment: pure streaming (keep the loads alive)
+        if (a[0].x == 1234.5f && b[0].y == -1234.5f) acc[0][0].x += 1;
+        continue;
+      }
 #pragma unroll
       for (int v = 0; v < VC; ++v) {
         if (pi == 0) {
@@ -136,6 +140,126 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1)
     if (dbg & 1) continue;  // profiling experiment: streaming + stage A only
     C* Gblk = G + ((size_t)f * pl.p1 + k1) * RR * pl.M2;
     fast_stage_b_to_g<R, Q, RR, P>(pl, bp, T, W2s, tw2s, Gblk, kTmaConsumers / 32);
+  }
+}
+
+template <class R>
+__host__ __device__ inline size_t tma_adj_smem(int n2, int q, int r, int M2, int p) {
+  using C = typename CT<R>::C;
+  size_t b = sizeof(C) * ((size_t)r * ldT_of(n2, q) + (size_t)r * M2 + p / 2 + 1 + 2 * (size_t)r * M2);
+  b = (b + 15) & ~size_t(15);
+  return b + 128 + 4 * sizeof(uint64_t);  // + alignment slack for the bulk-copy buffer
+}
+
+// Persistent adjoint rows pass (pft_adjoint_2d second half, pft.cpp:205-224):
+// a producer warp prefetches each row block's r1 x M2 slice of the adjoint
+// intermediate (contiguous) with one bulk copy into a double buffer, so the
+// D-dagger gather / FFT / B2-dagger phase never waits on global memory; the
+// A-dagger expansion then streams the q1 output rows with 128-bit stores.
+template <class R, int Q, int RR, int P, int VC>
+__global__ void __launch_bounds__(kTmaConsumers + 32, 1)
+    kt_adj_rows(PftDev<R> pl, BPar<R, Q, RR> bp, const typename CT<R>::C* __restrict__ Gt,
+                typename CT<R>::C* __restrict__ out, int ntiles) {
+  using C = typename CT<R>::C;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int n2 = pl.n2, M2 = pl.M2, mt2 = pl.mt2;
+  C* T = reinterpret_cast<C*>(smem_raw);
+  const int ldT = ldT_of(n2, Q);
+  C* W2s = T + (size_t)RR * ldT;
+  C* tw2s = W2s + (size_t)RR * M2;
+  // [2][RR * M2]; bulk-copy destinations must be 16-byte aligned
+  C* gbuf = reinterpret_cast<C*>((reinterpret_cast<uintptr_t>(tw2s + P / 2 + 1) + 127) & ~uintptr_t(127));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(gbuf + 2 * (size_t)RR * M2) + 15) & ~uintptr_t(15));
+  uint64_t* full = bars;
+  uint64_t* empty = bars + 2;
+  fast_load_tables(pl, W2s, tw2s);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const uint32_t blk_bytes = (uint32_t)(RR * M2 * sizeof(C));
+  if (threadIdx.x >= kTmaConsumers) {
+    if (threadIdx.x != kTmaConsumers) return;
+    uint32_t i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int s = i & 1;
+      if (i >= 2) mbar_wait(&empty[s], ((i >> 1) - 1) & 1);
+      mbar_arrive_expect_tx(&full[s], blk_bytes);
+      bulk_g2s(gbuf + (size_t)s * RR * M2, Gt + (size_t)t * RR * M2, blk_bytes, &full[s]);
+    }
+    return;
+  }
+
+  constexpr int PL = P < 32 ? P : 32;
+  constexpr int S = P / PL;
+  constexpr int GPW = 32 / PL;
+  constexpr int LP = (P >= 128) ? 7 : (P >= 64) ? 6 : (P >= 32) ? 5 : (P >= 16) ? 4 : (P >= 8) ? 3 : (P >= 4) ? 2 : 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = kTmaConsumers / 32;
+  const int lig = lane & (PL - 1), giw = lane / PL;
+  uint32_t i = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+    const int s = i & 1;
+    const int f = t / pl.p1, k1 = t % pl.p1;
+    const C* Gblk = gbuf + (size_t)s * RR * M2;
+    mbar_wait(&full[s], (i >> 1) & 1);
+    named_sync(1, kTmaConsumers);  // previous block's A-dagger has finished reading T
+    for (int base = warp * GPW; base < RR; base += NW * GPW) {
+      const int j1 = base + giw;
+      const bool valid = j1 < RR;
+      C x[S][RR];
+#pragma unroll
+      for (int ss = 0; ss < S; ++ss) {
+#pragma unroll
+        for (int j = 0; j < RR; ++j) x[ss][j] = czero<C>();
+        if (valid) {
+          const int u2 = ss * PL + lig;
+          for (int b = (u2 + mt2) & (P - 1); b < M2; b += P) {
+            const C g = Gblk[(size_t)j1 * M2 + b];
+#pragma unroll
+            for (int j = 0; j < RR; ++j) cmacc(x[ss][j], W2s[j * M2 + b], g);
+          }
+        }
+      }
+      fft_dif<S, RR>(x, P, PL, lig, tw2s, +1);
+      if (!valid) continue;
+#pragma unroll
+      for (int ss = 0; ss < S; ++ss) {
+        const int k2 = bitrev(ss * PL + lig, LP);
+        C* trow = T + (size_t)j1 * ldT + (size_t)k2 * (Q + 1);
+        expand_pairs<R, Q, RR>(bp.b2, x[ss], [&](int l, C v) { trow[l] = v; });
+      }
+    }
+    named_sync(1, kTmaConsumers);
+    if (threadIdx.x == 0) mbar_arrive(&empty[s]);  // every consumer is past its gbuf reads
+    // A-dagger: rows k1*Q .. k1*Q+Q-1 of the output field
+    C* o = out + ((size_t)f * pl.n1 + (size_t)k1 * Q) * n2;
+    for (int c = threadIdx.x * VC; c < n2; c += kTmaConsumers * VC) {
+      C tv[VC][RR];
+#pragma unroll
+      for (int v = 0; v < VC; ++v) {
+        const int tc = (c + v) + (c + v) / Q;
+#pragma unroll
+        for (int j = 0; j < RR; ++j) tv[v][j] = T[(size_t)j * ldT + tc];
+      }
+      auto store = [&](int l, const C (&z)[VC]) {
+        if constexpr (VC == 2 && sizeof(C) == 8) {
+          *reinterpret_cast<float4*>(o + (size_t)l * n2 + c) = make_float4(z[0].x, z[0].y, z[VC - 1].x, z[VC - 1].y);
+        } else {
+#pragma unroll
+          for (int v = 0; v < VC; ++v) o[(size_t)l * n2 + c + v] = z[v];
+        }
+      };
+      expand_pairs_v<R, Q, RR, VC>(bp.b1, tv, store, [&](int l, const C (&zl)[VC], const C (&zm)[VC]) {
+        store(l, zl);
+        store(Q - l, zm);
+      });
+    }
   }
 }
 
