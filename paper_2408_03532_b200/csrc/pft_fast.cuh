@@ -176,6 +176,90 @@ __device__ __forceinline__ void expand_pairs_v(const R (&b)[Q / 2 + 1][RR],
   }
 }
 
+// ---- shared-memory coefficient rows (rolled loops: no uniform-register spills) ----
+// Row l of B (RR values) padded to RRP = round_up(RR, 16 bytes) for vector loads.
+template <class R, int RR>
+constexpr int brow_pad() {
+  return sizeof(R) == 4 ? (RR + 3) / 4 * 4 : (RR + 1) / 2 * 2;
+}
+
+template <class R, int Q, int RR>
+__device__ __forceinline__ void stage_btab(const R (&b)[Q / 2 + 1][RR], R* dst) {
+  constexpr int RP = brow_pad<R, RR>();
+  for (int i = threadIdx.x; i < (Q / 2 + 1) * RP; i += blockDim.x) {
+    const int l = i / RP, j = i % RP;
+    dst[i] = j < RR ? b[l][j] : R(0);
+  }
+}
+
+template <class R, int RR>
+__device__ __forceinline__ void load_brow(const R* __restrict__ row, R (&b)[RR]) {
+  constexpr int RP = brow_pad<R, RR>();
+  R t[RP];
+  if constexpr (sizeof(R) == 4) {
+#pragma unroll
+    for (int k = 0; k < RP; k += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(row + k);
+      t[k] = v.x;
+      t[k + 1] = v.y;
+      t[k + 2] = v.z;
+      t[k + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < RP; k += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(row + k);
+      t[k] = v.x;
+      t[k + 1] = v.y;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < RR; ++j) b[j] = t[j];
+}
+
+// expand_pairs_v with the coefficients read from a shared-memory table (btab,
+// rows of brow_pad entries) in a rolled loop over l.
+template <class R, int Q, int RR, int V, class Single, class Pair>
+__device__ __forceinline__ void expand_pairs_sm(const R* __restrict__ btab, const typename CT<R>::C (&x)[V][RR],
+                                                Single&& single, Pair&& pair) {
+  using C = typename CT<R>::C;
+  constexpr int RP = brow_pad<R, RR>();
+  {
+    R b0[RR];
+    load_brow<R, RR>(btab, b0);
+    const R bh = btab[(Q / 2) * RP];
+    C e[V], h[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      e[v] = czero<C>();
+      h[v] = czero<C>();
+#pragma unroll
+      for (int j = 0; j < RR; ++j) bmacc(e[v], b0[j], x[v][j], j & 1);
+      bmacc(h[v], bh, x[v][0], false);
+    }
+    single(0, e);
+    single(Q / 2, h);
+  }
+  // partial unroll: independent pairs overlap their LDS / FMA latency chains
+#pragma unroll 3
+  for (int l = 1; l < Q / 2; ++l) {
+    R bl[RR];
+    load_brow<R, RR>(btab + l * RP, bl);
+    C zl[V], zm[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      C e = czero<C>(), o = czero<C>();
+#pragma unroll
+      for (int j = 0; j < RR; j += 2) bmacc(e, bl[j], x[v][j], false);
+#pragma unroll
+      for (int j = 1; j < RR; j += 2) bmacc(o, bl[j], x[v][j], true);
+      zl[v] = cadd(e, o);
+      zm[v] = csub(e, o);
+    }
+    pair(l, zl, zm);
+  }
+}
+
 // Stage B (+ FFT over k2 + axis-2 band) from T in shared memory, pairing over l2.
 template <class R, int Q, int RR, int P>
 __device__ __forceinline__ void fast_stage_b_to_g(const PftDev<R>& pl, const BPar<R, Q, RR>& bp,

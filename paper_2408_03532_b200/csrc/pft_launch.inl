@@ -170,14 +170,14 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
 bool tma_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, const EpiArgs& ep, int batch,
                   cudaStream_t st) {
   if (epi != 0 || !ep.vec_ok || std::getenv("PFTG_NO_TMA")) return false;
-  int vc = 0;
-  if (pd.n2 == kTmaConsumers) vc = 1;
-  else if (sizeof(R_) == 4 && pd.n2 == 2 * kTmaConsumers) vc = 2;
-  if (!vc) return false;
-  return dispatch_fast(pd, [&](auto q, auto r, auto p) {
+  // P2 owns column pairs (c64) or single columns (c128); any even n2 works
+  const int vc = sizeof(R_) == 4 ? 2 : 1;
+  if (pd.n2 % vc) return false;
+  bool launched = false;
+  const bool matched = dispatch_fast(pd, [&](auto q, auto r, auto p) {
     constexpr int Q = decltype(q)::value, RR = decltype(r)::value, P = decltype(p)::value;
     const size_t smem = tma_adj_smem<R_>(pd.n2, Q, RR, pd.M2, P);
-    if (smem > 227 * 1024) throw std::invalid_argument("pftg: plan too large for the TMA adjoint rows pass");
+    if (smem > 227 * 1024) return;  // double-buffered T does not fit: use kf_adj_rows
     const auto bp = make_bpar<R_, Q, RR>(pd);
     int dev = 0, nsm = 148;
     PFTG_CUDA(cudaGetDevice(&dev));
@@ -185,16 +185,15 @@ bool tma_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, c
     const int ntiles = pd.p1 * batch;
     const int grid = ntiles < nsm ? ntiles : nsm;
     auto* out = reinterpret_cast<typename CT<R_>::C*>(ep.out);
-    if (vc == 2) {
-      auto k = kt_adj_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
-      allow_smem(k);
-      k<<<grid, kTmaConsumers + 32, smem, st>>>(pd, bp, Gt, out, ntiles);
-    } else {
-      auto k = kt_adj_rows<R_, Q, RR, P, 1>;
-      allow_smem(k);
-      k<<<grid, kTmaConsumers + 32, smem, st>>>(pd, bp, Gt, out, ntiles);
-    }
+    const char* dv = std::getenv("PFTG_DEBUG_ADJ");
+    const int dbg = dv ? std::atoi(dv) : 0;
+    constexpr int NT = 32 * (adj_p1_warps<RR, P>() + kAdjP2Warps);
+    auto k = kt_adj_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
+    allow_smem(k);
+    k<<<grid, NT, smem, st>>>(pd, bp, Gt, out, ntiles, dbg);
+    launched = true;
   });
+  return matched && launched;
 }
 
 bool fast_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, const EpiArgs& ep, int batch,

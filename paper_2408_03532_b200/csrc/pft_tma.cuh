@@ -41,8 +41,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1)
   const int ldT = ldT_of(n2, Q);
   C* W2s = T + (size_t)RR * ldT;
   C* tw2s = W2s + (size_t)RR * pl.M2;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(tw2s + P / 2 + 1) + 15) & ~uintptr_t(15));
+  uint64_t* bars = smem_after<uint64_t>(smem_raw, tw2s + P / 2 + 1, 16);
   uint64_t* full = bars;
   uint64_t* empty = bars + NS;
 
@@ -143,123 +142,174 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialized persistent adjoint rows pass (pft_adjoint_2d second half,
+// pft.cpp:205-224). One CTA per SM loops over (field, k1) row blocks:
+//   group P1 (one warp per j1): D-dagger gather of the block's r1 x M2 slice
+//     (prefetched by a 1-D bulk copy into a double buffer), inverse FFT over
+//     k2 in registers, B2-dagger expansion with row-pair symmetry -> T[i & 1];
+//   group P2 (10 warps): A-dagger expansion of T[i & 1] with row-pair symmetry
+//     and 128-bit streaming stores of the q1 output rows.
+// T is double-buffered, so P1 builds block i+1 while P2 writes block i; the two
+// groups hand off through mbarriers (tready / tfree). W2 is read through L1.
+constexpr int kAdjP2Warps = 10;
+
+template <int RR, int P>
+constexpr int adj_p1_warps() {
+  constexpr int gpw = 32 / (P < 32 ? P : 32);
+  return (RR + gpw - 1) / gpw;
+}
+
 template <class R>
 __host__ __device__ inline size_t tma_adj_smem(int n2, int q, int r, int M2, int p) {
   using C = typename CT<R>::C;
-  size_t b = sizeof(C) * ((size_t)r * ldT_of(n2, q) + (size_t)r * M2 + p / 2 + 1 + 2 * (size_t)r * M2);
+  size_t b = sizeof(C) * (2 * (size_t)r * ldT_of(n2, q) + p / 2 + 1 + 2 * (size_t)r * M2);
   b = (b + 15) & ~size_t(15);
-  return b + 128 + 4 * sizeof(uint64_t);  // + alignment slack for the bulk-copy buffer
+  return b + 128 + 8 * sizeof(uint64_t) + 4096;  // alignment slack, barriers, coefficient tables
 }
 
-// Persistent adjoint rows pass (pft_adjoint_2d second half, pft.cpp:205-224):
-// a producer warp prefetches each row block's r1 x M2 slice of the adjoint
-// intermediate (contiguous) with one bulk copy into a double buffer, so the
-// D-dagger gather / FFT / B2-dagger phase never waits on global memory; the
-// A-dagger expansion then streams the q1 output rows with 128-bit stores.
 template <class R, int Q, int RR, int P, int VC>
-__global__ void __launch_bounds__(kTmaConsumers + 32, 1)
+__global__ void __launch_bounds__(32 * (adj_p1_warps<RR, P>() + kAdjP2Warps), 1)
     kt_adj_rows(PftDev<R> pl, BPar<R, Q, RR> bp, const typename CT<R>::C* __restrict__ Gt,
-                typename CT<R>::C* __restrict__ out, int ntiles) {
+                typename CT<R>::C* __restrict__ out, int ntiles, int dbg) {
   using C = typename CT<R>::C;
+  constexpr int NP1 = adj_p1_warps<RR, P>();
+  constexpr int P1T = 32 * NP1, P2T = 32 * kAdjP2Warps;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int n2 = pl.n2, M2 = pl.M2, mt2 = pl.mt2;
-  C* T = reinterpret_cast<C*>(smem_raw);
   const int ldT = ldT_of(n2, Q);
-  C* W2s = T + (size_t)RR * ldT;
-  C* tw2s = W2s + (size_t)RR * M2;
-  // [2][RR * M2]; bulk-copy destinations must be 16-byte aligned
-  C* gbuf = reinterpret_cast<C*>((reinterpret_cast<uintptr_t>(tw2s + P / 2 + 1) + 127) & ~uintptr_t(127));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(gbuf + 2 * (size_t)RR * M2) + 15) & ~uintptr_t(15));
-  uint64_t* full = bars;
-  uint64_t* empty = bars + 2;
-  fast_load_tables(pl, W2s, tw2s);
+  C* Tb = reinterpret_cast<C*>(smem_raw);  // [2][RR][ldT]
+  C* tw2s = Tb + 2 * (size_t)RR * ldT;
+  constexpr int RP = brow_pad<R, RR>();
+  R* btab1 = smem_after<R>(smem_raw, tw2s + P / 2 + 1, 16);
+  R* btab2 = btab1 + (Q / 2 + 1) * RP;
+  C* gbuf = smem_after<C>(smem_raw, btab2 + (Q / 2 + 1) * RP, 128);  // [2][RR * M2]
+  uint64_t* bars = smem_after<uint64_t>(smem_raw, gbuf + 2 * (size_t)RR * M2, 16);
+  uint64_t* gfull = bars;       // TMA -> P1
+  uint64_t* tready = bars + 2;  // P1 -> P2
+  uint64_t* tfree = bars + 4;   // P2 -> P1
+  const C* W2g = pl.W2t;        // L1-resident table
+
+  for (int i = threadIdx.x; i < P / 2; i += blockDim.x) tw2s[i] = pl.tw2[i];
+  stage_btab<R, Q, RR>(bp.b1, btab1);
+  stage_btab<R, Q, RR>(bp.b2, btab2);
+  const uint32_t blk_bytes = (uint32_t)(RR * M2 * sizeof(C));
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&gfull[s], 1);
+      mbar_init(&tready[s], 1);
+      mbar_init(&tfree[s], 1);
     }
     mbar_fence_init();
+    for (int s = 0; s < 2; ++s) {  // prefetch the first two blocks
+      const int t = blockIdx.x + s * gridDim.x;
+      if (t < ntiles) {
+        mbar_arrive_expect_tx(&gfull[s], blk_bytes);
+        bulk_g2s(gbuf + (size_t)s * RR * M2, Gt + (size_t)t * RR * M2, blk_bytes, &gfull[s]);
+      }
+    }
   }
   __syncthreads();
-  const uint32_t blk_bytes = (uint32_t)(RR * M2 * sizeof(C));
-  if (threadIdx.x >= kTmaConsumers) {
-    if (threadIdx.x != kTmaConsumers) return;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp < NP1) {
+    // ---------------- P1: gather + inverse FFT + B2-dagger -> T ----------------
+    constexpr int PL = P < 32 ? P : 32;
+    constexpr int S = P / PL;
+    constexpr int GPW = 32 / PL;
+    constexpr int LP = (P >= 128) ? 7 : (P >= 64) ? 6 : (P >= 32) ? 5 : (P >= 16) ? 4 : (P >= 8) ? 3 : (P >= 4) ? 2 : 1;
+    const int lig = lane & (PL - 1), giw = lane / PL;
+    const int j1 = warp * GPW + giw;
+    const bool valid = j1 < RR;
     uint32_t i = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
       const int s = i & 1;
-      if (i >= 2) mbar_wait(&empty[s], ((i >> 1) - 1) & 1);
-      mbar_arrive_expect_tx(&full[s], blk_bytes);
-      bulk_g2s(gbuf + (size_t)s * RR * M2, Gt + (size_t)t * RR * M2, blk_bytes, &full[s]);
+      const C* Gblk = gbuf + (size_t)s * RR * M2;
+      C* T = Tb + (size_t)s * RR * ldT;
+      mbar_wait(&gfull[s], (i >> 1) & 1);
+      if (i >= 2) mbar_wait(&tfree[s], ((i >> 1) - 1) & 1);
+      if (!(dbg & 1)) {
+        C x[S][RR];
+#pragma unroll
+        for (int ss = 0; ss < S; ++ss) {
+#pragma unroll
+          for (int j = 0; j < RR; ++j) x[ss][j] = czero<C>();
+          if (valid) {
+            const int u2 = ss * PL + lig;
+            for (int b = (u2 + mt2) & (P - 1); b < M2; b += P) {
+              const C g = Gblk[(size_t)j1 * M2 + b];
+#pragma unroll
+              for (int j = 0; j < RR; ++j) cmacc(x[ss][j], __ldg(W2g + j * M2 + b), g);
+            }
+          }
+        }
+        fft_dif<S, RR>(x, P, PL, lig, tw2s, +1);
+        if (valid) {
+#pragma unroll
+          for (int ss = 0; ss < S; ++ss) {
+            const int k2 = bitrev(ss * PL + lig, LP);
+            C* trow = T + (size_t)j1 * ldT + (size_t)k2 * (Q + 1);
+            C xs[1][RR];
+#pragma unroll
+            for (int j = 0; j < RR; ++j) xs[0][j] = x[ss][j];
+            expand_pairs_sm<R, Q, RR, 1>(
+                btab2, xs, [&](int l, const C (&z)[1]) { trow[l] = z[0]; },
+                [&](int l, const C (&zl)[1], const C (&zm)[1]) {
+                  trow[l] = zl[0];
+                  trow[Q - l] = zm[0];
+                });
+          }
+        }
+      }
+      named_sync(1, P1T);  // all of P1 is done with gbuf[s] and T[s]
+      if (threadIdx.x == 0) {
+        mbar_arrive(&tready[s]);
+        const int tn = t + 2 * (int)gridDim.x;
+        if (tn < ntiles) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive_expect_tx(&gfull[s], blk_bytes);
+          bulk_g2s(gbuf + (size_t)s * RR * M2, Gt + (size_t)tn * RR * M2, blk_bytes, &gfull[s]);
+        }
+      }
     }
     return;
   }
 
-  constexpr int PL = P < 32 ? P : 32;
-  constexpr int S = P / PL;
-  constexpr int GPW = 32 / PL;
-  constexpr int LP = (P >= 128) ? 7 : (P >= 64) ? 6 : (P >= 32) ? 5 : (P >= 16) ? 4 : (P >= 8) ? 3 : (P >= 4) ? 2 : 1;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int NW = kTmaConsumers / 32;
-  const int lig = lane & (PL - 1), giw = lane / PL;
+  // ---------------- P2: A-dagger expansion + streaming stores ----------------
+  const int tid = threadIdx.x - P1T;
   uint32_t i = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
     const int s = i & 1;
     const int f = t / pl.p1, k1 = t % pl.p1;
-    const C* Gblk = gbuf + (size_t)s * RR * M2;
-    mbar_wait(&full[s], (i >> 1) & 1);
-    named_sync(1, kTmaConsumers);  // previous block's A-dagger has finished reading T
-    for (int base = warp * GPW; base < RR; base += NW * GPW) {
-      const int j1 = base + giw;
-      const bool valid = j1 < RR;
-      C x[S][RR];
-#pragma unroll
-      for (int ss = 0; ss < S; ++ss) {
-#pragma unroll
-        for (int j = 0; j < RR; ++j) x[ss][j] = czero<C>();
-        if (valid) {
-          const int u2 = ss * PL + lig;
-          for (int b = (u2 + mt2) & (P - 1); b < M2; b += P) {
-            const C g = Gblk[(size_t)j1 * M2 + b];
-#pragma unroll
-            for (int j = 0; j < RR; ++j) cmacc(x[ss][j], W2s[j * M2 + b], g);
-          }
-        }
-      }
-      fft_dif<S, RR>(x, P, PL, lig, tw2s, +1);
-      if (!valid) continue;
-#pragma unroll
-      for (int ss = 0; ss < S; ++ss) {
-        const int k2 = bitrev(ss * PL + lig, LP);
-        C* trow = T + (size_t)j1 * ldT + (size_t)k2 * (Q + 1);
-        expand_pairs<R, Q, RR>(bp.b2, x[ss], [&](int l, C v) { trow[l] = v; });
-      }
-    }
-    named_sync(1, kTmaConsumers);
-    if (threadIdx.x == 0) mbar_arrive(&empty[s]);  // every consumer is past its gbuf reads
-    // A-dagger: rows k1*Q .. k1*Q+Q-1 of the output field
+    const C* T = Tb + (size_t)s * RR * ldT;
+    mbar_wait(&tready[s], (i >> 1) & 1);
     C* o = out + ((size_t)f * pl.n1 + (size_t)k1 * Q) * n2;
-    for (int c = threadIdx.x * VC; c < n2; c += kTmaConsumers * VC) {
-      C tv[VC][RR];
+    if (!(dbg & 4)) {
+      for (int c = tid * VC; c < n2; c += P2T * VC) {
+        C tv[VC][RR];
 #pragma unroll
-      for (int v = 0; v < VC; ++v) {
-        const int tc = (c + v) + (c + v) / Q;
+        for (int v = 0; v < VC; ++v) {
+          const int tc = (c + v) + (c + v) / Q;
 #pragma unroll
-        for (int j = 0; j < RR; ++j) tv[v][j] = T[(size_t)j * ldT + tc];
-      }
-      auto store = [&](int l, const C (&z)[VC]) {
-        if constexpr (VC == 2 && sizeof(C) == 8) {
-          *reinterpret_cast<float4*>(o + (size_t)l * n2 + c) = make_float4(z[0].x, z[0].y, z[VC - 1].x, z[VC - 1].y);
-        } else {
-#pragma unroll
-          for (int v = 0; v < VC; ++v) o[(size_t)l * n2 + c + v] = z[v];
+          for (int j = 0; j < RR; ++j) tv[v][j] = T[(size_t)j * ldT + tc];
         }
-      };
-      expand_pairs_v<R, Q, RR, VC>(bp.b1, tv, store, [&](int l, const C (&zl)[VC], const C (&zm)[VC]) {
-        store(l, zl);
-        store(Q - l, zm);
-      });
+        auto store = [&](int l, const C (&z)[VC]) {
+          if ((dbg & 2) && z[0].x != R(12345.5)) return;
+          if constexpr (VC == 2 && sizeof(C) == 8) {
+            *reinterpret_cast<float4*>(o + (size_t)l * n2 + c) = make_float4(z[0].x, z[0].y, z[VC - 1].x, z[VC - 1].y);
+          } else {
+#pragma unroll
+            for (int v = 0; v < VC; ++v) o[(size_t)l * n2 + c + v] = z[v];
+          }
+        };
+        expand_pairs_sm<R, Q, RR, VC>(btab1, tv, store, [&](int l, const C (&zl)[VC], const C (&zm)[VC]) {
+          store(l, zl);
+          store(Q - l, zm);
+        });
+      }
     }
+    named_sync(2, P2T);  // all of P2 is done reading T[s]
+    if (tid == 0) mbar_arrive(&tfree[s]);
   }
 }
 

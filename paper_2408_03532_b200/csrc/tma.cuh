@@ -55,6 +55,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Aligned carve-out of dynamic shared memory that keeps the pointer derived
+// from `base` (so the compiler still emits LDS/STS, not generic loads).
+template <class T>
+__device__ __forceinline__ T* smem_after(unsigned char* base, const void* after, size_t align) {
+  size_t off = static_cast<size_t>(static_cast<const unsigned char*>(after) - base);
+  off = (off + align - 1) & ~(align - 1);
+  return reinterpret_cast<T*>(base + off);
+}
+
 // Named barrier over `count` threads (multiple of 32), id != 0.
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
