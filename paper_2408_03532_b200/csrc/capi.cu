@@ -283,16 +283,16 @@ template <class R>
 void apply_dev(const pftg_plan* plan, const void* z, void* band, std::size_t batch, cudaStream_t st) {
   const PftDev<R>& pd = plan_dev<R>(*plan);
   const std::size_t chunk = std::min(batch, chunk_fields(pd));
-  const std::size_t gsz = (std::size_t)pd.p1 * pd.r1 * pd.M2;
+  const std::size_t gsz = (std::size_t)g_field_elems<R>(pd);
   Scratch G(sizeof(Cx<R>) * gsz * chunk, st);
   const std::size_t nz = (std::size_t)pd.n1 * pd.n2, nb = (std::size_t)pd.M1 * pd.M2;
   for (std::size_t b0 = 0; b0 < batch; b0 += chunk) {
     const int nbat = static_cast<int>(std::min(chunk, batch - b0));
     Src<R> src{static_cast<const Cx<R>*>(z) + b0 * nz, pd.n2, (long long)nz, nullptr, nullptr,
                vec_ok(z, pd.n2, nz)};
-    launch_fwd_rows<R>(pd, src, G.as<Cx<R>>(), nbat, st);
+    const bool strip = launch_fwd_rows<R>(pd, src, G.as<Cx<R>>(), nbat, st, vec_ok(band, pd.M2, nb));
     launch_fwd_cols<R>(pd, 0, G.as<Cx<R>>(), static_cast<Cx<R>*>(band) + b0 * nb, nullptr, 0, nullptr, nullptr,
-                       nbat, st);
+                       nbat, st, strip);
   }
 }
 

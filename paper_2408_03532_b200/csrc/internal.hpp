@@ -66,14 +66,20 @@ template <class R>
 const PftDev<R>& plan_dev(const pftg_plan& p);
 
 // ---- PFT building blocks (pft_launch_*.cu); all stream-ordered ----
+// Returns true when G was written in the strip-major layout (only if
+// want_strip and the persistent cols kernel handles the plan); pass that
+// flag to launch_fwd_cols.
 template <class R>
-void launch_fwd_rows(const PftDev<R>& pd, const Src<R>& src, typename CT<R>::C* G, int batch,
-                     cudaStream_t st);
+bool launch_fwd_rows(const PftDev<R>& pd, const Src<R>& src, typename CT<R>::C* G, int batch,
+                     cudaStream_t st, bool want_strip = false);
 // mode 0: band out; 1: residual -> Gout; 2: evaluator partials [batch][cols_strips]
 template <class R>
 void launch_fwd_cols(const PftDev<R>& pd, int mode, const typename CT<R>::C* G, typename CT<R>::C* band,
                      const R* dcrop, long long dstride, typename CT<R>::C* Gout, double* partial, int batch,
-                     cudaStream_t st);
+                     cudaStream_t st, bool strip = false);
+// G elements per field needed by either layout
+template <class R>
+long long g_field_elems(const PftDev<R>& pd);
 template <class R>
 int cols_strips(const PftDev<R>& pd);
 template <class R>

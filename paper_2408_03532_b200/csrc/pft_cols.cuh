@@ -1,0 +1,234 @@
+// Persistent cols passes for the specialized plan shapes (batched PFT).
+//
+// The cols pass of the forward PFT (FFT over k1 + axis-1 band contraction,
+// the k1 half of pft.cpp:147-170) and of the adjoint (the D-dagger gather over
+// a + backward FFT over u1, pft.cpp:184-205) touch only ~16 % of a field's
+// bytes but were latency-bound as one-shot CTAs. Here each CTA loops over
+// band strips of kStripNB columns and double-buffers its input:
+//  * forward: the rows pass writes G strip-major (pft_fast.cuh), so a strip is
+//    one contiguous 1-D bulk copy (cp.async.bulk) issued one iteration ahead;
+//  * adjoint: the band strip (kStripNB columns of every row) is prefetched into
+//    registers one iteration ahead and parked in shared memory.
+#pragma once
+
+#include "pft_fast.cuh"
+#include "tma.cuh"
+
+namespace pftg {
+
+constexpr int kColsThreads = 256;
+
+// Elements per field of the strip-major G layout.
+template <class R>
+__host__ inline long long strip_field_elems(const PftDev<R>& pd) {
+  return (long long)(pd.M2 / kStripNB) * pd.p1 * strip_rec(pd.r1);
+}
+
+template <class R>
+__host__ __device__ inline size_t cols_fwd_smem(int p1, int r, int M1) {
+  using C = typename CT<R>::C;
+  size_t b = sizeof(C) * (2 * (size_t)p1 * strip_rec(r) + (size_t)M1 * (kStripNB + 1) + p1 / 2 + 1);
+  return ((b + 15) & ~size_t(15)) + 128 + 2 * sizeof(uint64_t);
+}
+
+template <class R, int RR, int P>
+__global__ void __launch_bounds__(kColsThreads, 2)
+    kc_fwd_cols(PftDev<R> pl, const typename CT<R>::C* __restrict__ G, long long gstride,
+                typename CT<R>::C* __restrict__ band, int nstrips_field, int ntotal) {
+  using C = typename CT<R>::C;
+  constexpr int REC = strip_rec(RR);
+  constexpr int PL = P < 32 ? P : 32;
+  constexpr int S = P / PL;
+  constexpr int GPW = 32 / PL;
+  constexpr int LP = (P >= 128) ? 7 : (P >= 64) ? 6 : (P >= 32) ? 5 : (P >= 16) ? 4 : (P >= 8) ? 3 : (P >= 4) ? 2 : 1;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int M1 = pl.M1, M2 = pl.M2, mt1 = pl.mt1;
+  const int sbytes_e = P * REC;  // elements per strip
+  C* buf = reinterpret_cast<C*>(smem_raw);  // [2][P * REC]
+  C* Ys = buf + 2 * (size_t)sbytes_e;       // [M1][kStripNB + 1]
+  C* tw1s = Ys + (size_t)M1 * (kStripNB + 1);
+  uint64_t* full = smem_after<uint64_t>(smem_raw, tw1s + P / 2 + 1, 16);
+  const uint32_t strip_bytes = (uint32_t)(sbytes_e * sizeof(C));
+  for (int i = threadIdx.x; i < P / 2; i += blockDim.x) tw1s[i] = pl.tw1[i];
+  auto strip_src = [&](int sg) {
+    const int f = sg / nstrips_field, st = sg % nstrips_field;
+    return G + (size_t)f * gstride + (size_t)st * sbytes_e;
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_fence_init();
+    for (int s = 0; s < 2; ++s) {
+      const int sg = blockIdx.x + s * gridDim.x;
+      if (sg < ntotal) {
+        mbar_arrive_expect_tx(&full[s], strip_bytes);
+        bulk_g2s(buf + (size_t)s * sbytes_e, strip_src(sg), strip_bytes, &full[s]);
+      }
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lig = lane & (PL - 1), giw = lane / PL;
+  const int bb = warp * GPW + giw;  // band column within the strip (kColsThreads/32*GPW >= kStripNB)
+  const bool valid = bb < kStripNB;
+  uint32_t i = 0;
+  for (int sg = blockIdx.x; sg < ntotal; sg += gridDim.x, ++i) {
+    const int s = i & 1;
+    const int f = sg / nstrips_field, b0 = (sg % nstrips_field) * kStripNB;
+    const C* sb = buf + (size_t)s * sbytes_e;
+    mbar_wait(&full[s], (i >> 1) & 1);
+    C x[S][RR];
+#pragma unroll
+    for (int ss = 0; ss < S; ++ss) {
+      const int k1 = ss * PL + lig;
+#pragma unroll
+      for (int j = 0; j < RR; ++j) x[ss][j] = valid ? sb[(size_t)k1 * REC + j * kStripNB + bb] : czero<C>();
+    }
+    fft_dif<S, RR>(x, P, PL, lig, tw1s, -1);
+    if (valid) {
+#pragma unroll
+      for (int ss = 0; ss < S; ++ss) {
+        const int u1 = bitrev(ss * PL + lig, LP);
+        band_contract<RR>(pl.W1t, M1, (u1 + mt1) & (P - 1), P, RR, x[ss],
+                          [&](int a, C v) { Ys[(size_t)a * (kStripNB + 1) + bb] = v; });
+      }
+    }
+    __syncthreads();  // strip buffer s consumed, Ys complete
+    if (threadIdx.x == 0 && sg + 2 * (int)gridDim.x < ntotal) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(&full[s], strip_bytes);
+      bulk_g2s(buf + (size_t)s * sbytes_e, strip_src(sg + 2 * gridDim.x), strip_bytes, &full[s]);
+    }
+    // band rows a, columns b0 .. b0+7: 4 threads x 2 columns per row (64-byte segments)
+    C* bf = band + (size_t)f * M1 * M2 + b0;
+    for (int e = threadIdx.x; e < M1 * (kStripNB / 2); e += blockDim.x) {
+      const int a = e / (kStripNB / 2), cc = (e % (kStripNB / 2)) * 2;
+      const C v0 = Ys[(size_t)a * (kStripNB + 1) + cc], v1 = Ys[(size_t)a * (kStripNB + 1) + cc + 1];
+      if constexpr (sizeof(C) == 8) {
+        *reinterpret_cast<float4*>(bf + (size_t)a * M2 + cc) = make_float4(v0.x, v0.y, v1.x, v1.y);
+      } else {
+        bf[(size_t)a * M2 + cc] = v0;
+        bf[(size_t)a * M2 + cc + 1] = v1;
+      }
+    }
+    __syncthreads();  // Ys free for the next strip
+  }
+}
+
+template <class R>
+__host__ __device__ inline size_t cols_adj_smem(int p1, int r, int M1) {
+  using C = typename CT<R>::C;
+  size_t b = sizeof(C) * ((size_t)M1 * (kStripNB + 1) + (size_t)p1 * (r * kStripNB + 1) + p1 / 2 + 1);
+  return ((b + 15) & ~size_t(15)) + 128;
+}
+
+// Adjoint cols pass: band strip -> Gt[f][k1][j1][b] (row-block layout read by
+// the adjoint rows pass). The next strip's band values are loaded into
+// registers while the current strip is transformed.
+template <class R, int RR, int P>
+__global__ void __launch_bounds__(kColsThreads, 2)
+    kc_adj_cols(PftDev<R> pl, const typename CT<R>::C* __restrict__ band, typename CT<R>::C* __restrict__ Gt,
+                int nstrips_field, int ntotal) {
+  using C = typename CT<R>::C;
+  constexpr int PL = P < 32 ? P : 32;
+  constexpr int S = P / PL;
+  constexpr int GPW = 32 / PL;
+  constexpr int LP = (P >= 128) ? 7 : (P >= 64) ? 6 : (P >= 32) ? 5 : (P >= 16) ? 4 : (P >= 8) ? 3 : (P >= 4) ? 2 : 1;
+  constexpr int LDY = kStripNB + 1;
+  constexpr int GREC = RR * kStripNB + 1;  // padded per-k1 record: conflict-free k1-strided writes
+  // per-thread share of a strip: M1 rows x kStripNB columns, 2 columns per item
+  constexpr int MAXIT = 8;  // supports M1 * kStripNB / 2 <= kColsThreads * MAXIT
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int M1 = pl.M1, M2 = pl.M2, mt1 = pl.mt1;
+  C* Ys = reinterpret_cast<C*>(smem_raw);  // [M1][LDY]
+  C* Gs = Ys + (size_t)M1 * LDY;           // [P][GREC]
+  C* tw1s = Gs + (size_t)P * GREC;
+  for (int i = threadIdx.x; i < P / 2; i += blockDim.x) tw1s[i] = pl.tw1[i];
+  const int items = M1 * (kStripNB / 2);
+  C pre[MAXIT][2];
+  auto prefetch = [&](int sg) {
+    const int f = sg / nstrips_field, b0 = (sg % nstrips_field) * kStripNB;
+    const C* bf = band + (size_t)f * M1 * M2 + b0;
+#pragma unroll
+    for (int it = 0; it < MAXIT; ++it) {
+      const int e = threadIdx.x + it * kColsThreads;
+      if (e < items) {
+        const int a = e / (kStripNB / 2), cc = (e % (kStripNB / 2)) * 2;
+        if constexpr (sizeof(C) == 8) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(bf + (size_t)a * M2 + cc));
+          pre[it][0] = CT<R>::mk(v.x, v.y);
+          pre[it][1] = CT<R>::mk(v.z, v.w);
+        } else {
+          pre[it][0] = __ldg(bf + (size_t)a * M2 + cc);
+          pre[it][1] = __ldg(bf + (size_t)a * M2 + cc + 1);
+        }
+      }
+    }
+  };
+  auto park = [&]() {
+#pragma unroll
+    for (int it = 0; it < MAXIT; ++it) {
+      const int e = threadIdx.x + it * kColsThreads;
+      if (e < items) {
+        const int a = e / (kStripNB / 2), cc = (e % (kStripNB / 2)) * 2;
+        Ys[(size_t)a * LDY + cc] = pre[it][0];
+        Ys[(size_t)a * LDY + cc + 1] = pre[it][1];
+      }
+    }
+  };
+  if ((int)blockIdx.x < ntotal) {
+    prefetch(blockIdx.x);
+    park();
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lig = lane & (PL - 1), giw = lane / PL;
+  const int bb = warp * GPW + giw;
+  const bool valid = bb < kStripNB;
+  for (int sg = blockIdx.x; sg < ntotal; sg += gridDim.x) {
+    const int f = sg / nstrips_field, b0 = (sg % nstrips_field) * kStripNB;
+    const bool more = sg + (int)gridDim.x < ntotal;
+    if (more) prefetch(sg + gridDim.x);  // in flight during the transform below
+    C x[S][RR];
+#pragma unroll
+    for (int ss = 0; ss < S; ++ss) {
+#pragma unroll
+      for (int j = 0; j < RR; ++j) x[ss][j] = czero<C>();
+      if (valid) {
+        const int u1 = ss * PL + lig;
+        for (int a = (u1 + mt1) & (P - 1); a < M1; a += P) {
+          const C y = Ys[(size_t)a * LDY + bb];
+#pragma unroll
+          for (int j = 0; j < RR; ++j) cmacc(x[ss][j], __ldg(pl.W1t + j * M1 + a), y);
+        }
+      }
+    }
+    fft_dif<S, RR>(x, P, PL, lig, tw1s, +1);
+    if (valid) {
+#pragma unroll
+      for (int ss = 0; ss < S; ++ss) {
+        const int k1 = bitrev(ss * PL + lig, LP);
+#pragma unroll
+        for (int j = 0; j < RR; ++j) Gs[(size_t)k1 * GREC + j * kStripNB + bb] = x[ss][j];
+      }
+    }
+    __syncthreads();  // Ys consumed, Gs complete
+    // Gt[f][k1][j1][b0 .. b0+7]: 64-byte segments, 2 columns per item
+    C* gf = Gt + (size_t)f * P * RR * M2 + b0;
+    for (int e = threadIdx.x; e < P * RR * (kStripNB / 2); e += blockDim.x) {
+      const int kj = e / (kStripNB / 2), cc = (e % (kStripNB / 2)) * 2;
+      const int k1 = kj / RR, j = kj % RR;
+      const C v0 = Gs[(size_t)k1 * GREC + j * kStripNB + cc], v1 = Gs[(size_t)k1 * GREC + j * kStripNB + cc + 1];
+      if constexpr (sizeof(C) == 8) {
+        *reinterpret_cast<float4*>(gf + (size_t)kj * M2 + cc) = make_float4(v0.x, v0.y, v1.x, v1.y);
+      } else {
+        gf[(size_t)kj * M2 + cc] = v0;
+        gf[(size_t)kj * M2 + cc + 1] = v1;
+      }
+    }
+    if (more) park();
+    __syncthreads();  // Ys refilled, Gs drained
+  }
+}
+
+}  // namespace pftg

@@ -260,12 +260,21 @@ __device__ __forceinline__ void expand_pairs_sm(const R* __restrict__ btab, cons
   }
 }
 
+// Strip-major layout of the rows -> cols intermediate used by the persistent
+// cols pass (pft_cols.cuh): G[f][b / kStripNB][k1][j1 * kStripNB + b % kStripNB],
+// each (strip, k1) record padded by one element (conflict-free k1-strided reads).
+constexpr int kStripNB = 8;
+__host__ __device__ constexpr int strip_rec(int r) { return r * kStripNB + 1; }
+
 // Stage B (+ FFT over k2 + axis-2 band) from T in shared memory, pairing over l2.
+// Output: Gblk[j1][b] (row-block layout) or, when gstrip != nullptr, the
+// strip-major layout of field gstrip for row block k1.
 template <class R, int Q, int RR, int P>
 __device__ __forceinline__ void fast_stage_b_to_g(const PftDev<R>& pl, const BPar<R, Q, RR>& bp,
                                                   const typename CT<R>::C* T, const typename CT<R>::C* W2s,
                                                   const typename CT<R>::C* tw2, typename CT<R>::C* Gblk,
-                                                  int nwarps = -1) {
+                                                  int nwarps = -1, typename CT<R>::C* gstrip = nullptr,
+                                                  int k1 = 0) {
   using C = typename CT<R>::C;
   constexpr int PL = P < 32 ? P : 32;
   constexpr int S = P / PL;
@@ -306,8 +315,15 @@ __device__ __forceinline__ void fast_stage_b_to_g(const PftDev<R>& pl, const BPa
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int u2 = bitrev(s * PL + lig, LP);
-      band_contract<RR>(W2s, M2, (u2 + mt2) & (P - 1), P, RR, x[s],
-                        [&](int b, C v) { Gblk[(size_t)j1 * M2 + b] = v; });
+      if (gstrip) {
+        constexpr int REC = strip_rec(RR);
+        band_contract<RR>(W2s, M2, (u2 + mt2) & (P - 1), P, RR, x[s], [&](int b, C v) {
+          gstrip[((size_t)(b / kStripNB) * pl.p1 + k1) * REC + j1 * kStripNB + (b % kStripNB)] = v;
+        });
+      } else {
+        band_contract<RR>(W2s, M2, (u2 + mt2) & (P - 1), P, RR, x[s],
+                          [&](int b, C v) { Gblk[(size_t)j1 * M2 + b] = v; });
+      }
     }
   }
 }

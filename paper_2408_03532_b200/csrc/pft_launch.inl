@@ -11,6 +11,7 @@
 #include "internal.hpp"
 #include "pft_fast.cuh"
 #include "pft_tma.cuh"
+#include "pft_cols.cuh"
 
 namespace pftg {
 
@@ -105,6 +106,25 @@ bool dispatch_fast(const PftDev<R>& pd, F&& f) {
   return false;
 }
 
+int sm_count() {
+  int dev = 0, nsm = 148;
+  PFTG_CUDA(cudaGetDevice(&dev));
+  PFTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  return nsm;
+}
+
+// The persistent cols kernels (pft_cols.cuh) handle this plan.
+template <class R>
+bool fast_cols_ok(const PftDev<R>& pd) {
+  if (pd.M2 % kStripNB || pd.M1 * (kStripNB / 2) > kColsThreads * 8) return false;
+  bool ok = false;
+  dispatch_fast(pd, [&](auto, auto r, auto p) {
+    constexpr int RR = decltype(r)::value, P = decltype(p)::value;
+    ok = cols_fwd_smem<R>(P, RR, pd.M1) <= 227 * 1024 && cols_adj_smem<R>(P, RR, pd.M1) <= 227 * 1024;
+  });
+  return ok;
+}
+
 }  // namespace
 
 using R_ = PFTG_REAL;
@@ -133,7 +153,9 @@ bool fast_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C*
 
 // Persistent TMA-fed rows pass (pft_tma.cuh) for plain batched fields whose
 // rows are whole 16-byte multiples and span exactly 512 x {1,2} columns.
-bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* G, int batch, cudaStream_t st) {
+bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* G, int batch, cudaStream_t st,
+                  bool strip) {
+  const long long gstride = strip ? strip_field_elems(pd) : 0;
   if (src.offs || src.probe || !src.vec_ok) return false;
   if (std::getenv("PFTG_NO_TMA")) return false;
   int vc = 0;
@@ -158,11 +180,13 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
     if (vc == 2) {
       auto k = kt_fwd_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
       allow_smem(k);
-      k<<<grid, kTmaConsumers + 32, smem, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns, G, dbg);
+      k<<<grid, kTmaConsumers + 32, smem, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns, G, dbg,
+                                                gstride);
     } else {
       auto k = kt_fwd_rows<R_, Q, RR, P, 1>;
       allow_smem(k);
-      k<<<grid, kTmaConsumers + 32, smem, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns, G, dbg);
+      k<<<grid, kTmaConsumers + 32, smem, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns, G, dbg,
+                                                gstride);
     }
   });
 }
@@ -226,12 +250,18 @@ bool fast_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, 
 }  // namespace
 
 template <>
-void launch_fwd_rows<R_>(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* G, int batch,
-                         cudaStream_t st) {
+bool launch_fwd_rows<R_>(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* G, int batch,
+                         cudaStream_t st, bool want_strip) {
   ProfScope prof(st, K_FWD_ROWS);
-  if (tma_fwd_rows(pd, src, G, batch, st) || fast_fwd_rows(pd, src, G, batch, st)) {
+  // strip-major G only when the persistent cols kernel can consume it
+  const bool strip = want_strip && fast_cols_ok(pd);
+  if (tma_fwd_rows(pd, src, G, batch, st, strip)) {
     PFTG_LAUNCH_CHECK();
-    return;
+    return strip;
+  }
+  if (fast_fwd_rows(pd, src, G, batch, st)) {
+    PFTG_LAUNCH_CHECK();
+    return false;
   }
   const size_t smem = rows_smem_bytes(pd);
   if (smem > 227 * 1024) throw std::invalid_argument("pftg: plan too large for the rows pass (smem)");
@@ -242,6 +272,13 @@ void launch_fwd_rows<R_>(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R
     k<<<dim3(pd.p1, batch), rows_threads<R_>(), smem, st>>>(pd, src, G);
   });
   PFTG_LAUNCH_CHECK();
+  return false;
+}
+
+template <>
+long long g_field_elems<R_>(const PftDev<R_>& pd) {
+  const long long rowblk = (long long)pd.p1 * pd.r1 * pd.M2;
+  return fast_cols_ok(pd) ? std::max(rowblk, strip_field_elems(pd)) : rowblk;
 }
 
 template <>
@@ -252,7 +289,25 @@ int cols_strips<R_>(const PftDev<R_>& pd) {
 template <>
 void launch_fwd_cols<R_>(const PftDev<R_>& pd, int mode, const typename CT<R_>::C* G,
                          typename CT<R_>::C* band, const R_* dcrop, long long dstride,
-                         typename CT<R_>::C* Gout, double* partial, int batch, cudaStream_t st) {
+                         typename CT<R_>::C* Gout, double* partial, int batch, cudaStream_t st,
+                         bool strip) {
+  if (strip) {
+    // G in strip-major layout (written by the TMA rows pass): persistent cols kernel
+    if (mode != 0) throw std::logic_error("pftg: strip-major G only feeds the plain forward cols pass");
+    ProfScope prof(st, K_FWD_COLS);
+    const bool ok = dispatch_fast(pd, [&](auto q, auto r, auto p) {
+      constexpr int RR = decltype(r)::value, P = decltype(p)::value;
+      const size_t smem = cols_fwd_smem<R_>(P, RR, pd.M1);
+      auto k = kc_fwd_cols<R_, RR, P>;
+      allow_smem(k);
+      const int nsf = pd.M2 / kStripNB, total = nsf * batch;
+      const int grid = std::min(total, 2 * sm_count());
+      k<<<grid, kColsThreads, smem, st>>>(pd, G, strip_field_elems(pd), band, nsf, total);
+    });
+    if (!ok) throw std::logic_error("pftg: strip-major G for an unspecialized plan");
+    PFTG_LAUNCH_CHECK();
+    return;
+  }
   const size_t smem = cols_smem_bytes(pd);
   if (smem > 227 * 1024) throw std::invalid_argument("pftg: plan too large for the cols pass (smem)");
   const dim3 grid(cols_strips(pd), batch);
@@ -283,9 +338,22 @@ void launch_fwd_cols<R_>(const PftDev<R_>& pd, int mode, const typename CT<R_>::
 template <>
 void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, typename CT<R_>::C* Gt,
                          int batch, cudaStream_t st) {
+  ProfScope prof(st, K_ADJ_COLS);
+  if (fast_cols_ok(pd) && !std::getenv("PFTG_NO_TMA")) {
+    dispatch_fast(pd, [&](auto q, auto r, auto p) {
+      constexpr int RR = decltype(r)::value, P = decltype(p)::value;
+      const size_t smem = cols_adj_smem<R_>(P, RR, pd.M1);
+      auto k = kc_adj_cols<R_, RR, P>;
+      allow_smem(k);
+      const int nsf = pd.M2 / kStripNB, total = nsf * batch;
+      const int grid = std::min(total, 2 * sm_count());
+      k<<<grid, kColsThreads, smem, st>>>(pd, band, Gt, nsf, total);
+    });
+    PFTG_LAUNCH_CHECK();
+    return;
+  }
   const size_t smem = cols_smem_bytes(pd);
   if (smem > 227 * 1024) throw std::invalid_argument("pftg: plan too large for the cols pass (smem)");
-  ProfScope prof(st, K_ADJ_COLS);
   dispatch_sr(slots_of(pd.p1), rb_of(std::max(pd.r1, pd.r2)), [&](auto s, auto rb) {
     auto k = k_adj_cols<R_, decltype(s)::value, decltype(rb)::value>;
     static bool once = (allow_smem(k), true);

@@ -32,7 +32,8 @@ __host__ __device__ inline size_t tma_rows_smem(int n2, int q, int r, int M2, in
 template <class R, int Q, int RR, int P, int VC>
 __global__ void __launch_bounds__(kTmaConsumers + 32, 1)
     kt_fwd_rows(PftDev<R> pl, BPar<R, Q, RR> bp, const typename CT<R>::C* __restrict__ z, long long ld,
-                long long bstride, int ntiles, int NS, typename CT<R>::C* __restrict__ G, int dbg) {
+                long long bstride, int ntiles, int NS, typename CT<R>::C* __restrict__ G, int dbg,
+                long long gstride) {
   using C = typename CT<R>::C;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int n2 = pl.n2;
@@ -138,7 +139,9 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1)
     named_sync(1, kTmaConsumers);
     if (dbg & 1) continue;  // profiling experiment: streaming + stage A only
     C* Gblk = G + ((size_t)f * pl.p1 + k1) * RR * pl.M2;
-    fast_stage_b_to_g<R, Q, RR, P>(pl, bp, T, W2s, tw2s, Gblk, kTmaConsumers / 32);
+    // gstride > 0: strip-major layout for the persistent cols pass (field stride gstride)
+    fast_stage_b_to_g<R, Q, RR, P>(pl, bp, T, W2s, tw2s, Gblk, kTmaConsumers / 32,
+                                   gstride > 0 ? G + (size_t)f * gstride : nullptr, k1);
   }
 }
 
