@@ -274,12 +274,12 @@ __device__ __forceinline__ void fast_stage_b_to_g(const PftDev<R>& pl, const BPa
                                                   const typename CT<R>::C* T, const typename CT<R>::C* W2s,
                                                   const typename CT<R>::C* tw2, typename CT<R>::C* Gblk,
                                                   int nwarps = -1, typename CT<R>::C* gstrip = nullptr,
-                                                  int k1 = 0) {
+                                                  int k1 = 0, int warp0 = 0) {
   using C = typename CT<R>::C;
   constexpr int PL = P < 32 ? P : 32;
   constexpr int S = P / PL;
   constexpr int GPW = 32 / PL;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) - warp0;  // warp within the calling group
   if (nwarps < 0) nwarps = blockDim.x >> 5;
   const int lig = lane & (PL - 1), giw = lane / PL;
   const int ldT = ldT_of(pl.n2, Q), M2 = pl.M2, mt2 = pl.mt2;

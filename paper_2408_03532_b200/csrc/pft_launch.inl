@@ -177,6 +177,23 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
     const char* dv = std::getenv("PFTG_DEBUG_TMA");
     const int dbg = dv ? std::atoi(dv) : 0;
     if (const char* e = std::getenv("PFTG_TMA_NS")) ns = std::min(ns, std::atoi(e));
+    // warp-specialized version when the double-buffered T still leaves >= 3 ring slots
+    int ns2 = 6;
+    while (ns2 > 3 && tma2_rows_smem<R_>(pd.n2, Q, RR, P, ns2) > 227 * 1024) --ns2;
+    if (!dbg && !std::getenv("PFTG_NO_WS") && tma2_rows_smem<R_>(pd.n2, Q, RR, P, ns2) <= 227 * 1024) {
+      const size_t smem2 = tma2_rows_smem<R_>(pd.n2, Q, RR, P, ns2);
+      constexpr int NT = kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32;
+      auto k = kt2_fwd_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
+      if (vc == 2) {
+        allow_smem(k);
+        k<<<grid, NT, smem2, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride);
+      } else {
+        auto k1 = kt2_fwd_rows<R_, Q, RR, P, 1>;
+        allow_smem(k1);
+        k1<<<grid, NT, smem2, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride);
+      }
+      return;
+    }
     if (vc == 2) {
       auto k = kt_fwd_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
       allow_smem(k);

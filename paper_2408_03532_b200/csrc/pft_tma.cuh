@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1)
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int f = t / pl.p1, k1 = t % pl.p1;
       const C* base = z + (long long)f * bstride + (long long)k1 * Q * ld;
+      // (an L2 bulk prefetch of the next row block was measured slower: 93 -> 101 us)
       for (int pi = 0; pi < Q / 2; ++pi, ++seq) {
         const int s = seq % NS;
         if (seq >= NS) mbar_wait(&empty[s], ((seq / NS) - 1) & 1);
@@ -143,6 +144,156 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1)
     fast_stage_b_to_g<R, Q, RR, P>(pl, bp, T, W2s, tw2s, Gblk, kTmaConsumers / 32,
                                    gstride > 0 ? G + (size_t)f * gstride : nullptr, k1);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialized variant of kt_fwd_rows: group A (16 warps) streams row
+// pairs from the TMA ring and accumulates stage A into T[i & 1]; group B (one
+// warp per j1) runs stage B / FFT / band on T[(i-1) & 1] concurrently, so HBM
+// streaming never stops for the compute phase. T is double-buffered (the ring
+// is correspondingly shallower) and W2 is read through L1.
+template <int RR, int P>
+constexpr int fwd_b_warps() {
+  constexpr int gpw = 32 / (P < 32 ? P : 32);
+  return (RR + gpw - 1) / gpw;
+}
+
+template <class R>
+__host__ __device__ inline size_t tma2_rows_smem(int n2, int q, int r, int p, int ns) {
+  using C = typename CT<R>::C;
+  size_t b = sizeof(C) * ((size_t)ns * 2 * n2 + 2 * (size_t)r * ldT_of(n2, q) + p / 2 + 1);
+  b = (b + 15) & ~size_t(15);
+  return b + (2 * ns + 4) * sizeof(uint64_t);
+}
+
+template <class R, int Q, int RR, int P, int VC>
+__global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32, 1)
+    kt2_fwd_rows(PftDev<R> pl, BPar<R, Q, RR> bp, const typename CT<R>::C* __restrict__ z, long long ld,
+                 long long bstride, int ntiles, int NS, typename CT<R>::C* __restrict__ G, long long gstride) {
+  using C = typename CT<R>::C;
+  constexpr int NBW = fwd_b_warps<RR, P>();
+  constexpr int AT = kTmaConsumers, BT = 32 * NBW;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int n2 = pl.n2;
+  const int ldT = ldT_of(n2, Q);
+  C* ring = reinterpret_cast<C*>(smem_raw);
+  C* Tb = ring + (size_t)NS * 2 * n2;  // [2][RR][ldT]
+  C* tw2s = Tb + 2 * (size_t)RR * ldT;
+  uint64_t* bars = smem_after<uint64_t>(smem_raw, tw2s + P / 2 + 1, 16);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + NS;
+  uint64_t* tready = bars + 2 * NS;
+  uint64_t* tfree = tready + 2;
+  for (int i = threadIdx.x; i < P / 2; i += blockDim.x) tw2s[i] = pl.tw2[i];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], AT / 32);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tready[s], 1);
+      mbar_init(&tfree[s], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const uint32_t row_bytes = (uint32_t)(n2 * sizeof(C));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x >= AT + BT) {
+    // ---------------- producer ----------------
+    if (threadIdx.x != AT + BT) return;
+    uint32_t seq = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int f = t / pl.p1, k1 = t % pl.p1;
+      const C* base = z + (long long)f * bstride + (long long)k1 * Q * ld;
+      for (int pi = 0; pi < Q / 2; ++pi, ++seq) {
+        const int s = seq % NS;
+        if (seq >= NS) mbar_wait(&empty[s], ((seq / NS) - 1) & 1);
+        const int la = pi == 0 ? 0 : pi, lb = pi == 0 ? Q / 2 : Q - pi;
+        mbar_arrive_expect_tx(&full[s], 2 * row_bytes);
+        C* slot = ring + (size_t)s * 2 * n2;
+        bulk_g2s(slot, base + (long long)la * ld, row_bytes, &full[s]);
+        bulk_g2s(slot + n2, base + (long long)lb * ld, row_bytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  if (threadIdx.x >= AT) {
+    // ---------------- group B: stage B + FFT + band from T[i & 1] ----------------
+    uint32_t i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int s = i & 1;
+      const int f = t / pl.p1, k1 = t % pl.p1;
+      mbar_wait(&tready[s], (i >> 1) & 1);
+      C* Gblk = G + ((size_t)f * pl.p1 + k1) * RR * pl.M2;
+      fast_stage_b_to_g<R, Q, RR, P>(pl, bp, Tb + (size_t)s * RR * ldT, pl.W2t, tw2s, Gblk, NBW,
+                                     gstride > 0 ? G + (size_t)f * gstride : nullptr, k1, AT / 32);
+      named_sync(2, BT);
+      if (threadIdx.x == AT) mbar_arrive(&tfree[s]);
+    }
+    return;
+  }
+
+  // ---------------- group A: stream + stage A -> T[i & 1] ----------------
+  const int c0 = threadIdx.x * VC;
+  uint32_t seq = 0, i = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+    const int s2 = i & 1;
+    C acc[VC][RR];
+#pragma unroll
+    for (int v = 0; v < VC; ++v)
+#pragma unroll
+      for (int j = 0; j < RR; ++j) acc[v][j] = czero<C>();
+#pragma unroll
+    for (int pi = 0; pi < Q / 2; ++pi, ++seq) {
+      const int s = seq % NS;
+      mbar_wait(&full[s], (seq / NS) & 1);
+      const C* slot = ring + (size_t)s * 2 * n2;
+      C a[VC], b[VC];
+      if constexpr (VC == 2 && sizeof(C) == 8) {
+        const float4 ta = *reinterpret_cast<const float4*>(slot + c0);
+        const float4 tb = *reinterpret_cast<const float4*>(slot + n2 + c0);
+        a[0] = CT<R>::mk(ta.x, ta.y);
+        a[VC - 1] = CT<R>::mk(ta.z, ta.w);
+        b[0] = CT<R>::mk(tb.x, tb.y);
+        b[VC - 1] = CT<R>::mk(tb.z, tb.w);
+      } else {
+#pragma unroll
+        for (int v = 0; v < VC; ++v) {
+          a[v] = slot[c0 + v];
+          b[v] = slot[n2 + c0 + v];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+      for (int v = 0; v < VC; ++v) {
+        if (pi == 0) {
+#pragma unroll
+          for (int j = 0; j < RR; ++j) bmac(acc[v][j], bp.b1[0][j], a[v], j & 1);
+          bmac(acc[v][0], bp.b1[Q / 2][0], b[v], false);
+        } else {
+          const C sp = cadd(a[v], b[v]), dm = csub(a[v], b[v]);
+#pragma unroll
+          for (int j = 0; j < RR; ++j) bmac(acc[v][j], bp.b1[pi][j], (j & 1) ? dm : sp, j & 1);
+        }
+      }
+    }
+    if (i >= 2) mbar_wait(&tfree[s2], ((i >> 1) - 1) & 1);  // group B is done with T[s2]
+    C* T = Tb + (size_t)s2 * RR * ldT;
+#pragma unroll
+    for (int v = 0; v < VC; ++v) {
+      const int c = c0 + v;
+      const int tc = c + c / Q;
+#pragma unroll
+      for (int j = 0; j < RR; ++j) T[(size_t)j * ldT + tc] = acc[v][j];
+    }
+    named_sync(1, AT);
+    if (threadIdx.x == 0) mbar_arrive(&tready[s2]);
+  }
+  (void)warp;
 }
 
 // ---------------------------------------------------------------------------

@@ -55,6 +55,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Asynchronous HBM -> L2 prefetch of a contiguous range (multiple of 16 bytes).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // Aligned carve-out of dynamic shared memory that keeps the pointer derived
 // from `base` (so the compiler still emits LDS/STS, not generic loads).
 template <class T>

@@ -148,3 +148,21 @@ def test_plan_immutability_bit_identical():
     a = P.pft_apply_2d(g, z)
     b = P.pft_apply_2d(g, z)
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("dtype,tol", [(np.complex64, TOL64), (np.complex128, TOL128)])
+def test_cfg2_kernel_shape_well_conditioned(ref, dtype, tol):
+    """The batched cfg2 kernel path (q=32, r=10, p=32 on 1024^2: persistent TMA
+    rows passes + persistent cols passes) on a well-conditioned plan of the same
+    shape (mt=40, eps=1e-3 -> r=10, xi=1.25), batch 37 so the chunking, the
+    strip-major intermediate and partial last strips are all exercised."""
+    table = DATA / "scope_table_v1.txt"
+    g, r = _plans(ref, table, 1024, 1024, 40, 40, 32, 32, 1e-3)
+    assert (g.q1, g.r1, g.p1) == (32, 10, 32)
+    rng = np.random.default_rng(21)
+    z = cnormal(rng, (37, 1024, 1024), dtype)
+    band = P.pft_apply_2d(g, torch.from_numpy(z).cuda()).cpu().numpy()
+    back = P.pft_adjoint_2d(g, torch.from_numpy(band).cuda()).cpu().numpy()
+    for b in (0, 17, 36):
+        assert rel_l2(band[b], r.apply(z[b].astype(np.complex128))) <= tol
+        assert rel_l2(back[b], r.adjoint(band[b].astype(np.complex128))) <= tol
