@@ -220,18 +220,38 @@ __global__ void __launch_bounds__(256) k_fft_cols(int n1, int n2, int lg1, int l
   const int f = blockIdx.y, c0 = blockIdx.x * nc;
   C* Xf = X + (size_t)f * x_bstride;
   for (int i = threadIdx.x; i < n1 / 2; i += blockDim.x) tws[i] = tw[i];
-  for (int i = threadIdx.x; i < n1 * nc; i += blockDim.x) {
-    const int rr = i / nc, cc = i % nc;
-    strip[(size_t)rr * ld + cc] = Xf[(size_t)rr * n2 + c0 + cc];
+  // strip loads: 8 independent loads in flight per thread (nc is a power of two)
+  const int tot = n1 * nc, lnc = __ffs(nc) - 1, cm = nc - 1;
+  for (int base = threadIdx.x; base < tot; base += 8 * blockDim.x) {
+    C v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * blockDim.x;
+      if (i < tot) v[u] = Xf[(size_t)(i >> lnc) * n2 + c0 + (i & cm)];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * blockDim.x;
+      if (i < tot) strip[(size_t)(i >> lnc) * ld + (i & cm)] = v[u];
+    }
   }
   const R* df = nullptr;
   if (MODE != COL_NATURAL) {
     const long long di = d_index ? d_index[f] : f;
     df = d + di * d_bstride;
     if (dmode == 0) {
-      for (int i = threadIdx.x; i < n1 * nc; i += blockDim.x) {
-        const int rr = i / nc, cc = i % nc;
-        ds[(size_t)rr * nc + cc] = df[(size_t)rr * n2 + c0 + cc];
+      for (int base = threadIdx.x; base < tot; base += 8 * blockDim.x) {
+        R v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = base + u * blockDim.x;
+          if (i < tot) v[u] = df[(size_t)(i >> lnc) * n2 + c0 + (i & cm)];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = base + u * blockDim.x;
+          if (i < tot) ds[(size_t)(i >> lnc) * nc + (i & cm)] = v[u];
+        }
       }
     }
   }
@@ -322,10 +342,8 @@ __global__ void __launch_bounds__(256) k_fft_cols(int n1, int n2, int lg1, int l
     return;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < n1 * nc; i += blockDim.x) {
-    const int rr = i / nc, cc = i % nc;
-    Xf[(size_t)rr * n2 + c0 + cc] = strip[(size_t)rr * ld + cc];
-  }
+  for (int i = threadIdx.x; i < tot; i += blockDim.x)
+    Xf[(size_t)(i >> lnc) * n2 + c0 + (i & cm)] = strip[(size_t)(i >> lnc) * ld + (i & cm)];
 }
 
 // d_perm[f][rp][cp] = d[f][bitrev(rp)][bitrev(cp)]  (float or double)
