@@ -61,7 +61,8 @@ int pftg_device_ok(void);
  * graph capture is bracketed by CUDA events on its own stream. profile_end
  * fills, per kernel id (0 pft rows fwd, 1 pft cols fwd, 2 pft cols adj,
  * 3 pft rows adj, 4 fft rows, 5 fft cols): summed milliseconds, timed launch
- * count and the number of launches issued since profile_begin (arrays of 6). */
+ * count and the number of launches issued since profile_begin, graph replays
+ * included (arrays of 6). */
 int pftg_profile_begin(void);
 int pftg_profile_end(double* ms, int* count, int* launches);
 

@@ -110,13 +110,13 @@ class KernelProfile:
         return self
 
     def __exit__(self, *exc):
-        ms = (C.c_double * 6)()
-        cnt = (C.c_int * 6)()
-        launches = (C.c_int * 6)()
+        ms = (C.c_double * len(KERNEL_NAMES))()
+        cnt = (C.c_int * len(KERNEL_NAMES))()
+        launches = (C.c_int * len(KERNEL_NAMES))()
         check(lib().pftg_profile_end(ms, cnt, launches))
-        self.ms = {KERNEL_NAMES[k]: ms[k] for k in range(6)}
-        self.count = {KERNEL_NAMES[k]: cnt[k] for k in range(6)}
-        self.launches = {KERNEL_NAMES[k]: launches[k] for k in range(6)}
+        self.ms = {KERNEL_NAMES[k]: ms[k] for k in range(len(KERNEL_NAMES))}
+        self.count = {KERNEL_NAMES[k]: cnt[k] for k in range(len(KERNEL_NAMES))}
+        self.launches = {KERNEL_NAMES[k]: launches[k] for k in range(len(KERNEL_NAMES))}
         return False
 
 

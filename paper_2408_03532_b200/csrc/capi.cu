@@ -84,6 +84,18 @@ bool capturing(cudaStream_t st) {
 }
 }  // namespace
 
+void prof_launch_snapshot(int* out) {
+  ProfState& p = prof();
+  std::lock_guard<std::mutex> lock(p.mu);
+  std::copy(p.launches, p.launches + K_NUM, out);
+}
+
+void prof_add_launches(const int* delta) {
+  ProfState& p = prof();
+  std::lock_guard<std::mutex> lock(p.mu);
+  for (int k = 0; k < K_NUM; ++k) p.launches[k] += delta[k];
+}
+
 ProfScope::ProfScope(cudaStream_t s, int k) : kid(k), st(s) {
   ProfState& p = prof();
   {

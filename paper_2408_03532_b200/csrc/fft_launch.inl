@@ -69,26 +69,31 @@ void launch_fft_rows<R_>(int mode, int epi, int n1, int n2, const RowSrc<R_>& sr
   const C_* tw = fft_twiddles<R_>(n2);
   const int S = slots_for(n2);
   const int P = n2 / S;
-  const int rows_per_cta = 8 * (32 / P);
+  // Small batches (one ePIE position) get narrower CTAs so the pass spreads
+  // over the SMs instead of queueing rows behind a few blocks.
+  int threads = 256;
+  while (threads > 64 && (long long)((n1 + threads / 32 * (32 / P) - 1) / (threads / 32 * (32 / P))) * batch < 2 * 148)
+    threads /= 2;
+  const int rows_per_cta = threads / 32 * (32 / P);
   const dim3 grid((n1 + rows_per_cta - 1) / rows_per_cta, batch);
   const size_t smem = sizeof(C_) * (n2 / 2 + 1);
   ProfScope prof(st, K_FFT_ROWS);
   dispatch_slots(S, [&](auto s) {
     constexpr int SS = decltype(s)::value;
     if (mode == ROW_DIF_STORE) {
-      k_fft_rows<R_, SS, ROW_DIF_STORE, EPI_STORE><<<grid, 256, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
+      k_fft_rows<R_, SS, ROW_DIF_STORE, EPI_STORE><<<grid, threads, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
                                                                            x_bstride, sign, scale, ep);
     } else if (mode == ROW_DIT_NATURAL) {
-      k_fft_rows<R_, SS, ROW_DIT_NATURAL, EPI_STORE><<<grid, 256, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
+      k_fft_rows<R_, SS, ROW_DIT_NATURAL, EPI_STORE><<<grid, threads, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
                                                                              x_bstride, sign, scale, ep);
     } else if (epi == EPI_STORE) {
-      k_fft_rows<R_, SS, ROW_DIT_PROJ, EPI_STORE><<<grid, 256, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
+      k_fft_rows<R_, SS, ROW_DIT_PROJ, EPI_STORE><<<grid, threads, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
                                                                           x_bstride, sign, scale, ep);
     } else if (epi == EPI_OBJ) {
-      k_fft_rows<R_, SS, ROW_DIT_PROJ, EPI_OBJ><<<grid, 256, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
+      k_fft_rows<R_, SS, ROW_DIT_PROJ, EPI_OBJ><<<grid, threads, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
                                                                         x_bstride, sign, scale, ep);
     } else {
-      k_fft_rows<R_, SS, ROW_DIT_PROJ, EPI_PROBE><<<grid, 256, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
+      k_fft_rows<R_, SS, ROW_DIT_PROJ, EPI_PROBE><<<grid, threads, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
                                                                           x_bstride, sign, scale, ep);
     }
   });
@@ -109,7 +114,12 @@ void launch_fft_cols<R_>(int mode, int n1, int n2, C_* X, long long x_bstride, c
   const C_* tw = fft_twiddles<R_>(n1);
   const int S = slots_for(n1);
   const int nc0 = sizeof(R_) == 4 ? 16 : 8;
-  const int nc = n2 < nc0 ? n2 : nc0;
+  int nc = n2 < nc0 ? n2 : nc0;
+  // Narrow strips for small batches (ePIE positions); the evaluation modes keep
+  // the fixed strip count their per-CTA partial sums are laid out by.
+  if (mode == COL_PROJECT || mode == COL_NATURAL)
+    while (nc > 2 && (long long)(n2 / nc) * batch < 148) nc /= 2;
+  const int threads = std::max(64, std::min(256, nc * (n1 / S)));  // one lane group per column
   const dim3 grid(n2 / nc, batch);
   size_t smem = sizeof(C_) * ((size_t)n1 * (nc + 1) + n1 / 2 + 1);
   if (mode != COL_NATURAL && dmode == 0) smem += sizeof(R_) * (size_t)n1 * nc;
@@ -122,25 +132,25 @@ void launch_fft_cols<R_>(int mode, int n1, int n2, C_* X, long long x_bstride, c
       auto k = k_fft_cols<R_, SS, COL_PROJECT>;
       static bool once = (allow_smem_fft(k), true);
       (void)once;
-      k<<<grid, 256, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
+      k<<<grid, threads, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
                                  dmode, sign, partial);
     } else if (mode == COL_EVAL) {
       auto k = k_fft_cols<R_, SS, COL_EVAL>;
       static bool once = (allow_smem_fft(k), true);
       (void)once;
-      k<<<grid, 256, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
+      k<<<grid, threads, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
                                  dmode, sign, partial);
     } else if (mode == COL_EVAL_NAT) {
       auto k = k_fft_cols<R_, SS, COL_EVAL_NAT>;
       static bool once = (allow_smem_fft(k), true);
       (void)once;
-      k<<<grid, 256, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
+      k<<<grid, threads, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
                                  dmode, sign, partial);
     } else {
       auto k = k_fft_cols<R_, SS, COL_NATURAL>;
       static bool once = (allow_smem_fft(k), true);
       (void)once;
-      k<<<grid, 256, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
+      k<<<grid, threads, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
                                  dmode, sign, partial);
     }
   });

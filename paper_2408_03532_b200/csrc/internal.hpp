@@ -123,6 +123,9 @@ void check_fft_len(std::size_t n);
 // each launch on its own stream while profiling is on (never inside a graph
 // capture). Kernel ids:
 enum KernelId { K_FWD_ROWS = 0, K_FWD_COLS, K_ADJ_COLS, K_ADJ_ROWS, K_FFT_ROWS, K_FFT_COLS, K_NUM };
+// launch counters: snapshot (K_NUM ints) and credit replays of a captured graph
+void prof_launch_snapshot(int* out);
+void prof_add_launches(const int* delta);
 struct ProfScope {
   int kid;
   cudaStream_t st;

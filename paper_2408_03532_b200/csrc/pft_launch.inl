@@ -325,9 +325,15 @@ void launch_fwd_cols<R_>(const PftDev<R_>& pd, int mode, const typename CT<R_>::
     PFTG_LAUNCH_CHECK();
     return;
   }
-  const size_t smem = cols_smem_bytes(pd);
+  // Narrower strips when one launch covers few fields (an ePIE position): the
+  // pass is latency-bound, so spread it over more SMs. MODE 2 keeps the plan's
+  // strip count (its per-CTA partial sums are laid out by it).
+  PftDev<R_> pl = pd;
+  if (mode != 2)
+    while (pl.nb > 1 && (long long)cols_strips(pl) * batch < 148) pl.nb /= 2;
+  const size_t smem = cols_smem_bytes(pl);
   if (smem > 227 * 1024) throw std::invalid_argument("pftg: plan too large for the cols pass (smem)");
-  const dim3 grid(cols_strips(pd), batch);
+  const dim3 grid(cols_strips(pl), batch);
   const R_* dc = dcrop;  // batch element f reads dcrop + f*dstride
   ProfScope prof(st, K_FWD_COLS);
   dispatch_sr(slots_of(pd.p1), rb_of(std::max(pd.r1, pd.r2)), [&](auto s, auto rb) {
@@ -336,17 +342,17 @@ void launch_fwd_cols<R_>(const PftDev<R_>& pd, int mode, const typename CT<R_>::
       auto k = k_fwd_cols<R_, S, RB, 0>;
       static bool once = (allow_smem(k), true);
       (void)once;
-      k<<<grid, 256, smem, st>>>(pd, G, band, dc, dstride, Gout, partial);
+      k<<<grid, 256, smem, st>>>(pl, G, band, dc, dstride, Gout, partial);
     } else if (mode == 1) {
       auto k = k_fwd_cols<R_, S, RB, 1>;
       static bool once = (allow_smem(k), true);
       (void)once;
-      k<<<grid, 256, smem, st>>>(pd, G, band, dc, dstride, Gout, partial);
+      k<<<grid, 256, smem, st>>>(pl, G, band, dc, dstride, Gout, partial);
     } else {
       auto k = k_fwd_cols<R_, S, RB, 2>;
       static bool once = (allow_smem(k), true);
       (void)once;
-      k<<<grid, 256, smem, st>>>(pd, G, band, dc, dstride, Gout, partial);
+      k<<<grid, 256, smem, st>>>(pl, G, band, dc, dstride, Gout, partial);
     }
   });
   PFTG_LAUNCH_CHECK();
@@ -356,7 +362,7 @@ template <>
 void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, typename CT<R_>::C* Gt,
                          int batch, cudaStream_t st) {
   ProfScope prof(st, K_ADJ_COLS);
-  if (fast_cols_ok(pd) && !std::getenv("PFTG_NO_TMA")) {
+  if (fast_cols_ok(pd) && (long long)(pd.M2 / kStripNB) * batch >= 148 && !std::getenv("PFTG_NO_TMA")) {
     dispatch_fast(pd, [&](auto q, auto r, auto p) {
       constexpr int RR = decltype(r)::value, P = decltype(p)::value;
       const size_t smem = cols_adj_smem<R_>(P, RR, pd.M1);
@@ -369,13 +375,15 @@ void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, t
     PFTG_LAUNCH_CHECK();
     return;
   }
-  const size_t smem = cols_smem_bytes(pd);
+  PftDev<R_> pl = pd;
+  while (pl.nb > 1 && (long long)cols_strips(pl) * batch < 148) pl.nb /= 2;
+  const size_t smem = cols_smem_bytes(pl);
   if (smem > 227 * 1024) throw std::invalid_argument("pftg: plan too large for the cols pass (smem)");
   dispatch_sr(slots_of(pd.p1), rb_of(std::max(pd.r1, pd.r2)), [&](auto s, auto rb) {
     auto k = k_adj_cols<R_, decltype(s)::value, decltype(rb)::value>;
     static bool once = (allow_smem(k), true);
     (void)once;
-    k<<<dim3(cols_strips(pd), batch), 256, smem, st>>>(pd, band, Gt);
+    k<<<dim3(cols_strips(pl), batch), 256, smem, st>>>(pl, band, Gt);
   });
   PFTG_LAUNCH_CHECK();
 }

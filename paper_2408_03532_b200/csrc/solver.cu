@@ -21,6 +21,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -121,6 +122,7 @@ struct pftg_solver {
   void* dperm = nullptr;
   void* dcrop = nullptr;
   long long* doffs = nullptr;  // per list position
+  int graph_launches[2][K_NUM] = {};  // kernel launches captured per graph (credited per replay)
   void* G = nullptr;
   void* Gt = nullptr;
   void* X = nullptr;
@@ -278,7 +280,10 @@ void run(pftg_solver& s, int max_sweeps) {
       enqueue_sweep<R>(s, band);
     } else {
       cudaGraphExec_t& g = s.graph[band ? 0 : 1];
+      int* delta = s.graph_launches[band ? 0 : 1];
       if (!g) {
+        int before[K_NUM], after[K_NUM];
+        prof_launch_snapshot(before);
         cudaGraph_t graph;
         PFTG_CUDA(cudaStreamBeginCapture(s.st, cudaStreamCaptureModeThreadLocal));
         try {
@@ -290,6 +295,10 @@ void run(pftg_solver& s, int max_sweeps) {
         PFTG_CUDA(cudaStreamEndCapture(s.st, &graph));
         PFTG_CUDA(cudaGraphInstantiate(&g, graph, 0));
         cudaGraphDestroy(graph);
+        prof_launch_snapshot(after);
+        for (int k = 0; k < K_NUM; ++k) delta[k] = after[k] - before[k];
+      } else {
+        prof_add_launches(delta);  // a replay launches every captured kernel again
       }
       PFTG_CUDA(cudaGraphLaunch(g, s.st));
     }

@@ -189,3 +189,21 @@ def test_cfg3_full_problem_one_band_one_fft_sweep(ref):
     assert np.allclose(r128.objective, objr, rtol=1e-10)
     r64 = P.hybrid_solve(d, prob.offsets, pinit, init, P.SolverConfig(mt1=32, mt2=32, **kw))
     assert rel_l2(r64.frame, fr) <= 1e-3 and rel_l2(r64.probe, pr) <= 1e-3
+
+
+
+@pytest.mark.parametrize("w,dtype,pft", [(64, np.complex128, 1), (128, np.complex128, 0), (64, np.complex64, 1)])
+def test_hybrid_solve_shuffled_matches_reference(ref, w, dtype, pft):
+    """Shuffled visit order (the reference's mt19937_64 Fisher-Yates stream,
+    solver.cpp:164-169) through the band and full-FFT stages, blind."""
+    rng = np.random.default_rng(31)
+    obj, probe, offs = _small_problem(rng, n=2 * w + 32, w=w, npos=9)
+    d = ref.simulate(obj, probe, offs)
+    init = np.exp(1j * 0.1 * rng.standard_normal(obj.shape)) * 0.8
+    kw = dict(pft_sweeps=pft, fft_sweeps=2, beta=0.5, gamma=0.05, beta_pft=0.25 / w ** 2,
+              gamma_pft=0.0125 / w ** 2, eps_pft=1e-3, blind=True, shuffled=True, seed=7)
+    got = P.hybrid_solve(d, offs, probe * 0.9, init, P.SolverConfig(**kw), dtype=dtype)
+    f_ref, p_ref, _, _, _ = ref.hybrid_solve(init, probe * 0.9, offs, d, table_path=DATA / "scope_table_v1.txt",
+                                             **kw)
+    tol = 1e-10 if dtype == np.complex128 else 1e-4
+    assert rel_l2(got.frame, f_ref) <= tol and rel_l2(got.probe, p_ref) <= tol
