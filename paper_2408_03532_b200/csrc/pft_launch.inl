@@ -178,8 +178,9 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
     const int dbg = dv ? std::atoi(dv) : 0;
     if (const char* e = std::getenv("PFTG_TMA_NS")) ns = std::min(ns, std::atoi(e));
     // warp-specialized version when the double-buffered T still leaves >= 3 ring slots
-    int ns2 = 6;
+    int ns2 = 12;
     while (ns2 > 3 && tma2_rows_smem<R_>(pd.n2, Q, RR, P, ns2) > 227 * 1024) --ns2;
+    if (const char* e = std::getenv("PFTG_TMA_NS")) ns2 = std::max(3, std::min(ns2, std::atoi(e)));
     if (!dbg && !std::getenv("PFTG_NO_WS") && tma2_rows_smem<R_>(pd.n2, Q, RR, P, ns2) <= 227 * 1024) {
       const size_t smem2 = tma2_rows_smem<R_>(pd.n2, Q, RR, P, ns2);
       constexpr int NT = kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32;

@@ -148,10 +148,13 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1)
 
 // ---------------------------------------------------------------------------
 // Warp-specialized variant of kt_fwd_rows: group A (16 warps) streams row
-// pairs from the TMA ring and accumulates stage A into T[i & 1]; group B (one
-// warp per j1) runs stage B / FFT / band on T[(i-1) & 1] concurrently, so HBM
-// streaming never stops for the compute phase. T is double-buffered (the ring
-// is correspondingly shallower) and W2 is read through L1.
+// pairs from the TMA ring and accumulates stage A in registers; group B (one
+// warp per j1) runs stage B / FFT / band of the previous block concurrently, so
+// HBM streaming never stops for the compute phase. T is single-buffered: group
+// B holds it only for stage B (its results stay in registers for the FFT and
+// band), while group A needs it again only after a whole block of streaming,
+// so the shared memory a second T would take goes to the TMA ring instead
+// (8 x 16 KB in flight per SM instead of 3). W2 is read through L1.
 template <int RR, int P>
 constexpr int fwd_b_warps() {
   constexpr int gpw = 32 / (P < 32 ? P : 32);
@@ -161,9 +164,9 @@ constexpr int fwd_b_warps() {
 template <class R>
 __host__ __device__ inline size_t tma2_rows_smem(int n2, int q, int r, int p, int ns) {
   using C = typename CT<R>::C;
-  size_t b = sizeof(C) * ((size_t)ns * 2 * n2 + 2 * (size_t)r * ldT_of(n2, q) + p / 2 + 1);
+  size_t b = sizeof(C) * ((size_t)ns * 2 * n2 + (size_t)r * ldT_of(n2, q) + p / 2 + 1);
   b = (b + 15) & ~size_t(15);
-  return b + (2 * ns + 4) * sizeof(uint64_t);
+  return b + (2 * ns + 2) * sizeof(uint64_t);
 }
 
 template <class R, int Q, int RR, int P, int VC>
@@ -177,23 +180,21 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
   const int n2 = pl.n2;
   const int ldT = ldT_of(n2, Q);
   C* ring = reinterpret_cast<C*>(smem_raw);
-  C* Tb = ring + (size_t)NS * 2 * n2;  // [2][RR][ldT]
-  C* tw2s = Tb + 2 * (size_t)RR * ldT;
+  C* T = ring + (size_t)NS * 2 * n2;  // [RR][ldT]
+  C* tw2s = T + (size_t)RR * ldT;
   uint64_t* bars = smem_after<uint64_t>(smem_raw, tw2s + P / 2 + 1, 16);
   uint64_t* full = bars;
   uint64_t* empty = bars + NS;
   uint64_t* tready = bars + 2 * NS;
-  uint64_t* tfree = tready + 2;
+  uint64_t* tfree = tready + 1;
   for (int i = threadIdx.x; i < P / 2; i += blockDim.x) tw2s[i] = pl.tw2[i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], AT / 32);
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&tready[s], 1);
-      mbar_init(&tfree[s], 1);
-    }
+    mbar_init(tready, 1);
+    mbar_init(tfree, 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -221,26 +222,69 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
   }
 
   if (threadIdx.x >= AT) {
-    // ---------------- group B: stage B + FFT + band from T[i & 1] ----------------
+    // ---------------- group B: stage B (releases T) + FFT + band ----------------
+    constexpr int PL = P < 32 ? P : 32;
+    constexpr int S = P / PL;
+    constexpr int GPW = 32 / PL;
+    constexpr int LP = (P >= 128) ? 7 : (P >= 64) ? 6 : (P >= 32) ? 5 : (P >= 16) ? 4 : (P >= 8) ? 3 : (P >= 4) ? 2 : 1;
+    const int lig = lane & (PL - 1), giw = lane / PL;
+    const int j1 = (warp - AT / 32) * GPW + giw;  // NBW * GPW >= RR: one j1 per lane group
+    const bool valid = j1 < RR;
+    const int M2 = pl.M2, mt2 = pl.mt2;
     uint32_t i = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-      const int s = i & 1;
       const int f = t / pl.p1, k1 = t % pl.p1;
-      mbar_wait(&tready[s], (i >> 1) & 1);
-      C* Gblk = G + ((size_t)f * pl.p1 + k1) * RR * pl.M2;
-      fast_stage_b_to_g<R, Q, RR, P>(pl, bp, Tb + (size_t)s * RR * ldT, pl.W2t, tw2s, Gblk, NBW,
-                                     gstride > 0 ? G + (size_t)f * gstride : nullptr, k1, AT / 32);
-      named_sync(2, BT);
-      if (threadIdx.x == AT) mbar_arrive(&tfree[s]);
+      mbar_wait(tready, i & 1);
+      C x[S][RR];
+#pragma unroll
+      for (int ss = 0; ss < S; ++ss) {
+#pragma unroll
+        for (int j = 0; j < RR; ++j) x[ss][j] = czero<C>();
+        if (valid) {
+          const int k2 = ss * PL + lig;
+          const C* trow = T + (size_t)j1 * ldT + (size_t)k2 * (Q + 1);
+          {
+            const C t0 = trow[0], th = trow[Q / 2];
+#pragma unroll
+            for (int j = 0; j < RR; ++j) bmac(x[ss][j], bp.b2[0][j], t0, j & 1);
+            bmac(x[ss][0], bp.b2[Q / 2][0], th, false);
+          }
+#pragma unroll
+          for (int l = 1; l < Q / 2; ++l) {
+            const C a = trow[l], b = trow[Q - l];
+            const C sp = cadd(a, b), dm = csub(a, b);
+#pragma unroll
+            for (int j = 0; j < RR; ++j) bmac(x[ss][j], bp.b2[l][j], (j & 1) ? dm : sp, j & 1);
+          }
+        }
+      }
+      named_sync(2, BT);  // group B is done reading T: group A may overwrite it
+      if (threadIdx.x == AT) mbar_arrive(tfree);
+      fft_dif<S, RR>(x, P, PL, lig, tw2s, -1);
+      if (!valid) continue;
+#pragma unroll
+      for (int ss = 0; ss < S; ++ss) {
+        const int u2 = bitrev(ss * PL + lig, LP);
+        if (gstride > 0) {
+          C* gstrip = G + (size_t)f * gstride;
+          constexpr int REC = strip_rec(RR);
+          band_contract<RR>(pl.W2t, M2, (u2 + mt2) & (P - 1), P, RR, x[ss], [&](int b, C v) {
+            gstrip[((size_t)(b / kStripNB) * pl.p1 + k1) * REC + j1 * kStripNB + (b % kStripNB)] = v;
+          });
+        } else {
+          C* Gblk = G + ((size_t)f * pl.p1 + k1) * RR * M2;
+          band_contract<RR>(pl.W2t, M2, (u2 + mt2) & (P - 1), P, RR, x[ss],
+                            [&](int b, C v) { Gblk[(size_t)j1 * M2 + b] = v; });
+        }
+      }
     }
     return;
   }
 
-  // ---------------- group A: stream + stage A -> T[i & 1] ----------------
+  // ---------------- group A: stream + stage A -> T ----------------
   const int c0 = threadIdx.x * VC;
   uint32_t seq = 0, i = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-    const int s2 = i & 1;
     C acc[VC][RR];
 #pragma unroll
     for (int v = 0; v < VC; ++v)
@@ -281,8 +325,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
         }
       }
     }
-    if (i >= 2) mbar_wait(&tfree[s2], ((i >> 1) - 1) & 1);  // group B is done with T[s2]
-    C* T = Tb + (size_t)s2 * RR * ldT;
+    if (i >= 1) mbar_wait(tfree, (i - 1) & 1);  // group B has finished stage B of the previous block
 #pragma unroll
     for (int v = 0; v < VC; ++v) {
       const int c = c0 + v;
@@ -291,9 +334,8 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
       for (int j = 0; j < RR; ++j) T[(size_t)j * ldT + tc] = acc[v][j];
     }
     named_sync(1, AT);
-    if (threadIdx.x == 0) mbar_arrive(&tready[s2]);
+    if (threadIdx.x == 0) mbar_arrive(tready);
   }
-  (void)warp;
 }
 
 // ---------------------------------------------------------------------------
