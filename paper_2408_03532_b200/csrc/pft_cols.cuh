@@ -231,4 +231,283 @@ __global__ void __launch_bounds__(kColsThreads, 2)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Lane-local variants for p1 = 32 (complex64): one thread runs a whole 32-point
+// FFT in registers (the radix-2 DIF of common.cuh with the same twiddle table
+// and operation order, so results are bit-identical to the lane-group FFT),
+// instead of one lane group per sequence with 5 shuffle stages. The band
+// contraction is then done per band row a by one thread: the r1 W1[j][a]
+// coefficients stay in its registers for the CTA's lifetime and the kStripNB
+// outputs of a row are stored as one 64-byte segment.
+
+// Radix-2 DIF over N values held by one thread: natural in, bit-reversed out.
+template <int N, class C>
+__device__ __forceinline__ void fft_dif_local(C (&x)[N], const C (&w)[N / 2], int sign) {
+#pragma unroll
+  for (int h = N / 2; h >= 1; h >>= 1) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if ((i & h) == 0) {
+        C tw = w[(i & (h - 1)) * (N / (2 * h))];
+        if (sign > 0) tw.y = -tw.y;
+        const C a = x[i], c = x[i + h];
+        x[i] = cadd(a, c);
+        x[i + h] = cmul(csub(a, c), tw);
+      }
+    }
+  }
+}
+
+constexpr int kLocalP = 32;
+
+// Forward: warp-specialized. Warps 0..2 (one thread per (j1, bb) sequence)
+// run the FFTs of strip i into Xs[i & 1] while warps 3..6 run the band
+// contraction of strip i-1; mbarriers hand the spectrum buffers back and
+// forth, so neither group idles at a block barrier. A band thread owns the
+// rows a and a + 128 (same u1 = (a - mt1) mod 32): every spectrum value it
+// reads from shared memory feeds two rows, and its 2 x r1 W1 coefficients
+// stay in registers (M1 <= 256).
+constexpr int kFftWarps = 3, kBandWarps = 4;
+constexpr int kStripBufs = 3;  // strips in flight: covers the L2/HBM latency of a strip load
+
+template <class R>
+__host__ __device__ inline size_t cols_fwd_local_smem(int r, int M1) {
+  (void)M1;
+  using C = typename CT<R>::C;
+  const size_t b =
+      sizeof(C) * (kStripBufs * (size_t)kLocalP * strip_rec(r) + 2 * (size_t)kLocalP * (r * kStripNB + 1));
+  return ((b + 15) & ~size_t(15)) + 128 + (kStripBufs + 4) * sizeof(uint64_t);
+}
+
+template <class R, int RR>
+__global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
+    kc_fwd_cols_local(PftDev<R> pl, const typename CT<R>::C* __restrict__ G, long long gstride,
+                      typename CT<R>::C* __restrict__ band, int nstrips_field, int ntotal, int dbg) {
+  using C = typename CT<R>::C;
+  static_assert(sizeof(R) == 4, "lane-local cols pass: complex64");
+  constexpr int P = kLocalP;
+  constexpr int REC = strip_rec(RR);
+  constexpr int NSEQ = RR * kStripNB;  // (j1, bb) sequences per strip
+  static_assert(NSEQ <= 32 * kFftWarps, "one FFT thread per sequence");
+  constexpr int LDX = NSEQ + 1;        // Xs[u][j1 * 8 + bb], padded
+  constexpr int FT = 32 * kFftWarps, BT = 32 * kBandWarps;
+  static_assert(BT % P == 0, "rows a and a + BT share u1");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int M1 = pl.M1, M2 = pl.M2, mt1 = pl.mt1;
+  const int sbytes_e = P * REC;
+  C* buf = reinterpret_cast<C*>(smem_raw);        // [kStripBufs][P * REC]
+  C* Xs = buf + kStripBufs * (size_t)sbytes_e;    // [2][P][LDX]
+  uint64_t* bars = smem_after<uint64_t>(smem_raw, Xs + 2 * (size_t)P * LDX, 16);
+  uint64_t* full = bars;                 // TMA -> FFT warps
+  uint64_t* xready = bars + kStripBufs;  // FFT -> band warps
+  uint64_t* xfree = xready + 2;          // band -> FFT warps
+  const uint32_t strip_bytes = (uint32_t)(sbytes_e * sizeof(C));
+  auto strip_src = [&](int sg) {
+    const int f = sg / nstrips_field, st = sg % nstrips_field;
+    return G + (size_t)f * gstride + (size_t)st * sbytes_e;
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStripBufs; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&xready[s], 1);
+      mbar_init(&xfree[s], 1);
+    }
+    mbar_fence_init();
+    for (int s = 0; s < kStripBufs; ++s) {
+      const int sg = blockIdx.x + s * gridDim.x;
+      if (sg < ntotal) {
+        mbar_arrive_expect_tx(&full[s], strip_bytes);
+        bulk_g2s(buf + (size_t)s * sbytes_e, strip_src(sg), strip_bytes, &full[s]);
+      }
+    }
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < FT) {
+    // ---------------- FFT warps ----------------
+    C w[P / 2];  // twiddles, in registers for the CTA's lifetime
+#pragma unroll
+    for (int k = 0; k < P / 2; ++k) w[k] = pl.tw1[k];
+    uint32_t i = 0;
+    for (int sg = blockIdx.x; sg < ntotal; sg += gridDim.x, ++i) {
+      const int s = i & 1, sbi = (int)(i % kStripBufs);
+      const C* sb = buf + (size_t)sbi * sbytes_e;
+      C* X = Xs + (size_t)s * P * LDX;
+      if (!(dbg & 4) || i < kStripBufs) mbar_wait(&full[sbi], (i / kStripBufs) & 1);
+      if (i >= 2) mbar_wait(&xfree[s], ((i >> 1) - 1) & 1);
+      if (t < NSEQ && !(dbg & 1)) {
+        // sequence (j1, bb) = (t / 8, t % 8): FFT over k1, spectrum to X[u][t]
+        C x[P];
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) x[k1] = sb[(size_t)k1 * REC + t];
+        fft_dif_local<P>(x, w, -1);
+#pragma unroll
+        for (int pos = 0; pos < P; ++pos) X[(size_t)((__brev((unsigned)pos) >> 27) & (P - 1)) * LDX + t] = x[pos];
+      }
+      named_sync(1, FT);  // strip buffer sbi consumed, X complete
+      if (t == 0) {
+        mbar_arrive(&xready[s]);
+        if (!(dbg & 4) && sg + kStripBufs * (int)gridDim.x < ntotal) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive_expect_tx(&full[sbi], strip_bytes);
+          bulk_g2s(buf + (size_t)sbi * sbytes_e, strip_src(sg + kStripBufs * gridDim.x), strip_bytes, &full[sbi]);
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- band warps ----------------
+  const int tb = t - FT;
+  const int a0 = tb, a1 = tb + BT;
+  const bool v0 = a0 < M1, v1 = a1 < M1;
+  C w0[RR], w1[RR];
+#pragma unroll
+  for (int j = 0; j < RR; ++j) {
+    w0[j] = v0 ? __ldg(pl.W1t + (size_t)j * M1 + a0) : czero<C>();
+    w1[j] = v1 ? __ldg(pl.W1t + (size_t)j * M1 + a1) : czero<C>();
+  }
+  const int ua = (a0 - mt1) & (P - 1);  // == (a1 - mt1) & (P - 1): BT is a multiple of P
+  uint32_t i = 0;
+  for (int sg = blockIdx.x; sg < ntotal; sg += gridDim.x, ++i) {
+    const int s = i & 1;
+    const int f = sg / nstrips_field, b0 = (sg % nstrips_field) * kStripNB;
+    const C* xr = Xs + (size_t)s * P * LDX + (size_t)ua * LDX;
+    mbar_wait(&xready[s], (i >> 1) & 1);
+    if (v0 && !(dbg & 2)) {
+      // band rows a0, a1, columns b0 .. b0+7: sum_j W1[j][a] X_j[u1] (band_contract order)
+      C out0[kStripNB], out1[kStripNB];
+#pragma unroll
+      for (int bb = 0; bb < kStripNB; ++bb) {
+        C acc0 = czero<C>(), acc1 = czero<C>();
+#pragma unroll
+        for (int j = 0; j < RR; ++j) {
+          const C xv = xr[j * kStripNB + bb];
+          cmac(acc0, w0[j], xv);
+          cmac(acc1, w1[j], xv);
+        }
+        out0[bb] = acc0;
+        out1[bb] = acc1;
+      }
+      C* dst = band + (size_t)f * M1 * M2 + (size_t)a0 * M2 + b0;
+#pragma unroll
+      for (int bb = 0; bb < kStripNB; bb += 2)
+        *reinterpret_cast<float4*>(dst + bb) = make_float4(out0[bb].x, out0[bb].y, out0[bb + 1].x, out0[bb + 1].y);
+      if (v1) {
+        dst += (size_t)BT * M2;
+#pragma unroll
+        for (int bb = 0; bb < kStripNB; bb += 2)
+          *reinterpret_cast<float4*>(dst + bb) =
+              make_float4(out1[bb].x, out1[bb].y, out1[bb + 1].x, out1[bb + 1].y);
+      }
+    }
+    named_sync(2, BT);  // X[s] fully read
+    if (tb == 0) mbar_arrive(&xfree[s]);
+  }
+}
+
+template <class R>
+__host__ __device__ inline size_t cols_adj_local_smem(int r, int M1) {
+  using C = typename CT<R>::C;
+  const size_t b = sizeof(C) * ((size_t)M1 * (kStripNB + 1) + (size_t)r * kStripNB * (kLocalP + 1) +
+                                (size_t)kLocalP * (r * kStripNB + 1));
+  return ((b + 15) & ~size_t(15)) + 128;
+}
+
+// Adjoint: gather over the band rows of each u1 (thread (u1, bb)), then one
+// thread per (j1, bb) runs the inverse 32-point FFT; Gt row-block layout.
+template <class R, int RR>
+__global__ void __launch_bounds__(kColsThreads, 2)
+    kc_adj_cols_local(PftDev<R> pl, const typename CT<R>::C* __restrict__ band, typename CT<R>::C* __restrict__ Gt,
+                      int nstrips_field, int ntotal) {
+  using C = typename CT<R>::C;
+  constexpr int P = kLocalP;
+  constexpr int LDY = kStripNB + 1;
+  constexpr int NSEQ = RR * kStripNB;
+  constexpr int LDS_ = P + 1;              // Xs[(j1, bb)][u]
+  constexpr int GREC = RR * kStripNB + 1;  // Gs[k1][j1 * 8 + bb]
+  constexpr int MAXIT = 8;
+  static_assert(sizeof(R) == 4, "lane-local cols pass: complex64");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int M1 = pl.M1, M2 = pl.M2, mt1 = pl.mt1;
+  C* Ys = reinterpret_cast<C*>(smem_raw);  // [M1][LDY]
+  C* Xs = Ys + (size_t)M1 * LDY;           // [NSEQ][LDS_]
+  C* Gs = Xs + (size_t)NSEQ * LDS_;        // [P][GREC]
+  C w[P / 2];
+#pragma unroll
+  for (int k = 0; k < P / 2; ++k) w[k] = pl.tw1[k];
+  const int items = M1 * (kStripNB / 2);
+  C pre[MAXIT][2];
+  auto prefetch = [&](int sg) {
+    const int f = sg / nstrips_field, b0 = (sg % nstrips_field) * kStripNB;
+    const C* bf = band + (size_t)f * M1 * M2 + b0;
+#pragma unroll
+    for (int it = 0; it < MAXIT; ++it) {
+      const int e = threadIdx.x + it * kColsThreads;
+      if (e < items) {
+        const int aa = e / (kStripNB / 2), cc = (e % (kStripNB / 2)) * 2;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(bf + (size_t)aa * M2 + cc));
+        pre[it][0] = CT<R>::mk(v.x, v.y);
+        pre[it][1] = CT<R>::mk(v.z, v.w);
+      }
+    }
+  };
+  auto park = [&]() {
+#pragma unroll
+    for (int it = 0; it < MAXIT; ++it) {
+      const int e = threadIdx.x + it * kColsThreads;
+      if (e < items) {
+        const int aa = e / (kStripNB / 2), cc = (e % (kStripNB / 2)) * 2;
+        Ys[(size_t)aa * LDY + cc] = pre[it][0];
+        Ys[(size_t)aa * LDY + cc + 1] = pre[it][1];
+      }
+    }
+  };
+  if ((int)blockIdx.x < ntotal) {
+    prefetch(blockIdx.x);
+    park();
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  const int gu = t >> 3, gbb = t & 7;  // gather thread (u1, bb), t < P * kStripNB
+  for (int sg = blockIdx.x; sg < ntotal; sg += gridDim.x) {
+    const int f = sg / nstrips_field, b0 = (sg % nstrips_field) * kStripNB;
+    const bool more = sg + (int)gridDim.x < ntotal;
+    if (more) prefetch(sg + gridDim.x);  // in flight during the transform below
+    if (t < P * kStripNB) {
+      C x[RR];
+#pragma unroll
+      for (int j = 0; j < RR; ++j) x[j] = czero<C>();
+      for (int aa = (gu + mt1) & (P - 1); aa < M1; aa += P) {
+        const C y = Ys[(size_t)aa * LDY + gbb];
+#pragma unroll
+        for (int j = 0; j < RR; ++j) cmacc(x[j], __ldg(pl.W1t + j * M1 + aa), y);
+      }
+#pragma unroll
+      for (int j = 0; j < RR; ++j) Xs[(size_t)(j * kStripNB + gbb) * LDS_ + gu] = x[j];
+    }
+    __syncthreads();  // Ys consumed, Xs complete
+    if (t < NSEQ) {
+      C x[P];
+#pragma unroll
+      for (int uu = 0; uu < P; ++uu) x[uu] = Xs[(size_t)t * LDS_ + uu];
+      fft_dif_local<P>(x, w, +1);
+#pragma unroll
+      for (int pos = 0; pos < P; ++pos) {
+        constexpr int LP = 5;
+        Gs[(size_t)((__brev((unsigned)pos) >> (32 - LP)) & (P - 1)) * GREC + t] = x[pos];
+      }
+    }
+    if (more) park();
+    __syncthreads();  // Gs complete, Ys refilled
+    C* gf = Gt + (size_t)f * P * RR * M2 + b0;
+    for (int e = threadIdx.x; e < P * RR * (kStripNB / 2); e += blockDim.x) {
+      const int kj = e / (kStripNB / 2), cc = (e % (kStripNB / 2)) * 2;
+      const int k1 = kj / RR, j = kj % RR;
+      const C v0 = Gs[(size_t)k1 * GREC + j * kStripNB + cc], v1 = Gs[(size_t)k1 * GREC + j * kStripNB + cc + 1];
+      *reinterpret_cast<float4*>(gf + (size_t)kj * M2 + cc) = make_float4(v0.x, v0.y, v1.x, v1.y);
+    }
+    __syncthreads();  // Gs drained
+  }
+}
+
 }  // namespace pftg

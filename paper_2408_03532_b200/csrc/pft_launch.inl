@@ -120,7 +120,9 @@ bool fast_cols_ok(const PftDev<R>& pd) {
   bool ok = false;
   dispatch_fast(pd, [&](auto, auto r, auto p) {
     constexpr int RR = decltype(r)::value, P = decltype(p)::value;
-    ok = cols_fwd_smem<R>(P, RR, pd.M1) <= 227 * 1024 && cols_adj_smem<R>(P, RR, pd.M1) <= 227 * 1024;
+    ok = cols_fwd_smem<R>(P, RR, pd.M1) <= 227 * 1024 && cols_adj_smem<R>(P, RR, pd.M1) <= 227 * 1024 &&
+         cols_fwd_local_smem<R>(RR, pd.M1) <= 227 * 1024 && cols_adj_local_smem<R>(RR, pd.M1) <= 227 * 1024 &&
+         (P != kLocalP || pd.M1 <= 2 * 32 * kBandWarps);
   });
   return ok;
 }
@@ -179,19 +181,21 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
     if (const char* e = std::getenv("PFTG_TMA_NS")) ns = std::min(ns, std::atoi(e));
     // warp-specialized version when the double-buffered T still leaves >= 3 ring slots
     int ns2 = 12;
-    while (ns2 > 3 && tma2_rows_smem<R_>(pd.n2, Q, RR, P, ns2) > 227 * 1024) --ns2;
+    while (ns2 > 3 && tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2) > 227 * 1024) --ns2;
     if (const char* e = std::getenv("PFTG_TMA_NS")) ns2 = std::max(3, std::min(ns2, std::atoi(e)));
-    if (!dbg && !std::getenv("PFTG_NO_WS") && tma2_rows_smem<R_>(pd.n2, Q, RR, P, ns2) <= 227 * 1024) {
-      const size_t smem2 = tma2_rows_smem<R_>(pd.n2, Q, RR, P, ns2);
+    const char* d2 = std::getenv("PFTG_DEBUG_WS");
+    const int dbg2 = d2 ? std::atoi(d2) : 0;
+    if (!dbg && !std::getenv("PFTG_NO_WS") && tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2) <= 227 * 1024) {
+      const size_t smem2 = tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2);
       constexpr int NT = kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32;
       auto k = kt2_fwd_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
       if (vc == 2) {
         allow_smem(k);
-        k<<<grid, NT, smem2, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride);
+        k<<<grid, NT, smem2, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride, dbg2);
       } else {
         auto k1 = kt2_fwd_rows<R_, Q, RR, P, 1>;
         allow_smem(k1);
-        k1<<<grid, NT, smem2, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride);
+        k1<<<grid, NT, smem2, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride, dbg2);
       }
       return;
     }
@@ -315,11 +319,22 @@ void launch_fwd_cols<R_>(const PftDev<R_>& pd, int mode, const typename CT<R_>::
     ProfScope prof(st, K_FWD_COLS);
     const bool ok = dispatch_fast(pd, [&](auto q, auto r, auto p) {
       constexpr int RR = decltype(r)::value, P = decltype(p)::value;
+      const int nsf = pd.M2 / kStripNB, total = nsf * batch;
+      int grid = std::min(total, 2 * sm_count());
+      if (const char* e = std::getenv("PFTG_COLS_GRID")) grid = std::min(total, std::atoi(e));
+      if constexpr (P == kLocalP && sizeof(R_) == 4) {
+        if (!std::getenv("PFTG_NO_LOCAL_COLS")) {
+          auto kl = kc_fwd_cols_local<R_, RR>;
+          allow_smem(kl);
+          const char* dc = std::getenv("PFTG_DEBUG_COLS");
+          kl<<<grid, 32 * (kFftWarps + kBandWarps), cols_fwd_local_smem<R_>(RR, pd.M1), st>>>(
+              pd, G, strip_field_elems(pd), band, nsf, total, dc ? std::atoi(dc) : 0);
+          return;
+        }
+      }
       const size_t smem = cols_fwd_smem<R_>(P, RR, pd.M1);
       auto k = kc_fwd_cols<R_, RR, P>;
       allow_smem(k);
-      const int nsf = pd.M2 / kStripNB, total = nsf * batch;
-      const int grid = std::min(total, 2 * sm_count());
       k<<<grid, kColsThreads, smem, st>>>(pd, G, strip_field_elems(pd), band, nsf, total);
     });
     if (!ok) throw std::logic_error("pftg: strip-major G for an unspecialized plan");
@@ -366,11 +381,19 @@ void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, t
   if (fast_cols_ok(pd) && (long long)(pd.M2 / kStripNB) * batch >= 148 && !std::getenv("PFTG_NO_TMA")) {
     dispatch_fast(pd, [&](auto q, auto r, auto p) {
       constexpr int RR = decltype(r)::value, P = decltype(p)::value;
+      const int nsf = pd.M2 / kStripNB, total = nsf * batch;
+      const int grid = std::min(total, 2 * sm_count());
+      if constexpr (P == kLocalP && sizeof(R_) == 4) {
+        if (!std::getenv("PFTG_NO_LOCAL_COLS")) {
+          auto kl = kc_adj_cols_local<R_, RR>;
+          allow_smem(kl);
+          kl<<<grid, kColsThreads, cols_adj_local_smem<R_>(RR, pd.M1), st>>>(pd, band, Gt, nsf, total);
+          return;
+        }
+      }
       const size_t smem = cols_adj_smem<R_>(P, RR, pd.M1);
       auto k = kc_adj_cols<R_, RR, P>;
       allow_smem(k);
-      const int nsf = pd.M2 / kStripNB, total = nsf * batch;
-      const int grid = std::min(total, 2 * sm_count());
       k<<<grid, kColsThreads, smem, st>>>(pd, band, Gt, nsf, total);
     });
     PFTG_LAUNCH_CHECK();

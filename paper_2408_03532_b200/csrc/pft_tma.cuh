@@ -162,9 +162,12 @@ constexpr int fwd_b_warps() {
 }
 
 template <class R>
-__host__ __device__ inline size_t tma2_rows_smem(int n2, int q, int r, int p, int ns) {
+__host__ __device__ inline size_t tma2_rows_smem(int n2, int q, int r, int M2, int p, int ns) {
   using C = typename CT<R>::C;
-  size_t b = sizeof(C) * ((size_t)ns * 2 * n2 + (size_t)r * ldT_of(n2, q) + p / 2 + 1);
+  // complex64: W2 row 0 (Horner band) + a strip-major staging block of the tile's G;
+  // complex128: the full W2 table (direct band contraction)
+  const size_t wtab = sizeof(R) == 4 ? (size_t)M2 + (size_t)(M2 / kStripNB) * strip_rec(r) : (size_t)r * M2;
+  size_t b = sizeof(C) * ((size_t)ns * 2 * n2 + (size_t)r * ldT_of(n2, q) + wtab + p / 2 + 1);
   b = (b + 15) & ~size_t(15);
   return b + (2 * ns + 2) * sizeof(uint64_t);
 }
@@ -172,7 +175,8 @@ __host__ __device__ inline size_t tma2_rows_smem(int n2, int q, int r, int p, in
 template <class R, int Q, int RR, int P, int VC>
 __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32, 1)
     kt2_fwd_rows(PftDev<R> pl, BPar<R, Q, RR> bp, const typename CT<R>::C* __restrict__ z, long long ld,
-                 long long bstride, int ntiles, int NS, typename CT<R>::C* __restrict__ G, long long gstride) {
+                 long long bstride, int ntiles, int NS, typename CT<R>::C* __restrict__ G, long long gstride,
+                 int dbg) {
   using C = typename CT<R>::C;
   constexpr int NBW = fwd_b_warps<RR, P>();
   constexpr int AT = kTmaConsumers, BT = 32 * NBW;
@@ -181,13 +185,22 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
   const int ldT = ldT_of(n2, Q);
   C* ring = reinterpret_cast<C*>(smem_raw);
   C* T = ring + (size_t)NS * 2 * n2;  // [RR][ldT]
-  C* tw2s = T + (size_t)RR * ldT;
+  constexpr bool HORNER = sizeof(R) == 4;
+  constexpr int REC = strip_rec(RR);
+  C* W2s = T + (size_t)RR * ldT;  // complex64: [M2] (row 0) then Gst [M2 / 8][REC]; complex128: [RR][M2]
+  C* Gst = W2s + pl.M2;
+  C* tw2s = W2s + (HORNER ? (size_t)pl.M2 + (size_t)(pl.M2 / kStripNB) * REC : (size_t)RR * pl.M2);
   uint64_t* bars = smem_after<uint64_t>(smem_raw, tw2s + P / 2 + 1, 16);
   uint64_t* full = bars;
   uint64_t* empty = bars + NS;
   uint64_t* tready = bars + 2 * NS;
   uint64_t* tfree = tready + 1;
-  for (int i = threadIdx.x; i < P / 2; i += blockDim.x) tw2s[i] = pl.tw2[i];
+  if constexpr (HORNER) {
+    for (int i = threadIdx.x; i < pl.M2; i += blockDim.x) W2s[i] = pl.W2t[i];
+    for (int i = threadIdx.x; i < pl.p2 / 2; i += blockDim.x) tw2s[i] = pl.tw2[i];
+  } else {
+    fast_load_tables(pl, W2s, tw2s);
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
@@ -235,6 +248,11 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
       const int f = t / pl.p1, k1 = t % pl.p1;
       mbar_wait(tready, i & 1);
+      if (dbg & 1) {  // profiling experiment: group B only hands T back
+        named_sync(2, BT);
+        if (threadIdx.x == AT) mbar_arrive(tfree);
+        continue;
+      }
       C x[S][RR];
 #pragma unroll
       for (int ss = 0; ss < S; ++ss) {
@@ -260,21 +278,59 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
       }
       named_sync(2, BT);  // group B is done reading T: group A may overwrite it
       if (threadIdx.x == AT) mbar_arrive(tfree);
+      if (dbg & 8) {  // profiling experiment: stage B only
+        if (x[0][0].x == 1234.5f) G[0] = x[0][1];
+        continue;
+      }
       fft_dif<S, RR>(x, P, PL, lig, tw2s, -1);
-      if (!valid) continue;
+      if (dbg & 4) {  // profiling experiment: stage B + FFT, no band
+        if (x[0][0].x == 1234.5f) G[0] = x[0][1];
+        continue;
+      }
+      if constexpr (HORNER) {
+        // band by Horner into the staging block, then coalesced record copies:
+        // this tile owns record (strip, k1) = 80 contiguous elements of every strip
+        if (valid) {
 #pragma unroll
-      for (int ss = 0; ss < S; ++ss) {
-        const int u2 = bitrev(ss * PL + lig, LP);
+          for (int ss = 0; ss < S; ++ss) {
+            const int u2 = bitrev(ss * PL + lig, LP);
+            band_horner<RR>(W2s, M2, (u2 + mt2) & (P - 1), P, mt2, R(1) / R(P), x[ss], [&](int b, C v) {
+              Gst[(size_t)(b / kStripNB) * REC + j1 * kStripNB + (b % kStripNB)] = v;
+            });
+          }
+        }
+        named_sync(2, BT);  // staging block complete
+        const int tb = threadIdx.x - AT;
+        constexpr int NREC = RR * kStripNB;
+        const int nrec = M2 / kStripNB;
         if (gstride > 0) {
-          C* gstrip = G + (size_t)f * gstride;
-          constexpr int REC = strip_rec(RR);
-          band_contract<RR>(pl.W2t, M2, (u2 + mt2) & (P - 1), P, RR, x[ss], [&](int b, C v) {
-            gstrip[((size_t)(b / kStripNB) * pl.p1 + k1) * REC + j1 * kStripNB + (b % kStripNB)] = v;
-          });
+          C* gstrip = G + (size_t)f * gstride + (size_t)k1 * REC;
+          for (int e = tb; e < nrec * NREC; e += BT) {
+            const int rr = e / NREC, w = e - rr * NREC;
+            gstrip[(size_t)rr * pl.p1 * REC + w] = Gst[(size_t)rr * REC + w];
+          }
         } else {
           C* Gblk = G + ((size_t)f * pl.p1 + k1) * RR * M2;
-          band_contract<RR>(pl.W2t, M2, (u2 + mt2) & (P - 1), P, RR, x[ss],
-                            [&](int b, C v) { Gblk[(size_t)j1 * M2 + b] = v; });
+          for (int e = tb; e < RR * M2; e += BT) {
+            const int jj = e / M2, b = e - jj * M2;
+            Gblk[e] = Gst[(size_t)(b / kStripNB) * REC + jj * kStripNB + (b % kStripNB)];
+          }
+        }
+      } else {
+        if (!valid) continue;
+#pragma unroll
+        for (int ss = 0; ss < S; ++ss) {
+          const int u2 = bitrev(ss * PL + lig, LP);
+          if (gstride > 0) {
+            C* gstrip = G + (size_t)f * gstride;
+            band_contract<RR>(W2s, M2, (u2 + mt2) & (P - 1), P, RR, x[ss], [&](int b, C v) {
+              gstrip[((size_t)(b / kStripNB) * pl.p1 + k1) * REC + j1 * kStripNB + (b % kStripNB)] = v;
+            });
+          } else {
+            C* Gblk = G + ((size_t)f * pl.p1 + k1) * RR * M2;
+            band_contract<RR>(W2s, M2, (u2 + mt2) & (P - 1), P, RR, x[ss],
+                              [&](int b, C v) { Gblk[(size_t)j1 * M2 + b] = v; });
+          }
         }
       }
     }
@@ -312,6 +368,10 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (dbg & 2) {  // profiling experiment: group A only consumes the ring
+        acc[0][0].x += a[0].x + b[0].y;
+        continue;
+      }
 #pragma unroll
       for (int v = 0; v < VC; ++v) {
         if (pi == 0) {

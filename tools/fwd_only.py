@@ -20,4 +20,5 @@ with KernelProfile() as prof:
     torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
 rows = prof.ms["pft_rows_fwd"] / prof.count["pft_rows_fwd"]
-print(f"{sys.argv[1] if len(sys.argv) > 1 else ''} fwd step {ms*1e3:.1f} us; rows launch {rows*1e3:.1f} us -> {32*8*2**20/rows/1e6:.0f} GB/s (per 32 fields)")
+cols = prof.ms["pft_cols_fwd"] / prof.count["pft_cols_fwd"]
+print(f"{sys.argv[1] if len(sys.argv) > 1 else ''} fwd step {ms*1e3:.1f} us; rows launch {rows*1e3:.1f} us -> {32*8*2**20/rows/1e6:.0f} GB/s (per 32 fields); cols launch {cols*1e3:.1f} us")
