@@ -265,8 +265,8 @@ constexpr int kLocalP = 32;
 // contraction of strip i-1; mbarriers hand the spectrum buffers back and
 // forth, so neither group idles at a block barrier. A band thread owns the
 // rows a and a + 128 (same u1 = (a - mt1) mod 32): every spectrum value it
-// reads from shared memory feeds two rows, and its 2 x r1 W1 coefficients
-// stay in registers (M1 <= 256).
+// reads from shared memory feeds two rows (M1 <= 256), each evaluated by
+// Horner's rule (band_horner, pft_fast.cuh).
 constexpr int kFftWarps = 3, kBandWarps = 4;
 constexpr int kStripBufs = 3;  // strips in flight: covers the L2/HBM latency of a strip load
 
@@ -360,12 +360,9 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
   const int tb = t - FT;
   const int a0 = tb, a1 = tb + BT;
   const bool v0 = a0 < M1, v1 = a1 < M1;
-  C w0[RR], w1[RR];
-#pragma unroll
-  for (int j = 0; j < RR; ++j) {
-    w0[j] = v0 ? __ldg(pl.W1t + (size_t)j * M1 + a0) : czero<C>();
-    w1[j] = v1 ? __ldg(pl.W1t + (size_t)j * M1 + a1) : czero<C>();
-  }
+  // Horner band (band_horner): W1[j][a] = tw(a) base_a^j
+  const C tw0 = v0 ? __ldg(pl.W1t + a0) : czero<C>(), tw1 = v1 ? __ldg(pl.W1t + a1) : czero<C>();
+  const R base0 = static_cast<R>(a0 - mt1) * (R(1) / R(P)), base1 = static_cast<R>(a1 - mt1) * (R(1) / R(P));
   const int ua = (a0 - mt1) & (P - 1);  // == (a1 - mt1) & (P - 1): BT is a multiple of P
   uint32_t i = 0;
   for (int sg = blockIdx.x; sg < ntotal; sg += gridDim.x, ++i) {
@@ -378,15 +375,17 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
       C out0[kStripNB], out1[kStripNB];
 #pragma unroll
       for (int bb = 0; bb < kStripNB; ++bb) {
-        C acc0 = czero<C>(), acc1 = czero<C>();
+        C acc0 = xr[(RR - 1) * kStripNB + bb], acc1 = acc0;
 #pragma unroll
-        for (int j = 0; j < RR; ++j) {
+        for (int j = RR - 2; j >= 0; --j) {
           const C xv = xr[j * kStripNB + bb];
-          cmac(acc0, w0[j], xv);
-          cmac(acc1, w1[j], xv);
+          acc0.x = fma(acc0.x, base0, xv.x);
+          acc0.y = fma(acc0.y, base0, xv.y);
+          acc1.x = fma(acc1.x, base1, xv.x);
+          acc1.y = fma(acc1.y, base1, xv.y);
         }
-        out0[bb] = acc0;
-        out1[bb] = acc1;
+        out0[bb] = cmul(tw0, acc0);
+        out1[bb] = cmul(tw1, acc1);
       }
       C* dst = band + (size_t)f * M1 * M2 + (size_t)a0 * M2 + b0;
 #pragma unroll
@@ -477,11 +476,8 @@ __global__ void __launch_bounds__(kColsThreads, 2)
       C x[RR];
 #pragma unroll
       for (int j = 0; j < RR; ++j) x[j] = czero<C>();
-      for (int aa = (gu + mt1) & (P - 1); aa < M1; aa += P) {
-        const C y = Ys[(size_t)aa * LDY + gbb];
-#pragma unroll
-        for (int j = 0; j < RR; ++j) cmacc(x[j], __ldg(pl.W1t + j * M1 + aa), y);
-      }
+      for (int aa = (gu + mt1) & (P - 1); aa < M1; aa += P)
+        gather_horner<RR>(x, __ldg(pl.W1t + aa), static_cast<R>(aa - mt1) * (R(1) / R(P)), Ys[(size_t)aa * LDY + gbb]);
 #pragma unroll
       for (int j = 0; j < RR; ++j) Xs[(size_t)(j * kStripNB + gbb) * LDS_ + gu] = x[j];
     }

@@ -281,6 +281,21 @@ __device__ __forceinline__ void band_horner(const C* __restrict__ W0, int M, int
   }
 }
 
+// Adjoint of the Horner band (D-dagger gather term): x[j] += conj(W[j][b]) g
+// = base_b^j * (conj(tw(b)) g), with the powers of base_b built incrementally.
+template <int RB, class C, class R>
+__device__ __forceinline__ void gather_horner(C (&x)[RB], C tw, R base, C g) {
+  C p = cmulc(tw, g);
+#pragma unroll
+  for (int j = 0; j < RB; ++j) {
+    x[j] = cadd(x[j], p);
+    if (j + 1 < RB) {
+      p.x *= base;
+      p.y *= base;
+    }
+  }
+}
+
 // Strip-major layout of the rows -> cols intermediate used by the persistent
 // cols pass (pft_cols.cuh): G[f][b / kStripNB][k1][j1 * kStripNB + b % kStripNB],
 // each (strip, k1) record padded by one element (conflict-free k1-strided reads).

@@ -494,8 +494,12 @@ __global__ void __launch_bounds__(32 * (adj_p1_warps<RR, P>() + kAdjP2Warps), 1)
             const int u2 = ss * PL + lig;
             for (int b = (u2 + mt2) & (P - 1); b < M2; b += P) {
               const C g = Gblk[(size_t)j1 * M2 + b];
+              if constexpr (sizeof(R) == 4) {
+                gather_horner<RR>(x[ss], __ldg(W2g + b), static_cast<R>(b - mt2) * (R(1) / R(P)), g);
+              } else {
 #pragma unroll
-              for (int j = 0; j < RR; ++j) cmacc(x[ss][j], __ldg(W2g + j * M2 + b), g);
+                for (int j = 0; j < RR; ++j) cmacc(x[ss][j], __ldg(W2g + j * M2 + b), g);
+              }
             }
           }
         }
