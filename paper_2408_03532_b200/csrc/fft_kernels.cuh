@@ -57,6 +57,17 @@ struct RowEpiArgs {
 template <int S>
 __host__ __device__ inline int fft_lanes(int n) { return n / S < 32 ? n / S : 32; }
 
+// Shared-memory swizzle for bit-reversed gathers over a length-2^lg axis: the
+// lanes of a warp read indices bitrev(s*32 + lane) = (bitrev5(lane) << (lg-5)) | c,
+// which all fall in one bank in a linear layout. XOR-ing the low 4 bits with
+// the bits above (lg-5) spreads them over 16 banks (2 wavefronts per 256 B,
+// the minimum for 8-byte elements); a bijection on [0, 2^lg) (Gray-code style:
+// each low bit is XOR-ed with a strictly higher one). Identity for lg <= 5.
+__device__ __forceinline__ int fft_swz(int i, int lg) {
+  const int sh = lg - 5;
+  return sh > 0 ? i ^ ((i >> sh) & 15) : i;
+}
+
 // grid = (ceil(rows / rows_per_cta), batch); block 256.
 // Each lane group (P lanes, S slots) transforms one row of length n2 = P*S.
 template <class R, int S, int MODE, int EPI>
@@ -99,16 +110,22 @@ __global__ void __launch_bounds__(256) k_fft_rows(int n1, int n2, int lg2, const
     return;
   }
   if (MODE == ROW_DIT_NATURAL) {
+    // coalesced natural loads into this row's shared-memory buffer, then the
+    // bit-reversed gather from shared memory (swizzled: conflict-free)
+    C* rb = tws + ((n2 / 2 + 2) & ~1) + (size_t)(warp * gpw + giw) * n2;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-      const int c = bitrev(s * P + lig, lg2);
+      const int c = s * P + lig;
       C v = czero<C>();
       if (valid) {
         v = srow[c];
         if (prow) v = cmul(prow[c], v);
       }
-      x[s][0] = v;
+      rb[fft_swz(c, lg2)] = v;
     }
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < S; ++s) x[s][0] = rb[fft_swz(bitrev(s * P + lig, lg2), lg2)];
     fft_dit<S, 1>(x, n2, P, lig, tws, sign);
     if (!valid) return;
     C* xr = X + (size_t)f * x_bstride + (size_t)r * n2;
@@ -212,7 +229,7 @@ __global__ void __launch_bounds__(256) k_fft_cols(int n1, int n2, int lg1, int l
                                                   int sign, double* __restrict__ partial) {
   using C = typename CT<R>::C;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int ld = nc + 1;
+  const int ld = nc + 1, ldd = nc + 1;  // padded: conflict-free column reads of the strip / d strip
   C* strip = reinterpret_cast<C*>(smem_raw);
   C* tws = strip + (size_t)n1 * ld;
   R* ds = reinterpret_cast<R*>(tws + n1 / 2 + 1);
@@ -232,7 +249,7 @@ __global__ void __launch_bounds__(256) k_fft_cols(int n1, int n2, int lg1, int l
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int i = base + u * blockDim.x;
-      if (i < tot) strip[(size_t)(i >> lnc) * ld + (i & cm)] = v[u];
+      if (i < tot) strip[(size_t)fft_swz(i >> lnc, lg1) * ld + (i & cm)] = v[u];
     }
   }
   const R* df = nullptr;
@@ -250,7 +267,7 @@ __global__ void __launch_bounds__(256) k_fft_cols(int n1, int n2, int lg1, int l
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int i = base + u * blockDim.x;
-          if (i < tot) ds[(size_t)(i >> lnc) * nc + (i & cm)] = v[u];
+          if (i < tot) ds[(size_t)(i >> lnc) * ldd + (i & cm)] = v[u];
         }
       }
     }
@@ -267,11 +284,11 @@ __global__ void __launch_bounds__(256) k_fft_cols(int n1, int n2, int lg1, int l
     if (MODE == COL_NATURAL) {
 #pragma unroll
       for (int s = 0; s < S; ++s)
-        x[s][0] = valid ? strip[(size_t)bitrev(s * P + lig, lg1) * ld + cc] : czero<C>();
+        x[s][0] = valid ? strip[(size_t)fft_swz(bitrev(s * P + lig, lg1), lg1) * ld + cc] : czero<C>();
       fft_dit<S, 1>(x, n1, P, lig, tws, sign);
       if (valid) {
 #pragma unroll
-        for (int s = 0; s < S; ++s) strip[(size_t)(s * P + lig) * ld + cc] = x[s][0];
+        for (int s = 0; s < S; ++s) strip[(size_t)fft_swz(s * P + lig, lg1) * ld + cc] = x[s][0];
       }
       continue;
     }
@@ -279,20 +296,20 @@ __global__ void __launch_bounds__(256) k_fft_cols(int n1, int n2, int lg1, int l
       // natural-order spectrum column vs the natural measured magnitudes (coalesced d strip)
 #pragma unroll
       for (int s = 0; s < S; ++s)
-        x[s][0] = valid ? strip[(size_t)bitrev(s * P + lig, lg1) * ld + cc] : czero<C>();
+        x[s][0] = valid ? strip[(size_t)fft_swz(bitrev(s * P + lig, lg1), lg1) * ld + cc] : czero<C>();
       fft_dit<S, 1>(x, n1, P, lig, tws, -1);
       if (valid) {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
           const C v = x[s][0];
-          const double e = (double)hypot(v.x, v.y) - (double)ds[(size_t)(s * P + lig) * nc + cc];
+          const double e = (double)hypot(v.x, v.y) - (double)ds[(size_t)(s * P + lig) * ldd + cc];
           local += e * e;
         }
       }
       continue;
     }
 #pragma unroll
-    for (int s = 0; s < S; ++s) x[s][0] = valid ? strip[(size_t)(s * P + lig) * ld + cc] : czero<C>();
+    for (int s = 0; s < S; ++s) x[s][0] = valid ? strip[(size_t)fft_swz(s * P + lig, lg1) * ld + cc] : czero<C>();
     fft_dif<S, 1>(x, n1, P, lig, tws, -1);
     // modulus projection: X <- d * X/|X|  (|X| == 0 -> d)   (solver.cpp:39-40)
 #pragma unroll
@@ -300,7 +317,7 @@ __global__ void __launch_bounds__(256) k_fft_cols(int n1, int n2, int lg1, int l
       const int rp = s * P + lig;  // bit-reversed row position
       R dv = 0;
       if (valid) {
-        if (dmode == 0) dv = ds[(size_t)rp * nc + cc];
+        if (dmode == 0) dv = ds[(size_t)rp * ldd + cc];
         else dv = df[(size_t)bitrev(rp, lg1) * n2 + bitrev(c0 + cc, lg2)];
       }
       const C v = x[s][0];
@@ -326,7 +343,7 @@ __global__ void __launch_bounds__(256) k_fft_cols(int n1, int n2, int lg1, int l
     fft_dit<S, 1>(x, n1, P, lig, tws, +1);
     if (valid) {
 #pragma unroll
-      for (int s = 0; s < S; ++s) strip[(size_t)(s * P + lig) * ld + cc] = x[s][0];
+      for (int s = 0; s < S; ++s) strip[(size_t)fft_swz(s * P + lig, lg1) * ld + cc] = x[s][0];
     }
   }
   if (MODE == COL_EVAL || MODE == COL_EVAL_NAT) {
@@ -343,7 +360,7 @@ __global__ void __launch_bounds__(256) k_fft_cols(int n1, int n2, int lg1, int l
   }
   __syncthreads();
   for (int i = threadIdx.x; i < tot; i += blockDim.x)
-    Xf[(size_t)(i >> lnc) * n2 + c0 + (i & cm)] = strip[(size_t)(i >> lnc) * ld + (i & cm)];
+    Xf[(size_t)(i >> lnc) * n2 + c0 + (i & cm)] = strip[(size_t)fft_swz(i >> lnc, lg1) * ld + (i & cm)];
 }
 
 // d_perm[f][rp][cp] = d[f][bitrev(rp)][bitrev(cp)]  (float or double)

@@ -76,7 +76,9 @@ void launch_fft_rows<R_>(int mode, int epi, int n1, int n2, const RowSrc<R_>& sr
     threads /= 2;
   const int rows_per_cta = threads / 32 * (32 / P);
   const dim3 grid((n1 + rows_per_cta - 1) / rows_per_cta, batch);
-  const size_t smem = sizeof(C_) * (n2 / 2 + 1);
+  size_t smem = sizeof(C_) * (n2 / 2 + 1);
+  // ROW_DIT_NATURAL stages each row in shared memory for its bit-reversed gather
+  if (mode == ROW_DIT_NATURAL) smem = sizeof(C_) * (((n2 / 2 + 2) & ~1) + (size_t)rows_per_cta * n2);
   ProfScope prof(st, K_FFT_ROWS);
   dispatch_slots(S, [&](auto s) {
     constexpr int SS = decltype(s)::value;
@@ -84,8 +86,10 @@ void launch_fft_rows<R_>(int mode, int epi, int n1, int n2, const RowSrc<R_>& sr
       k_fft_rows<R_, SS, ROW_DIF_STORE, EPI_STORE><<<grid, threads, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
                                                                            x_bstride, sign, scale, ep);
     } else if (mode == ROW_DIT_NATURAL) {
-      k_fft_rows<R_, SS, ROW_DIT_NATURAL, EPI_STORE><<<grid, threads, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
-                                                                             x_bstride, sign, scale, ep);
+      auto k = k_fft_rows<R_, SS, ROW_DIT_NATURAL, EPI_STORE>;
+      static bool once = (allow_smem_fft(k), true);
+      (void)once;
+      k<<<grid, threads, smem, st>>>(n1, n2, ilog2(n2), tw, src, X, x_bstride, sign, scale, ep);
     } else if (epi == EPI_STORE) {
       k_fft_rows<R_, SS, ROW_DIT_PROJ, EPI_STORE><<<grid, threads, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
                                                                           x_bstride, sign, scale, ep);
@@ -122,7 +126,7 @@ void launch_fft_cols<R_>(int mode, int n1, int n2, C_* X, long long x_bstride, c
   const int threads = std::max(64, std::min(256, nc * (n1 / S)));  // one lane group per column
   const dim3 grid(n2 / nc, batch);
   size_t smem = sizeof(C_) * ((size_t)n1 * (nc + 1) + n1 / 2 + 1);
-  if (mode != COL_NATURAL && dmode == 0) smem += sizeof(R_) * (size_t)n1 * nc;
+  if (mode != COL_NATURAL && dmode == 0) smem += sizeof(R_) * (size_t)n1 * (nc + 1);
   smem = (smem + 15) & ~size_t(15);
   if (smem < 64 * sizeof(double)) smem = 64 * sizeof(double);
   ProfScope prof(st, K_FFT_COLS);

@@ -378,7 +378,7 @@ template <>
 void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, typename CT<R_>::C* Gt,
                          int batch, cudaStream_t st) {
   ProfScope prof(st, K_ADJ_COLS);
-  if (fast_cols_ok(pd) && (long long)(pd.M2 / kStripNB) * batch >= 148 && !std::getenv("PFTG_NO_TMA")) {
+  if (fast_cols_ok(pd) && (long long)(pd.M2 / kStripNB) * batch >= 64 && !std::getenv("PFTG_NO_TMA")) {
     dispatch_fast(pd, [&](auto q, auto r, auto p) {
       constexpr int RR = decltype(r)::value, P = decltype(p)::value;
       const int nsf = pd.M2 / kStripNB, total = nsf * batch;
