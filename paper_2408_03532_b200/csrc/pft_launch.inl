@@ -158,13 +158,20 @@ bool fast_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C*
 bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* G, int batch, cudaStream_t st,
                   bool strip) {
   const long long gstride = strip ? strip_field_elems(pd) : 0;
-  if (src.offs || src.probe || !src.vec_ok) return false;
+  const bool plain = !src.offs && !src.probe;  // scan windows / exit waves: warp-specialized kernel only
+  // rows must share one 16-byte phase; windows off by 8 bytes (odd complex64
+  // offsets) are handled by the one-column-per-consumer kernel (vc == 1)
+  const bool base_ok = reinterpret_cast<uintptr_t>(src.base) % 16 == 0 && (src.ld * sizeof(typename CT<R_>::C)) % 16 == 0 &&
+                       (src.bstride * sizeof(typename CT<R_>::C)) % 16 == 0 &&
+                       (!src.probe || reinterpret_cast<uintptr_t>(src.probe) % 16 == 0);
+  if (!base_ok) return false;
   if (std::getenv("PFTG_NO_TMA")) return false;
   int vc = 0;
   if (pd.n2 == kTmaConsumers) vc = 1;
   else if (sizeof(R_) == 4 && pd.n2 == 2 * kTmaConsumers) vc = 2;
-  if (!vc || (src.ld % 2) || (src.bstride % 2)) return false;
-  return dispatch_fast(pd, [&](auto q, auto r, auto p) {
+  if (!vc || (vc == 2 && !src.vec_ok)) return false;
+  bool launched = false;
+  const bool matched = dispatch_fast(pd, [&](auto q, auto r, auto p) {
     constexpr int Q = decltype(q)::value, RR = decltype(r)::value, P = decltype(p)::value;
     int ns = 8;
     while (ns > 2 && tma_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns) > 227 * 1024) --ns;
@@ -180,25 +187,31 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
     const int dbg = dv ? std::atoi(dv) : 0;
     if (const char* e = std::getenv("PFTG_TMA_NS")) ns = std::min(ns, std::atoi(e));
     // warp-specialized version when the double-buffered T still leaves >= 3 ring slots
+    const bool wp = src.probe != nullptr;
     int ns2 = 12;
-    while (ns2 > 3 && tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2) > 227 * 1024) --ns2;
+    while (ns2 > 3 && tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, wp) > 227 * 1024) --ns2;
     if (const char* e = std::getenv("PFTG_TMA_NS")) ns2 = std::max(3, std::min(ns2, std::atoi(e)));
     const char* d2 = std::getenv("PFTG_DEBUG_WS");
     const int dbg2 = d2 ? std::atoi(d2) : 0;
-    if (!dbg && !std::getenv("PFTG_NO_WS") && tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2) <= 227 * 1024) {
-      const size_t smem2 = tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2);
+    if (!dbg && !std::getenv("PFTG_NO_WS") && tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, wp) <= 227 * 1024) {
+      const size_t smem2 = tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, wp);
       constexpr int NT = kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32;
       auto k = kt2_fwd_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
       if (vc == 2) {
         allow_smem(k);
-        k<<<grid, NT, smem2, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride, dbg2);
+        k<<<grid, NT, smem2, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride, dbg2, src.offs,
+                                   src.probe);
       } else {
         auto k1 = kt2_fwd_rows<R_, Q, RR, P, 1>;
         allow_smem(k1);
-        k1<<<grid, NT, smem2, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride, dbg2);
+        k1<<<grid, NT, smem2, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride, dbg2, src.offs,
+                                    src.probe);
       }
+      launched = true;
       return;
     }
+    if (!plain || !src.vec_ok) return;  // the single-group kernels stream plain, aligned fields only
+    launched = true;
     if (vc == 2) {
       auto k = kt_fwd_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
       allow_smem(k);
@@ -211,6 +224,7 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
                                                 gstride);
     }
   });
+  return matched && launched;
 }
 
 bool tma_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, const EpiArgs& ep, int batch,

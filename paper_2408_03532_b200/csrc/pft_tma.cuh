@@ -162,29 +162,38 @@ constexpr int fwd_b_warps() {
 }
 
 template <class R>
-__host__ __device__ inline size_t tma2_rows_smem(int n2, int q, int r, int M2, int p, int ns) {
+__host__ __device__ inline size_t tma2_rows_smem(int n2, int q, int r, int M2, int p, int ns, bool probe = false) {
   using C = typename CT<R>::C;
+  const size_t slot = 2 * (size_t)(n2 + 2) + (probe ? 2 * (size_t)n2 : 0);  // row pair (+2: alignment shift) + probe rows
   // complex64: W2 row 0 (Horner band) + a strip-major staging block of the tile's G;
   // complex128: the full W2 table (direct band contraction)
   const size_t wtab = sizeof(R) == 4 ? (size_t)M2 + (size_t)(M2 / kStripNB) * strip_rec(r) : (size_t)r * M2;
-  size_t b = sizeof(C) * ((size_t)ns * 2 * n2 + (size_t)r * ldT_of(n2, q) + wtab + p / 2 + 1);
+  size_t b = sizeof(C) * ((size_t)ns * slot + (size_t)r * ldT_of(n2, q) + wtab + p / 2 + 1);
   b = (b + 15) & ~size_t(15);
   return b + (2 * ns + 2) * sizeof(uint64_t);
 }
 
+// offs != nullptr: field f starts at z + offs[f] (scan windows); probe != nullptr:
+// the exit wave probe .* window is transformed (the probe rows ride in the same
+// ring slot as the window rows, both by bulk copy).
 template <class R, int Q, int RR, int P, int VC>
 __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32, 1)
     kt2_fwd_rows(PftDev<R> pl, BPar<R, Q, RR> bp, const typename CT<R>::C* __restrict__ z, long long ld,
                  long long bstride, int ntiles, int NS, typename CT<R>::C* __restrict__ G, long long gstride,
-                 int dbg) {
+                 int dbg, const long long* __restrict__ offs, const typename CT<R>::C* __restrict__ probe) {
   using C = typename CT<R>::C;
   constexpr int NBW = fwd_b_warps<RR, P>();
   constexpr int AT = kTmaConsumers, BT = 32 * NBW;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int n2 = pl.n2;
   const int ldT = ldT_of(n2, Q);
+  // slot: [row a (n2 + 2)][row b (n2 + 2)][probe row a][probe row b]; a window
+  // that starts 8 bytes past a 16-byte boundary (odd complex64 offset) is copied
+  // from one element earlier and read with shift 1 (one column per consumer)
+  const int lds = n2 + 2;
+  const size_t slot_e = 2 * (size_t)lds + (probe ? 2 * (size_t)n2 : 0);
   C* ring = reinterpret_cast<C*>(smem_raw);
-  C* T = ring + (size_t)NS * 2 * n2;  // [RR][ldT]
+  C* T = ring + (size_t)NS * slot_e;  // [RR][ldT]
   constexpr bool HORNER = sizeof(R) == 4;
   constexpr int REC = strip_rec(RR);
   C* W2s = T + (size_t)RR * ldT;  // complex64: [M2] (row 0) then Gst [M2 / 8][REC]; complex128: [RR][M2]
@@ -220,15 +229,23 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
     uint32_t seq = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int f = t / pl.p1, k1 = t % pl.p1;
-      const C* base = z + (long long)f * bstride + (long long)k1 * Q * ld;
+      const C* base = z + (offs ? offs[f] : (long long)f * bstride) + (long long)k1 * Q * ld;
+      const int sh = (int)((reinterpret_cast<uintptr_t>(base) & 15) / sizeof(C));
+      const uint32_t wbytes = row_bytes + (sh ? 16u : 0u);
+      base -= sh;
+      const C* pbase = probe ? probe + (size_t)k1 * Q * n2 : nullptr;
       for (int pi = 0; pi < Q / 2; ++pi, ++seq) {
         const int s = seq % NS;
         if (seq >= NS) mbar_wait(&empty[s], ((seq / NS) - 1) & 1);
         const int la = pi == 0 ? 0 : pi, lb = pi == 0 ? Q / 2 : Q - pi;
-        mbar_arrive_expect_tx(&full[s], 2 * row_bytes);
-        C* slot = ring + (size_t)s * 2 * n2;
-        bulk_g2s(slot, base + (long long)la * ld, row_bytes, &full[s]);
-        bulk_g2s(slot + n2, base + (long long)lb * ld, row_bytes, &full[s]);
+        mbar_arrive_expect_tx(&full[s], 2 * wbytes + (pbase ? 2 * row_bytes : 0u));
+        C* slot = ring + (size_t)s * slot_e;
+        bulk_g2s(slot, base + (long long)la * ld, wbytes, &full[s]);
+        bulk_g2s(slot + lds, base + (long long)lb * ld, wbytes, &full[s]);
+        if (pbase) {
+          bulk_g2s(slot + 2 * lds, pbase + (size_t)la * n2, row_bytes, &full[s]);
+          bulk_g2s(slot + 2 * lds + n2, pbase + (size_t)lb * n2, row_bytes, &full[s]);
+        }
       }
     }
     return;
@@ -341,6 +358,8 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
   const int c0 = threadIdx.x * VC;
   uint32_t seq = 0, i = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+    // alignment shift of this tile's window rows in the slot (see the producer)
+    const int sh = offs ? (int)((reinterpret_cast<uintptr_t>(z + offs[t / pl.p1]) & 15) / sizeof(C)) : 0;
     C acc[VC][RR];
 #pragma unroll
     for (int v = 0; v < VC; ++v)
@@ -350,11 +369,11 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
     for (int pi = 0; pi < Q / 2; ++pi, ++seq) {
       const int s = seq % NS;
       mbar_wait(&full[s], (seq / NS) & 1);
-      const C* slot = ring + (size_t)s * 2 * n2;
+      const C* slot = ring + (size_t)s * slot_e;
       C a[VC], b[VC];
-      if constexpr (VC == 2 && sizeof(C) == 8) {
+      if constexpr (VC == 2 && sizeof(C) == 8) {  // host guarantees sh == 0 here
         const float4 ta = *reinterpret_cast<const float4*>(slot + c0);
-        const float4 tb = *reinterpret_cast<const float4*>(slot + n2 + c0);
+        const float4 tb = *reinterpret_cast<const float4*>(slot + lds + c0);
         a[0] = CT<R>::mk(ta.x, ta.y);
         a[VC - 1] = CT<R>::mk(ta.z, ta.w);
         b[0] = CT<R>::mk(tb.x, tb.y);
@@ -362,8 +381,15 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
       } else {
 #pragma unroll
         for (int v = 0; v < VC; ++v) {
-          a[v] = slot[c0 + v];
-          b[v] = slot[n2 + c0 + v];
+          a[v] = slot[sh + c0 + v];
+          b[v] = slot[lds + sh + c0 + v];
+        }
+      }
+      if (probe) {  // exit wave: probe * window (stage_a_pairs order)
+#pragma unroll
+        for (int v = 0; v < VC; ++v) {
+          a[v] = cmul(slot[2 * lds + c0 + v], a[v]);
+          b[v] = cmul(slot[2 * lds + n2 + c0 + v], b[v]);
         }
       }
       __syncwarp();

@@ -207,3 +207,29 @@ def test_hybrid_solve_shuffled_matches_reference(ref, w, dtype, pft):
                                              **kw)
     tol = 1e-10 if dtype == np.complex128 else 1e-4
     assert rel_l2(got.frame, f_ref) <= tol and rel_l2(got.probe, p_ref) <= tol
+
+
+def test_evaluator_tma_windows_c64(ref):
+    """cfg4/cfg5 window shape (512^2, band M=128, p=64): the TMA rows pass reads
+    scan windows at even and odd complex64 offsets (8-byte phase shift) and
+    multiplies the probe in-kernel; band and FFT sums vs the reference."""
+    rng = np.random.default_rng(22)
+    w, n = 512, 600
+    obj = (cnormal(rng, (n, n)) * 0.5).astype(np.complex64)
+    probe = cnormal(rng, (w, w)).astype(np.complex64)
+    offs = np.array([[0, 0], [3, 5], [17, 64], [88, 87], [41, 2]], np.int64)
+    d = np.abs(cnormal(rng, (len(offs), w, w))).astype(np.float32) * 20
+    g = P.pft_plan_2d(w, w, 64, 64, 64, 64, 1e-3)
+    assert (g.q1, g.r1, g.p1) == (8, 9, 64)
+    r = ref.RefPlan.create(DATA / "scope_table_v1.txt", w, w, 64, 64, 64, 64, 1e-3)
+    dcrop = np.stack([ref.crop_centered(dj.astype(np.float64), 64, 64) for dj in d]).astype(np.float32)
+    fs, bs = P.evaluate(torch.from_numpy(obj).cuda(), torch.from_numpy(probe).cuda(), offs,
+                        torch.from_numpy(d).cuda(), plan=g, d_crop=torch.from_numpy(dcrop).cuda())
+    o64, p64 = obj.astype(np.complex128), probe.astype(np.complex128)
+    want_b = 0.0
+    for j, (r0, c0) in enumerate(offs):
+        ex = p64 * o64[r0:r0 + w, c0:c0 + w]
+        want_b += np.sum((np.abs(r.apply(ex)) - dcrop[j]) ** 2)
+    want_f = ref.objective_value(o64, p64, offs, d.astype(np.float64)) * len(offs)
+    assert abs(bs - want_b) <= 1e-5 * want_b
+    assert abs(fs - want_f) <= 1e-5 * want_f
