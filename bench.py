@@ -61,6 +61,29 @@ def peaks():
     return 6650.0, "fallback"
 
 
+# ncu --set full capture of the dominant kernel committed under profiles/
+# (tools/profile_round.sh: the first forward rows launch of tools/prof_pft.py,
+# 36 cfg2 fields). Returns DRAM bytes (read + write) per field, or None.
+PROFILE_CAPTURES = {"pft_rows_fwd": ("profiles/r1c_rows_fwd_raw.csv", 36),
+                    "pft_rows_adj": ("profiles/r1c_rows_adj_raw.csv", 36)}
+
+
+def captured_traffic_per_field(kname):
+    import csv
+    ent = PROFILE_CAPTURES.get(kname)
+    if not ent or not (ROOT / ent[0]).exists():
+        return None
+    rows = list(csv.reader(open(ROOT / ent[0])))
+    h = {x: j for j, x in enumerate(rows[0])}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = 0.0
+    for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        if m not in h:
+            return None
+        tot += float(rows[2][h[m]]) * scale.get(rows[1][h[m]], 1)
+    return tot / ent[1]
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -306,7 +329,12 @@ def run_ours(args):
                        "gb_per_s_algorithmic": alg_bytes_step * args.steps / (ms / 1e3) / 1e9 * world,
                        "parallelism": f"weak-scaled replicas x{world}, no data-path collective"},
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm,
-                         "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                         "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": (None if captured_traffic_per_field(kname) is None
+                                     else captured_traffic_per_field(kname) * fields_per_launch),
+                         "traffic_source": "ncu --set full DRAM read+write of the committed capture "
+                                           "(profiles/r1c_*_raw.csv), per field x fields per launch; "
+                                           "algorithmic bytes per launch = %.4g" % (kbytes * fields_per_launch),
                          "peak_kind": peak_kind, "kernel_avg_ms": k_avg_ms,
                          "kernel_ms": prof.ms, "kernel_launches": prof.count},
             "e2e": {"value": e2e_value, "unit": "transforms/s", "h2d_bytes_per_step": h2d,
