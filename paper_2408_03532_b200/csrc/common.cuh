@@ -100,6 +100,74 @@ __device__ __forceinline__ void bmacc(C& acc, R bv, C z, bool odd) {
     acc.y = fma(-bv, z.x, acc.y);
   }
 }
+// acc * s + x (Horner step with a real base)
+template <class C, class R>
+__device__ __forceinline__ C cfmar(C acc, R s, C x) {
+  acc.x = fma(acc.x, s, x.x);
+  acc.y = fma(acc.y, s, x.y);
+  return acc;
+}
+template <class C, class R>
+__device__ __forceinline__ C cscale(C a, R s) { a.x *= s; a.y *= s; return a; }
+
+// ---- complex64: packed f32x2 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2) ----
+// One packed instruction updates both halves of a complex value; each half is
+// rounded exactly like the scalar FFMA/FADD/FMUL it replaces. Non-template
+// overloads, so every complex64 caller of the helpers above picks them up.
+__device__ __forceinline__ unsigned long long f2pk(float2 a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2upk(unsigned long long r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2pk(a)), "l"(f2pk(b)), "l"(f2pk(c)));
+  return f2upk(d);
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2pk(a)), "l"(f2pk(b)));
+  return f2upk(d);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2pk(a)), "l"(f2pk(b)));
+  return f2upk(d);
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2pk(a)), "l"(f2pk(b)));
+  return f2upk(d);
+}
+// a * b = a.x (b.x, b.y) + a.y (-b.y, b.x)
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return f2fma(make_float2(a.x, a.x), b, f2mul(make_float2(a.y, a.y), make_float2(-b.y, b.x)));
+}
+// conj(a) * b = a.x (b.x, b.y) + a.y (b.y, -b.x)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  return f2fma(make_float2(a.x, a.x), b, f2mul(make_float2(a.y, a.y), make_float2(b.y, -b.x)));
+}
+__device__ __forceinline__ void cmac(float2& acc, float2 a, float2 b) {
+  acc = f2fma(make_float2(a.x, a.x), b, acc);
+  acc = f2fma(make_float2(a.y, a.y), make_float2(-b.y, b.x), acc);
+}
+__device__ __forceinline__ void cmacc(float2& acc, float2 a, float2 b) {
+  acc = f2fma(make_float2(a.x, a.x), b, acc);
+  acc = f2fma(make_float2(a.y, a.y), make_float2(b.y, -b.x), acc);
+}
+__device__ __forceinline__ void bmac(float2& acc, float bv, float2 z, bool odd) {
+  acc = odd ? f2fma(make_float2(-bv, bv), make_float2(z.y, z.x), acc) : f2fma(make_float2(bv, bv), z, acc);
+}
+__device__ __forceinline__ void bmacc(float2& acc, float bv, float2 z, bool odd) {
+  acc = odd ? f2fma(make_float2(bv, -bv), make_float2(z.y, z.x), acc) : f2fma(make_float2(bv, bv), z, acc);
+}
+__device__ __forceinline__ float2 cfmar(float2 acc, float s, float2 x) { return f2fma(acc, make_float2(s, s), x); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return f2mul(a, make_float2(s, s)); }
 
 template <class C>
 __device__ __forceinline__ C czero() { C r; r.x = 0; r.y = 0; return r; }
@@ -152,6 +220,7 @@ __device__ __forceinline__ void fft_dif(C (&x)[S][NB], int len, int P, int lig, 
     }
   }
   // cross-lane stages: h = P/2 ... 1
+#pragma unroll
   for (int h = P / 2; h >= 1; h >>= 1) {
     const bool upper = (lig & h) != 0;
     const C w = twiddle(tw, (lig & (h - 1)) * (len / (2 * h)), sign);
@@ -169,6 +238,7 @@ __device__ __forceinline__ void fft_dif(C (&x)[S][NB], int len, int P, int lig, 
 template <int S, int NB, class C>
 __device__ __forceinline__ void fft_dit(C (&x)[S][NB], int len, int P, int lig, const C* tw,
                                         int sign) {
+#pragma unroll
   for (int h = 1; h < P; h <<= 1) {
     const bool upper = (lig & h) != 0;
     const C w = twiddle(tw, (lig & (h - 1)) * (len / (2 * h)), sign);

@@ -273,10 +273,7 @@ __device__ __forceinline__ void band_horner(const C* __restrict__ W0, int M, int
     const R base = static_cast<R>(a - mt) * inv_p;
     C acc = x[RB - 1];
 #pragma unroll
-    for (int j = RB - 2; j >= 0; --j) {
-      acc.x = fma(acc.x, base, x[j].x);
-      acc.y = fma(acc.y, base, x[j].y);
-    }
+    for (int j = RB - 2; j >= 0; --j) acc = cfmar(acc, base, x[j]);
     emit(a, cmul(W0[a], acc));
   }
 }
@@ -289,10 +286,7 @@ __device__ __forceinline__ void gather_horner(C (&x)[RB], C tw, R base, C g) {
 #pragma unroll
   for (int j = 0; j < RB; ++j) {
     x[j] = cadd(x[j], p);
-    if (j + 1 < RB) {
-      p.x *= base;
-      p.y *= base;
-    }
+    if (j + 1 < RB) p = cscale(p, base);
   }
 }
 

@@ -1,6 +1,6 @@
-// Launchers for the PFT kernels; included once per precision by
-// pft_launch_f32.cu / pft_launch_f64.cu (PFTG_REAL = float | double) so the two
-// precisions compile in parallel.
+// Launchers for the PFT kernels; included by pft_launch_{f32,f64}_{fwd,adj,cols}.cu
+// (PFTG_REAL = float | double; PFTG_PART = 1 forward rows, 2 adjoint rows,
+// 3 cols passes) so the six kernel groups compile in parallel.
 #include <mutex>
 #include <set>
 #include <type_traits>
@@ -131,8 +131,19 @@ bool fast_cols_ok(const PftDev<R>& pd) {
 
 using R_ = PFTG_REAL;
 
+#ifndef PFTG_PART
+#define PFTG_PART_FWD 1
+#define PFTG_PART_ADJ 1
+#define PFTG_PART_COLS 1
+#else
+#define PFTG_PART_FWD (PFTG_PART == 1)
+#define PFTG_PART_ADJ (PFTG_PART == 2)
+#define PFTG_PART_COLS (PFTG_PART == 3)
+#endif
+
 namespace {
 
+#if PFTG_PART_FWD
 bool fast_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* G, int batch, cudaStream_t st) {
   return dispatch_fast(pd, [&](auto q, auto r, auto p) {
     constexpr int Q = decltype(q)::value, RR = decltype(r)::value, P = decltype(p)::value;
@@ -193,6 +204,27 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
     if (const char* e = std::getenv("PFTG_TMA_NS")) ns2 = std::max(3, std::min(ns2, std::atoi(e)));
     const char* d2 = std::getenv("PFTG_DEBUG_WS");
     const int dbg2 = d2 ? std::atoi(d2) : 0;
+    if constexpr (sizeof(R_) == 4 && Q == 32) {
+      // wide variant: 256 group-A threads x 4 columns with setmaxnreg (plain complex64 fields, n2 = 1024)
+      constexpr int AT = 256, NT = fwd_rows_threads<AT, RR, P>(true);
+      constexpr int L = (65536 / NT) & ~7, RB = L < 72 ? L : 72;
+      constexpr int RA0 = L + (((NT - AT) * (L - RB) / AT) & ~7), RA = RA0 > 248 ? 248 : RA0;
+      const size_t smem2 = tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, false);
+      if (plain && src.vec_ok && pd.n2 == AT * 4 && !dbg && !std::getenv("PFTG_NO_WS") &&
+          !std::getenv("PFTG_NO_WIDE") && smem2 <= 227 * 1024) {
+        auto k = kt2_fwd_rows<R_, Q, RR, P, 4, AT, RA, RB>;
+        cudaFuncAttributes fa{};
+        PFTG_CUDA(cudaFuncGetAttributes(&fa, k));
+        // the register hand-over must balance within the CTA's launch allocation
+        if (fa.numRegs >= RB && fa.numRegs <= RA && AT * (RA - fa.numRegs) <= (NT - AT) * (fa.numRegs - RB)) {
+          allow_smem(k);
+          k<<<grid, NT, smem2, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride, dbg2, nullptr,
+                                     nullptr);
+          launched = true;
+          return;
+        }
+      }
+    }
     if (!dbg && !std::getenv("PFTG_NO_WS") && tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, wp) <= 227 * 1024) {
       const size_t smem2 = tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, wp);
       constexpr int NT = kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32;
@@ -227,6 +259,9 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
   return matched && launched;
 }
 
+#endif  // PFTG_PART_FWD
+
+#if PFTG_PART_ADJ
 bool tma_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, const EpiArgs& ep, int batch,
                   cudaStream_t st) {
   if (epi != 0 || !ep.vec_ok || std::getenv("PFTG_NO_TMA")) return false;
@@ -247,6 +282,23 @@ bool tma_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, c
     auto* out = reinterpret_cast<typename CT<R_>::C*>(ep.out);
     const char* dv = std::getenv("PFTG_DEBUG_ADJ");
     const int dbg = dv ? std::atoi(dv) : 0;
+    if constexpr (sizeof(R_) == 4 && Q == 32) {
+      // wide variant: 8 P2 warps x 4 columns first, setmaxnreg hand-over (complex64, n2 = 1024)
+      constexpr int P2T = 256, NT = adj_rows_threads<RR, P, P2T>(true);
+      constexpr int L = (65536 / NT) & ~7, RB = L < 72 ? L : 72;
+      constexpr int RA0 = L + (((NT - P2T) * (L - RB) / P2T) & ~7), RA = RA0 > 248 ? 248 : RA0;
+      if (pd.n2 == P2T * 4 && !dbg && !std::getenv("PFTG_NO_WIDE")) {
+        auto k = kt_adj_rows<R_, Q, RR, P, 4, P2T, RA, RB>;
+        cudaFuncAttributes fa{};
+        PFTG_CUDA(cudaFuncGetAttributes(&fa, k));
+        if (fa.numRegs >= RB && fa.numRegs <= RA && P2T * (RA - fa.numRegs) <= (NT - P2T) * (fa.numRegs - RB)) {
+          allow_smem(k);
+          k<<<grid, NT, smem, st>>>(pd, bp, Gt, out, ntiles, 0);
+          launched = true;
+          return;
+        }
+      }
+    }
     constexpr int NT = 32 * (adj_p1_warps<RR, P>() + kAdjP2Warps);
     auto k = kt_adj_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
     allow_smem(k);
@@ -283,8 +335,11 @@ bool fast_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, 
   });
 }
 
+#endif  // PFTG_PART_ADJ
+
 }  // namespace
 
+#if PFTG_PART_FWD
 template <>
 bool launch_fwd_rows<R_>(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* G, int batch,
                          cudaStream_t st, bool want_strip) {
@@ -311,6 +366,9 @@ bool launch_fwd_rows<R_>(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R
   return false;
 }
 
+#endif  // PFTG_PART_FWD
+
+#if PFTG_PART_COLS
 template <>
 long long g_field_elems<R_>(const PftDev<R_>& pd) {
   const long long rowblk = (long long)pd.p1 * pd.r1 * pd.M2;
@@ -426,6 +484,9 @@ void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, t
   PFTG_LAUNCH_CHECK();
 }
 
+#endif  // PFTG_PART_COLS
+
+#if PFTG_PART_ADJ
 template <>
 void launch_adj_rows<R_>(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, const EpiArgs& ep,
                          int batch, cudaStream_t st) {
@@ -458,5 +519,7 @@ void launch_adj_rows<R_>(const PftDev<R_>& pd, int epi, const typename CT<R_>::C
   });
   PFTG_LAUNCH_CHECK();
 }
+
+#endif  // PFTG_PART_ADJ
 
 }  // namespace pftg

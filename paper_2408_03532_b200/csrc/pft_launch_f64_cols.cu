@@ -1,2 +1,3 @@
 #define PFTG_REAL double
+#define PFTG_PART 3
 #include "pft_launch.inl"

@@ -176,14 +176,30 @@ __host__ __device__ inline size_t tma2_rows_smem(int n2, int q, int r, int M2, i
 // offs != nullptr: field f starts at z + offs[f] (scan windows); probe != nullptr:
 // the exit wave probe .* window is transformed (the probe rows ride in the same
 // ring slot as the window rows, both by bulk copy).
-template <class R, int Q, int RR, int P, int VC>
-__global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32, 1)
+//
+// AT = group-A threads. AT = 512 (VC = 2 / 1 columns per thread) is the
+// general layout. AT = 256 with VC = 4 (complex64, n2 = 1024) halves the
+// per-slot overhead (barrier wait / arrive / addressing) per element: each
+// thread owns two column pairs half a row apart (conflict-free LDS.128), and
+// the warpgroups hand registers over with setmaxnreg: group A grows to RA, the
+// group-B + producer warpgroups shrink to RB (the block is padded to whole
+// warpgroups). RA = 0: no register redistribution.
+template <int AT, int RR, int P>
+constexpr int fwd_rows_threads(bool wg_aligned) {
+  const int n = AT + 32 * fwd_b_warps<RR, P>() + 32;
+  return wg_aligned ? (n + 127) / 128 * 128 : n;
+}
+
+template <class R, int Q, int RR, int P, int VC, int AT = kTmaConsumers, int RA = 0, int RB = 0>
+__global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P>(RA > 0), 1)
     kt2_fwd_rows(PftDev<R> pl, BPar<R, Q, RR> bp, const typename CT<R>::C* __restrict__ z, long long ld,
                  long long bstride, int ntiles, int NS, typename CT<R>::C* __restrict__ G, long long gstride,
                  int dbg, const long long* __restrict__ offs, const typename CT<R>::C* __restrict__ probe) {
   using C = typename CT<R>::C;
   constexpr int NBW = fwd_b_warps<RR, P>();
-  constexpr int AT = kTmaConsumers, BT = 32 * NBW;
+  constexpr int BT = 32 * NBW;
+  static_assert(VC != 4 || sizeof(R) == 4, "VC = 4: complex64 only");
+  static_assert(RA == 0 || AT % 128 == 0, "setmaxnreg needs warpgroup-aligned roles");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int n2 = pl.n2;
   const int ldT = ldT_of(n2, Q);
@@ -213,7 +229,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], AT / 32);
+      mbar_init(&empty[s], AT);
     }
     mbar_init(tready, 1);
     mbar_init(tfree, 1);
@@ -222,6 +238,10 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
   __syncthreads();
   const uint32_t row_bytes = (uint32_t)(n2 * sizeof(C));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if constexpr (RA > 0) {
+    if (threadIdx.x < AT) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RA));
+    else asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RB));
+  }
 
   if (threadIdx.x >= AT + BT) {
     // ---------------- producer ----------------
@@ -322,9 +342,16 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
         const int nrec = M2 / kStripNB;
         if (gstride > 0) {
           C* gstrip = G + (size_t)f * gstride + (size_t)k1 * REC;
-          for (int e = tb; e < nrec * NREC; e += BT) {
-            const int rr = e / NREC, w = e - rr * NREC;
-            gstrip[(size_t)rr * pl.p1 * REC + w] = Gst[(size_t)rr * REC + w];
+          if constexpr (BT % NREC == 0) {  // fixed record offset w per thread: no index division
+            constexpr int RSTEP = BT / NREC;
+            const int w = tb % NREC;
+            const size_t gstep = (size_t)pl.p1 * REC;
+            for (int rr = tb / NREC; rr < nrec; rr += RSTEP) gstrip[rr * gstep + w] = Gst[rr * REC + w];
+          } else {
+            for (int e = tb; e < nrec * NREC; e += BT) {
+              const int rr = e / NREC, w = e - rr * NREC;
+              gstrip[(size_t)rr * pl.p1 * REC + w] = Gst[(size_t)rr * REC + w];
+            }
           }
         } else {
           C* Gblk = G + ((size_t)f * pl.p1 + k1) * RR * M2;
@@ -355,8 +382,17 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
   }
 
   // ---------------- group A: stream + stage A -> T ----------------
+  // column of this thread's v-th accumulator
+  auto colv = [&](int v) { return VC == 4 ? 2 * (int)threadIdx.x + (v & 1) + (v >> 1) * (n2 >> 1) : (int)threadIdx.x * VC + v; };
   const int c0 = threadIdx.x * VC;
-  uint32_t seq = 0, i = 0;
+  const bool dbg_stream = VC != 4 && (dbg & 2) != 0;
+  // shared-memory byte address of this thread's first column in slot 0 (VC = 4)
+  const uint32_t abase = smem_u32(ring) + 16u * threadIdx.x;
+  const uint32_t slot_bytes = (uint32_t)(slot_e * sizeof(C));
+  // ring position (slot, phase) advanced incrementally: no division in the unrolled loop
+  int s = 0;
+  uint32_t ph = 0;
+  uint32_t i = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
     // alignment shift of this tile's window rows in the slot (see the producer)
     const int sh = offs ? (int)((reinterpret_cast<uintptr_t>(z + offs[t / pl.p1]) & 15) / sizeof(C)) : 0;
@@ -366,12 +402,23 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
 #pragma unroll
       for (int j = 0; j < RR; ++j) acc[v][j] = czero<C>();
 #pragma unroll
-    for (int pi = 0; pi < Q / 2; ++pi, ++seq) {
-      const int s = seq % NS;
-      mbar_wait(&full[s], (seq / NS) & 1);
+    for (int pi = 0; pi < Q / 2; ++pi) {
+      mbar_wait(&full[s], ph);
       const C* slot = ring + (size_t)s * slot_e;
       C a[VC], b[VC];
-      if constexpr (VC == 2 && sizeof(C) == 8) {  // host guarantees sh == 0 here
+      if constexpr (VC == 4) {  // host guarantees n2 == AT * VC, sh == 0 and no probe here
+        constexpr uint32_t N2 = AT * VC, ROWB = (N2 + 2) * 8;
+        const uint32_t sa = abase + (uint32_t)s * slot_bytes;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const float4 ta = lds128(sa + hh * (N2 / 2) * 8);
+          const float4 tb = lds128(sa + ROWB + hh * (N2 / 2) * 8);
+          a[2 * hh] = CT<R>::mk(ta.x, ta.y);
+          a[2 * hh + 1] = CT<R>::mk(ta.z, ta.w);
+          b[2 * hh] = CT<R>::mk(tb.x, tb.y);
+          b[2 * hh + 1] = CT<R>::mk(tb.z, tb.w);
+        }
+      } else if constexpr (VC == 2 && sizeof(C) == 8) {  // host guarantees sh == 0 here
         const float4 ta = *reinterpret_cast<const float4*>(slot + c0);
         const float4 tb = *reinterpret_cast<const float4*>(slot + lds + c0);
         a[0] = CT<R>::mk(ta.x, ta.y);
@@ -385,16 +432,19 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
           b[v] = slot[lds + sh + c0 + v];
         }
       }
-      if (probe) {  // exit wave: probe * window (stage_a_pairs order)
+      if (VC != 4 && probe) {  // exit wave: probe * window (stage_a_pairs order)
 #pragma unroll
         for (int v = 0; v < VC; ++v) {
           a[v] = cmul(slot[2 * lds + c0 + v], a[v]);
           b[v] = cmul(slot[2 * lds + n2 + c0 + v], b[v]);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      if (dbg & 2) {  // profiling experiment: group A only consumes the ring
+      mbar_arrive(&empty[s]);  // every consumer thread arrives (count AT): no warp sync needed
+      if (++s == NS) {
+        s = 0;
+        ph ^= 1u;
+      }
+      if (dbg_stream) {  // profiling experiment: group A only consumes the ring
         acc[0][0].x += a[0].x + b[0].y;
         continue;
       }
@@ -414,7 +464,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32
     if (i >= 1) mbar_wait(tfree, (i - 1) & 1);  // group B has finished stage B of the previous block
 #pragma unroll
     for (int v = 0; v < VC; ++v) {
-      const int c = c0 + v;
+      const int c = colv(v);
       const int tc = c + c / Q;
 #pragma unroll
       for (int j = 0; j < RR; ++j) T[(size_t)j * ldT + tc] = acc[v][j];
@@ -450,13 +500,27 @@ __host__ __device__ inline size_t tma_adj_smem(int n2, int q, int r, int M2, int
   return b + 128 + 8 * sizeof(uint64_t) + 4096;  // alignment slack, barriers, coefficient tables
 }
 
-template <class R, int Q, int RR, int P, int VC>
-__global__ void __launch_bounds__(32 * (adj_p1_warps<RR, P>() + kAdjP2Warps), 1)
+//
+// Wide variant (RA > 0, complex64, n2 == P2T * VC with VC = 4): P2 is 8 warps
+// (256 threads x 4 columns, two column pairs half a row apart, so each row is
+// exactly one round of 128-bit stores), placed first so the roles are whole
+// warpgroups; setmaxnreg moves registers from P1 (RB) to P2 (RA). The default
+// layout (P1 first, 10 P2 warps x 2 columns) needs 1.6 rounds per row.
+template <int RR, int P, int P2T>
+constexpr int adj_rows_threads(bool wide) {
+  const int n = 32 * adj_p1_warps<RR, P>() + P2T;
+  return wide ? (n + 127) / 128 * 128 : n;
+}
+
+template <class R, int Q, int RR, int P, int VC, int P2T_ = 32 * kAdjP2Warps, int RA = 0, int RB = 0>
+__global__ void __launch_bounds__(adj_rows_threads<RR, P, P2T_>(RA > 0), 1)
     kt_adj_rows(PftDev<R> pl, BPar<R, Q, RR> bp, const typename CT<R>::C* __restrict__ Gt,
                 typename CT<R>::C* __restrict__ out, int ntiles, int dbg) {
   using C = typename CT<R>::C;
   constexpr int NP1 = adj_p1_warps<RR, P>();
-  constexpr int P1T = 32 * NP1, P2T = 32 * kAdjP2Warps;
+  constexpr int P1T = 32 * NP1, P2T = P2T_;
+  constexpr bool WIDE = RA > 0;
+  static_assert(!WIDE || (VC == 4 && sizeof(R) == 4 && P2T % 128 == 0), "wide adjoint rows: complex64, VC = 4");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int n2 = pl.n2, M2 = pl.M2, mt2 = pl.mt2;
   const int ldT = ldT_of(n2, Q);
@@ -494,15 +558,23 @@ __global__ void __launch_bounds__(32 * (adj_p1_warps<RR, P>() + kAdjP2Warps), 1)
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp < NP1) {
+  // role layout: default P1 warps [0, NP1) then P2; wide: P2 threads [0, P2T) then P1, then padding
+  const int p1w = WIDE ? warp - P2T / 32 : warp;
+  if constexpr (WIDE) {
+    if ((int)threadIdx.x < P2T) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RA));
+    else asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RB));
+    if (p1w >= NP1) return;  // padding warps
+  }
+  if (p1w >= 0 && p1w < NP1) {
     // ---------------- P1: gather + inverse FFT + B2-dagger -> T ----------------
     constexpr int PL = P < 32 ? P : 32;
     constexpr int S = P / PL;
     constexpr int GPW = 32 / PL;
     constexpr int LP = (P >= 128) ? 7 : (P >= 64) ? 6 : (P >= 32) ? 5 : (P >= 16) ? 4 : (P >= 8) ? 3 : (P >= 4) ? 2 : 1;
     const int lig = lane & (PL - 1), giw = lane / PL;
-    const int j1 = warp * GPW + giw;
+    const int j1 = p1w * GPW + giw;
     const bool valid = j1 < RR;
+    const bool leader = p1w == 0 && lane == 0;
     uint32_t i = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
       const int s = i & 1;
@@ -548,7 +620,7 @@ __global__ void __launch_bounds__(32 * (adj_p1_warps<RR, P>() + kAdjP2Warps), 1)
         }
       }
       named_sync(1, P1T);  // all of P1 is done with gbuf[s] and T[s]
-      if (threadIdx.x == 0) {
+      if (leader) {
         mbar_arrive(&tready[s]);
         const int tn = t + 2 * (int)gridDim.x;
         if (tn < ntiles) {
@@ -562,7 +634,7 @@ __global__ void __launch_bounds__(32 * (adj_p1_warps<RR, P>() + kAdjP2Warps), 1)
   }
 
   // ---------------- P2: A-dagger expansion + streaming stores ----------------
-  const int tid = threadIdx.x - P1T;
+  const int tid = WIDE ? (int)threadIdx.x : (int)threadIdx.x - P1T;
   uint32_t i = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
     const int s = i & 1;
@@ -570,7 +642,27 @@ __global__ void __launch_bounds__(32 * (adj_p1_warps<RR, P>() + kAdjP2Warps), 1)
     const C* T = Tb + (size_t)s * RR * ldT;
     mbar_wait(&tready[s], (i >> 1) & 1);
     C* o = out + ((size_t)f * pl.n1 + (size_t)k1 * Q) * n2;
-    if (!(dbg & 4)) {
+    if constexpr (WIDE) {
+      // columns 2 tid + {0, 1} and 2 tid + n2 / 2 + {0, 1}; one pass covers the row
+      constexpr int N2 = P2T * VC;
+      C tv[VC][RR];
+#pragma unroll
+      for (int v = 0; v < VC; ++v) {
+        const int c = 2 * tid + (v & 1) + (v >> 1) * (N2 / 2);
+        const int tc = c + c / Q;
+#pragma unroll
+        for (int j = 0; j < RR; ++j) tv[v][j] = T[(size_t)j * ldT + tc];
+      }
+      C* ob = o + 2 * tid;
+      auto store = [&](int l, const C (&z)[VC]) {
+        *reinterpret_cast<float4*>(ob + (size_t)l * N2) = make_float4(z[0].x, z[0].y, z[1].x, z[1].y);
+        *reinterpret_cast<float4*>(ob + (size_t)l * N2 + N2 / 2) = make_float4(z[2].x, z[2].y, z[3].x, z[3].y);
+      };
+      expand_pairs_sm<R, Q, RR, VC>(btab1, tv, store, [&](int l, const C (&zl)[VC], const C (&zm)[VC]) {
+        store(l, zl);
+        store(Q - l, zm);
+      });
+    } else if (!(dbg & 4)) {
       for (int c = tid * VC; c < n2; c += P2T * VC) {
         C tv[VC][RR];
 #pragma unroll

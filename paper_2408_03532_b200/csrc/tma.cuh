@@ -69,6 +69,14 @@ __device__ __forceinline__ T* smem_after(unsigned char* base, const void* after,
   return reinterpret_cast<T*>(base + off);
 }
 
+// 128-bit shared-memory load from a byte address (keeps the address arithmetic
+// explicit: one IMAD per ring slot, immediate offsets for the rest).
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+
 // Named barrier over `count` threads (multiple of 32), id != 0.
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
