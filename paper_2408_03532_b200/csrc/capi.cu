@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -284,17 +285,28 @@ bool vec_ok(const void* p, long long ld, long long bstride) {
 
 // Fields per chunk so the chunk's G workspace (~p1*r1*M2 complex per field)
 // stays well inside L2 between the rows and cols passes.
+// The batch is split into equal chunks (e.g. 100 fields -> 2 x 50, not 73 + 27) so
+// every rows launch ends with a well-filled last round of tiles.
+// 48 MB of G per chunk: with the evict-first hint on the streamed fields it
+// stays L2-resident (126 MB L2). PFTG_CHUNK_MB overrides the budget (profiling).
 template <class R>
-std::size_t chunk_fields(const PftDev<R>& pd) {
+std::size_t chunk_fields(const PftDev<R>& pd, std::size_t batch = 0) {
   const std::size_t g = sizeof(Cx<R>) * (std::size_t)pd.p1 * pd.r1 * pd.M2;
-  std::size_t c = (24u << 20) / std::max<std::size_t>(g, 1);
-  return std::max<std::size_t>(1, std::min<std::size_t>(c, 65535));
+  std::size_t mb = 48;
+  if (const char* e = std::getenv("PFTG_CHUNK_MB")) mb = std::max(1, std::atoi(e));
+  std::size_t c = (mb << 20) / std::max<std::size_t>(g, 1);
+  c = std::max<std::size_t>(1, std::min<std::size_t>(c, 65535));
+  if (batch > c) {
+    const std::size_t k = (batch + c - 1) / c;
+    c = (batch + k - 1) / k;
+  }
+  return c;
 }
 
 template <class R>
 void apply_dev(const pftg_plan* plan, const void* z, void* band, std::size_t batch, cudaStream_t st) {
   const PftDev<R>& pd = plan_dev<R>(*plan);
-  const std::size_t chunk = std::min(batch, chunk_fields(pd));
+  const std::size_t chunk = std::min(batch, chunk_fields(pd, batch));
   const std::size_t gsz = (std::size_t)g_field_elems<R>(pd);
   Scratch G(sizeof(Cx<R>) * gsz * chunk, st);
   const std::size_t nz = (std::size_t)pd.n1 * pd.n2, nb = (std::size_t)pd.M1 * pd.M2;
@@ -311,7 +323,7 @@ void apply_dev(const pftg_plan* plan, const void* z, void* band, std::size_t bat
 template <class R>
 void adjoint_dev(const pftg_plan* plan, const void* band, void* z, std::size_t batch, cudaStream_t st) {
   const PftDev<R>& pd = plan_dev<R>(*plan);
-  const std::size_t chunk = std::min(batch, chunk_fields(pd));
+  const std::size_t chunk = std::min(batch, chunk_fields(pd, batch));
   const std::size_t gsz = (std::size_t)pd.p1 * pd.r1 * pd.M2;
   Scratch G(sizeof(Cx<R>) * gsz * chunk, st);
   const std::size_t nz = (std::size_t)pd.n1 * pd.n2, nb = (std::size_t)pd.M1 * pd.M2;
@@ -329,7 +341,7 @@ template <class R>
 void band_residual_dev(const pftg_plan* plan, const void* exit_wave, const void* dcrop, void* out,
                        std::size_t batch, cudaStream_t st) {
   const PftDev<R>& pd = plan_dev<R>(*plan);
-  const std::size_t chunk = std::min(batch, chunk_fields(pd));
+  const std::size_t chunk = std::min(batch, chunk_fields(pd, batch));
   const std::size_t gsz = (std::size_t)pd.p1 * pd.r1 * pd.M2;
   Scratch G(sizeof(Cx<R>) * gsz * chunk, st), Gt(sizeof(Cx<R>) * gsz * chunk, st);
   const std::size_t nz = (std::size_t)pd.n1 * pd.n2, nb = (std::size_t)pd.M1 * pd.M2;

@@ -176,6 +176,8 @@ __global__ void __launch_bounds__(kColsThreads, 2)
       }
     }
   };
+  griddep_launch_dependents();
+  griddep_wait();  // PDL: the band is the previous kernel's output
   if ((int)blockIdx.x < ntotal) {
     prefetch(blockIdx.x);
     park();
@@ -306,6 +308,8 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
     const int f = sg / nstrips_field, st = sg % nstrips_field;
     return G + (size_t)f * gstride + (size_t)st * sbytes_e;
   };
+  griddep_launch_dependents();
+  griddep_wait();  // PDL: G is the previous kernel's output
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStripBufs; ++s) mbar_init(&full[s], 1);
     for (int s = 0; s < 2; ++s) {
@@ -379,10 +383,8 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
 #pragma unroll
         for (int j = RR - 2; j >= 0; --j) {
           const C xv = xr[j * kStripNB + bb];
-          acc0.x = fma(acc0.x, base0, xv.x);
-          acc0.y = fma(acc0.y, base0, xv.y);
-          acc1.x = fma(acc1.x, base1, xv.x);
-          acc1.y = fma(acc1.y, base1, xv.y);
+          acc0 = cfmar(acc0, base0, xv);
+          acc1 = cfmar(acc1, base1, xv);
         }
         out0[bb] = cmul(tw0, acc0);
         out1[bb] = cmul(tw1, acc1);
@@ -461,6 +463,8 @@ __global__ void __launch_bounds__(kColsThreads, 2)
       }
     }
   };
+  griddep_launch_dependents();
+  griddep_wait();  // PDL: the band is the previous kernel's output
   if ((int)blockIdx.x < ntotal) {
     prefetch(blockIdx.x);
     park();

@@ -64,6 +64,25 @@ void allow_smem(K kernel) {
     PFTG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may be
+// scheduled while its predecessor in the stream drains; it calls
+// griddep_wait() before touching global memory (tma.cuh). PFTG_NO_PDL=1: plain launch.
+template <class... KA, class... A>
+void launch_pdl(void (*kernel)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+  static const bool off = std::getenv("PFTG_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  PFTG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...));
+}
+
 template <class R>
 constexpr int rows_threads() { return sizeof(R) == 4 ? 512 : 256; }
 
@@ -218,8 +237,8 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
         // the register hand-over must balance within the CTA's launch allocation
         if (fa.numRegs >= RB && fa.numRegs <= RA && AT * (RA - fa.numRegs) <= (NT - AT) * (fa.numRegs - RB)) {
           allow_smem(k);
-          k<<<grid, NT, smem2, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride, dbg2, nullptr,
-                                     nullptr);
+          launch_pdl(k, grid, NT, smem2, st, pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride, dbg2,
+                     (const long long*)nullptr, (const typename CT<R_>::C*)nullptr);
           launched = true;
           return;
         }
@@ -293,7 +312,7 @@ bool tma_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, c
         PFTG_CUDA(cudaFuncGetAttributes(&fa, k));
         if (fa.numRegs >= RB && fa.numRegs <= RA && P2T * (RA - fa.numRegs) <= (NT - P2T) * (fa.numRegs - RB)) {
           allow_smem(k);
-          k<<<grid, NT, smem, st>>>(pd, bp, Gt, out, ntiles, 0);
+          launch_pdl(k, grid, NT, smem, st, pd, bp, Gt, out, ntiles, 0);
           launched = true;
           return;
         }
@@ -399,8 +418,8 @@ void launch_fwd_cols<R_>(const PftDev<R_>& pd, int mode, const typename CT<R_>::
           auto kl = kc_fwd_cols_local<R_, RR>;
           allow_smem(kl);
           const char* dc = std::getenv("PFTG_DEBUG_COLS");
-          kl<<<grid, 32 * (kFftWarps + kBandWarps), cols_fwd_local_smem<R_>(RR, pd.M1), st>>>(
-              pd, G, strip_field_elems(pd), band, nsf, total, dc ? std::atoi(dc) : 0);
+          launch_pdl(kl, grid, 32 * (kFftWarps + kBandWarps), cols_fwd_local_smem<R_>(RR, pd.M1), st, pd, G,
+                     (long long)strip_field_elems(pd), band, nsf, total, dc ? std::atoi(dc) : 0);
           return;
         }
       }
@@ -459,7 +478,7 @@ void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, t
         if (!std::getenv("PFTG_NO_LOCAL_COLS")) {
           auto kl = kc_adj_cols_local<R_, RR>;
           allow_smem(kl);
-          kl<<<grid, kColsThreads, cols_adj_local_smem<R_>(RR, pd.M1), st>>>(pd, band, Gt, nsf, total);
+          launch_pdl(kl, grid, kColsThreads, cols_adj_local_smem<R_>(RR, pd.M1), st, pd, band, Gt, nsf, total);
           return;
         }
       }

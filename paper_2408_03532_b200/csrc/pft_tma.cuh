@@ -236,6 +236,8 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P>(RA > 0), 1)
     mbar_fence_init();
   }
   __syncthreads();
+  griddep_launch_dependents();
+  griddep_wait();  // PDL: the previous kernel's writes (and reads of our outputs) are complete
   const uint32_t row_bytes = (uint32_t)(n2 * sizeof(C));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if constexpr (RA > 0) {
@@ -246,6 +248,8 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P>(RA > 0), 1)
   if (threadIdx.x >= AT + BT) {
     // ---------------- producer ----------------
     if (threadIdx.x != AT + BT) return;
+    const uint64_t pol = l2_evict_first_policy();
+    const bool hint = !offs && !(dbg & 16);  // scan windows overlap (L2 reuse): no hint; dbg 16: profiling switch
     uint32_t seq = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int f = t / pl.p1, k1 = t % pl.p1;
@@ -260,8 +264,13 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P>(RA > 0), 1)
         const int la = pi == 0 ? 0 : pi, lb = pi == 0 ? Q / 2 : Q - pi;
         mbar_arrive_expect_tx(&full[s], 2 * wbytes + (pbase ? 2 * row_bytes : 0u));
         C* slot = ring + (size_t)s * slot_e;
-        bulk_g2s(slot, base + (long long)la * ld, wbytes, &full[s]);
-        bulk_g2s(slot + lds, base + (long long)lb * ld, wbytes, &full[s]);
+        if (hint) {
+          bulk_g2s_hint(slot, base + (long long)la * ld, wbytes, &full[s], pol);
+          bulk_g2s_hint(slot + lds, base + (long long)lb * ld, wbytes, &full[s], pol);
+        } else {
+          bulk_g2s(slot, base + (long long)la * ld, wbytes, &full[s]);
+          bulk_g2s(slot + lds, base + (long long)lb * ld, wbytes, &full[s]);
+        }
         if (pbase) {
           bulk_g2s(slot + 2 * lds, pbase + (size_t)la * n2, row_bytes, &full[s]);
           bulk_g2s(slot + 2 * lds + n2, pbase + (size_t)lb * n2, row_bytes, &full[s]);
@@ -540,6 +549,8 @@ __global__ void __launch_bounds__(adj_rows_threads<RR, P, P2T_>(RA > 0), 1)
   stage_btab<R, Q, RR>(bp.b1, btab1);
   stage_btab<R, Q, RR>(bp.b2, btab2);
   const uint32_t blk_bytes = (uint32_t)(RR * M2 * sizeof(C));
+  griddep_launch_dependents();
+  griddep_wait();  // PDL: Gt is the previous kernel's output
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(&gfull[s], 1);
@@ -655,8 +666,9 @@ __global__ void __launch_bounds__(adj_rows_threads<RR, P, P2T_>(RA > 0), 1)
       }
       C* ob = o + 2 * tid;
       auto store = [&](int l, const C (&z)[VC]) {
-        *reinterpret_cast<float4*>(ob + (size_t)l * N2) = make_float4(z[0].x, z[0].y, z[1].x, z[1].y);
-        *reinterpret_cast<float4*>(ob + (size_t)l * N2 + N2 / 2) = make_float4(z[2].x, z[2].y, z[3].x, z[3].y);
+        // streaming (evict-first) stores: the output is not re-read, Gt should stay in L2
+        __stcs(reinterpret_cast<float4*>(ob + (size_t)l * N2), make_float4(z[0].x, z[0].y, z[1].x, z[1].y));
+        __stcs(reinterpret_cast<float4*>(ob + (size_t)l * N2 + N2 / 2), make_float4(z[2].x, z[2].y, z[3].x, z[3].y));
       };
       expand_pairs_sm<R, Q, RR, VC>(btab1, tv, store, [&](int l, const C (&zl)[VC], const C (&zm)[VC]) {
         store(l, zl);

@@ -97,7 +97,7 @@ int main() {
       if (smem * ctas > 228 * 1024) continue;
       const int ncons = 512;  // 16 B per consumer thread per slot row
       const double gbs = timeit([&] { k_ring<<<nsm * ctas, ncons + 32, smem>>>(z, ntiles, rowb, NS, ncons, out); });
-      printf("ring ctas/SM=%d NS=%d (%zu KB in flight/SM): %.0f GB/s\n", ctas, NS, ctas * NS * 2 * rowb / 1024, gbs);
+      printf("ring ctas/SM=%d NS=%d (%d KB in flight/SM): %.0f GB/s\n", ctas, NS, ctas * NS * 2 * rowb / 1024, gbs);
     }
   cudaError_t err = cudaGetLastError();
   printf("status: %s\n", cudaGetErrorString(err));
