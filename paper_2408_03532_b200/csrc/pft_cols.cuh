@@ -269,15 +269,23 @@ constexpr int kLocalP = 32;
 // rows a and a + 128 (same u1 = (a - mt1) mod 32): every spectrum value it
 // reads from shared memory feeds two rows (M1 <= 256), each evaluated by
 // Horner's rule (band_horner, pft_fast.cuh).
-constexpr int kFftWarps = 3, kBandWarps = 4;
-constexpr int kStripBufs = 3;  // strips in flight: covers the L2/HBM latency of a strip load
+// FFT warps = one warpgroup (80 of its 128 threads own a sequence), band
+// warps = two warpgroups (one band row each); setmaxnreg moves registers from
+// the band warps (56) to the FFT warps (128: a whole 32-point transform + 16
+// twiddles per thread) at 2 CTAs per SM (80 registers at launch).
+constexpr int kFftWarps = 4, kBandWarps = 8;
+constexpr int kColsRegLaunch = 80, kColsRegFft = 128, kColsRegBand = 56;
+static_assert(32 * kFftWarps * (kColsRegFft - kColsRegLaunch) <= 32 * kBandWarps * (kColsRegLaunch - kColsRegBand),
+              "register hand-over must balance");
+constexpr int kStripBufs = 2;  // strips in flight (G is L2-resident between the passes)
+constexpr int kBandLd = 10;    // staged band rows: 80-byte stride, 16-byte aligned, conflict-light
 
 template <class R>
 __host__ __device__ inline size_t cols_fwd_local_smem(int r, int M1) {
-  (void)M1;
   using C = typename CT<R>::C;
   const size_t b =
-      sizeof(C) * (kStripBufs * (size_t)kLocalP * strip_rec(r) + 2 * (size_t)kLocalP * (r * kStripNB + 1));
+      sizeof(C) * (kStripBufs * (size_t)kLocalP * strip_rec(r) + 2 * (size_t)kLocalP * (r * kStripNB + 1) +
+                   (size_t)M1 * kBandLd);
   return ((b + 15) & ~size_t(15)) + 128 + (kStripBufs + 4) * sizeof(uint64_t);
 }
 
@@ -299,7 +307,8 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
   const int sbytes_e = P * REC;
   C* buf = reinterpret_cast<C*>(smem_raw);        // [kStripBufs][P * REC]
   C* Xs = buf + kStripBufs * (size_t)sbytes_e;    // [2][P][LDX]
-  uint64_t* bars = smem_after<uint64_t>(smem_raw, Xs + 2 * (size_t)P * LDX, 16);
+  C* Bs = Xs + 2 * (size_t)P * LDX;               // [M1][kBandLd]: the strip's band rows, staged
+  uint64_t* bars = smem_after<uint64_t>(smem_raw, Bs + (size_t)M1 * kBandLd, 16);
   uint64_t* full = bars;                 // TMA -> FFT warps
   uint64_t* xready = bars + kStripBufs;  // FFT -> band warps
   uint64_t* xfree = xready + 2;          // band -> FFT warps
@@ -327,6 +336,8 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
   }
   __syncthreads();
   const int t = threadIdx.x;
+  if (t < FT) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kColsRegFft));
+  else asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kColsRegBand));
   if (t < FT) {
     // ---------------- FFT warps ----------------
     C w[P / 2];  // twiddles, in registers for the CTA's lifetime
@@ -389,20 +400,28 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
         out0[bb] = cmul(tw0, acc0);
         out1[bb] = cmul(tw1, acc1);
       }
-      C* dst = band + (size_t)f * M1 * M2 + (size_t)a0 * M2 + b0;
+      // stage the rows in shared memory: the strip's 8 columns are 64 contiguous
+      // bytes per band row, stored below as 4 rows x 64 B per 16 lanes (whole sectors)
 #pragma unroll
       for (int bb = 0; bb < kStripNB; bb += 2)
-        *reinterpret_cast<float4*>(dst + bb) = make_float4(out0[bb].x, out0[bb].y, out0[bb + 1].x, out0[bb + 1].y);
+        *reinterpret_cast<float4*>(Bs + (size_t)a0 * kBandLd + bb) =
+            make_float4(out0[bb].x, out0[bb].y, out0[bb + 1].x, out0[bb + 1].y);
       if (v1) {
-        dst += (size_t)BT * M2;
 #pragma unroll
         for (int bb = 0; bb < kStripNB; bb += 2)
-          *reinterpret_cast<float4*>(dst + bb) =
+          *reinterpret_cast<float4*>(Bs + (size_t)a1 * kBandLd + bb) =
               make_float4(out1[bb].x, out1[bb].y, out1[bb + 1].x, out1[bb + 1].y);
       }
     }
-    named_sync(2, BT);  // X[s] fully read
+    named_sync(2, BT);  // X[s] fully read, Bs complete
     if (tb == 0) mbar_arrive(&xfree[s]);
+    C* bdst = band + (size_t)f * M1 * M2 + b0;
+    for (int k = tb; k < M1 * (kStripNB / 2); k += BT) {
+      const int row = k / (kStripNB / 2), q = k % (kStripNB / 2);
+      *reinterpret_cast<float4*>(bdst + (size_t)row * M2 + 2 * q) =
+          *reinterpret_cast<const float4*>(Bs + (size_t)row * kBandLd + 2 * q);
+    }
+    named_sync(2, BT);  // Bs drained
   }
 }
 

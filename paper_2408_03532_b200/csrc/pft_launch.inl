@@ -414,8 +414,11 @@ void launch_fwd_cols<R_>(const PftDev<R_>& pd, int mode, const typename CT<R_>::
       int grid = std::min(total, 2 * sm_count());
       if (const char* e = std::getenv("PFTG_COLS_GRID")) grid = std::min(total, std::atoi(e));
       if constexpr (P == kLocalP && sizeof(R_) == 4) {
-        if (!std::getenv("PFTG_NO_LOCAL_COLS")) {
-          auto kl = kc_fwd_cols_local<R_, RR>;
+        auto kl = kc_fwd_cols_local<R_, RR>;
+        cudaFuncAttributes fa{};
+        PFTG_CUDA(cudaFuncGetAttributes(&fa, kl));
+        // setmaxnreg hand-over inside the kernel assumes the launch register count
+        if (!std::getenv("PFTG_NO_LOCAL_COLS") && fa.numRegs == kColsRegLaunch) {
           allow_smem(kl);
           const char* dc = std::getenv("PFTG_DEBUG_COLS");
           launch_pdl(kl, grid, 32 * (kFftWarps + kBandWarps), cols_fwd_local_smem<R_>(RR, pd.M1), st, pd, G,
