@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/pftg.h"
+#include "eval_fft.cuh"
 #include "internal.hpp"
 
 namespace pftg {
@@ -522,7 +523,9 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
   Scratch doffs(sizeof(long long) * std::max<std::size_t>(count, 1), st);
   if (count) PFTG_CUDA(cudaMemcpyAsync(doffs.p, offs.data(), sizeof(long long) * count, cudaMemcpyHostToDevice, st));
   Scratch X(sizeof(Cx<R>) * n * chunk, st);
-  const int nstrips = fft_cols_strips<R>(n2);
+  // complex64 512 x 512 windows (BASELINE configs[4]): radix-8 register FFT kernels (eval_fft.cuh)
+  const bool fast512 = sizeof(R) == 4 && n1 == 512 && n2 == 512 && !std::getenv("PFTG_EVAL_LANEFFT");
+  const int nstrips = fast512 ? 64 : fft_cols_strips<R>(n2);
   Scratch part(sizeof(double) * nstrips * std::max<std::size_t>(count, 1), st);
   std::unique_ptr<Scratch> G, bpart;
   int bstrips = 0;
@@ -537,11 +540,31 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
     // full-FFT objective: rows (natural input, bitrev-gather + DIT) ...
     RowSrc<R> src{static_cast<const Cx<R>*>(frame), (long long)fc, 0, o, static_cast<const Cx<R>*>(probe)};
     RowEpiArgs ep{};
-    // natural-order spectrum (bit-reversed gathers stay on-chip) so the measured
-    // magnitudes are read as coalesced strips
-    launch_fft_rows<R>(ROW_DIT_NATURAL, EPI_STORE, n1, n2, src, X.as<Cx<R>>(), n, -1, 1.0, ep, nb, st);
-    launch_fft_cols<R>(COL_EVAL_NAT, n1, n2, X.as<Cx<R>>(), n, static_cast<const R*>(d) + (pb + c0) * n, n,
-                       nullptr, 0, -1, part.as<double>() + c0 * nstrips, nb, st);
+    if constexpr (sizeof(R) == 4) {
+      if (fast512) {
+        const float2* tw = fft_twiddles<float>(512);
+        {
+          ProfScope prof(st, K_FFT_ROWS);
+          ke_rows512<8><<<dim3(512 / (4 * 8), nb), 256, 0, st>>>(static_cast<const float2*>(frame), (long long)fc, o,
+                                                                 static_cast<const float2*>(probe), tw,
+                                                                 X.as<float2>());
+          PFTG_LAUNCH_CHECK();
+        }
+        {
+          ProfScope prof(st, K_FFT_COLS);
+          ke_cols512_eval<<<dim3(64, nb), 512, 0, st>>>(X.as<float2>(), static_cast<const float*>(d) + (pb + c0) * n,
+                                                        tw, part.as<double>() + c0 * nstrips);
+          PFTG_LAUNCH_CHECK();
+        }
+      }
+    }
+    if (!fast512) {
+      // natural-order spectrum (bit-reversed gathers stay on-chip) so the measured
+      // magnitudes are read as coalesced strips
+      launch_fft_rows<R>(ROW_DIT_NATURAL, EPI_STORE, n1, n2, src, X.as<Cx<R>>(), n, -1, 1.0, ep, nb, st);
+      launch_fft_cols<R>(COL_EVAL_NAT, n1, n2, X.as<Cx<R>>(), n, static_cast<const R*>(d) + (pb + c0) * n, n,
+                         nullptr, 0, -1, part.as<double>() + c0 * nstrips, nb, st);
+    }
     if (pd) {
       bool evec = vec_ok(frame, (long long)fc, 0) && vec_ok(probe, n2, 0);
       for (std::size_t j = c0; j < c0 + nb; ++j) evec = evec && (offs[j] % 2 == 0);

@@ -1,0 +1,175 @@
+// Full-FFT residual of the forward-model evaluator for 512 x 512 complex64
+// windows (BASELINE configs[4]): Phi_j = (1/n) sum_k (|FFT2(P .* z_j)_k| - d_jk)^2
+// (objective_value, /root/reference/proj/core/src/solver.cpp:89-102, in its
+// Parseval form; fast_fft2 forward unnormalized, fft.cpp:92-104).
+//
+// Each 512-point DFT is three radix-8 passes held in registers (Stockham
+// order, 512 = 8 x 8 x 8): a thread owns 8 points, runs an 8-point DFT
+// (24 complex adds), applies the inter-pass twiddles, and exchanges through
+// shared memory; the output comes out in natural order. Compared with the
+// lane-group radix-2 kernels (fft_kernels.cuh: 9 stages, 5 of them shuffle
+// stages) this is ~5x fewer instructions per point.
+//   pass 1: y[t][m]  = DFT8_k x[t + 64k] * W512^(t m)          (t < 64)
+//   pass 2: z[m][t1][j2] = DFT8_t2 y[t1 + 8 t2][m] * W64^(t1 j2)
+//   pass 3: X[m + 8 j2 + 64 j1] = DFT8_t1 z[m][t1][j2]
+// Shared-memory layouts S1[m * 66 + t] and S2[t1 * 72 + j2 * 8 + m] keep
+// every 16-lane phase of the exchanges on distinct banks.
+#pragma once
+
+#include "common.cuh"
+#include "tma.cuh"
+
+namespace pftg {
+
+constexpr int kE512Ld1 = 66, kE512Ld2 = 72, kE512Buf = 8 * kE512Ld2;
+
+// 8-point forward DFT (sign -1), natural in / natural out.
+__device__ __forceinline__ void dft8_fwd(float2 (&a)[8]) {
+  constexpr float r = 0.70710678118654752440f;
+  const float2 b0 = cadd(a[0], a[4]), b1 = cadd(a[1], a[5]), b2 = cadd(a[2], a[6]), b3 = cadd(a[3], a[7]);
+  const float2 d4 = csub(a[0], a[4]), d5 = csub(a[1], a[5]), d6 = csub(a[2], a[6]), d7 = csub(a[3], a[7]);
+  // odd half twiddles: W8^1 = r(1 - i), W8^2 = -i, W8^3 = -r(1 + i)
+  const float2 b5 = f2mul(make_float2(d5.x + d5.y, d5.y - d5.x), make_float2(r, r));
+  const float2 b6 = make_float2(d6.y, -d6.x);
+  const float2 b7 = f2mul(make_float2(d7.y - d7.x, -(d7.x + d7.y)), make_float2(r, r));
+  const float2 c0 = cadd(b0, b2), c2 = csub(b0, b2), c1 = cadd(b1, b3), e3 = csub(b1, b3);
+  const float2 c3 = make_float2(e3.y, -e3.x);
+  const float2 c4 = cadd(d4, b6), c6 = csub(d4, b6), c5 = cadd(b5, b7), e7 = csub(b5, b7);
+  const float2 c7 = make_float2(e7.y, -e7.x);
+  a[0] = cadd(c0, c1);
+  a[4] = csub(c0, c1);
+  a[2] = cadd(c2, c3);
+  a[6] = csub(c2, c3);
+  a[1] = cadd(c4, c5);
+  a[5] = csub(c4, c5);
+  a[3] = cadd(c6, c7);
+  a[7] = csub(c6, c7);
+}
+
+// W512^e for e in [0, 512) from the half table tw[k] = W512^k, k < 256.
+__device__ __forceinline__ float2 w512(const float2* tw, int e) {
+  const float2 w = tw[e & 255];
+  return (e & 256) ? make_float2(-w.x, -w.y) : w;
+}
+
+// Rows: x[r][c] = probe[r][c] * frame[offs[f] + r * ld + c]; X[f][r][:] =
+// DFT_512 of the row, natural order. grid (512 / (4 * RPG), positions), block
+// 256 = four 64-thread groups, each transforming RPG rows.
+template <int RPG>
+__global__ void __launch_bounds__(256, 3) ke_rows512(const float2* __restrict__ frame, long long ld,
+                                                  const long long* __restrict__ offs,
+                                                  const float2* __restrict__ probe, const float2* __restrict__ tw,
+                                                  float2* __restrict__ X) {
+  __shared__ float2 tws[256];
+  __shared__ __align__(16) float2 sbuf[4][kE512Buf];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tws[i] = tw[i];
+  __syncthreads();
+  const int g = threadIdx.x >> 6, l = threadIdx.x & 63;
+  const int f = blockIdx.y;
+  const int m = l & 7, hi = l >> 3;
+  float2* S = sbuf[g];
+  const float2* fr = frame + offs[f];
+  float2* Xf = X + (size_t)f * 512 * 512;
+  // the next row's window and probe values are loaded while this row is transformed
+  float2 nz[8], np[8];
+  auto load_row = [&](int rr) {
+    const int r = (blockIdx.x * RPG + rr) * 4 + g;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      np[k] = probe[(size_t)r * 512 + l + 64 * k];
+      nz[k] = fr[(long long)r * ld + l + 64 * k];
+    }
+  };
+  load_row(0);
+  for (int rr = 0; rr < RPG; ++rr) {
+    const int r = (blockIdx.x * RPG + rr) * 4 + g;
+    float2 a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = cmul(np[k], nz[k]);
+    if (rr + 1 < RPG) load_row(rr + 1);
+    dft8_fwd(a);
+#pragma unroll
+    for (int k = 1; k < 8; ++k) a[k] = cmul(a[k], w512(tws, l * k));  // pass 1: W512^(t m), t = l
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S[k * kE512Ld1 + l] = a[k];
+    named_sync(1 + g, 64);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = S[m * kE512Ld1 + hi + 8 * k];
+    dft8_fwd(a);
+#pragma unroll
+    for (int k = 1; k < 8; ++k) a[k] = cmul(a[k], w512(tws, 8 * hi * k));  // pass 2: W64^(t1 j2)
+    named_sync(1 + g, 64);  // S1 fully read
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S[hi * kE512Ld2 + k * 8 + m] = a[k];
+    named_sync(1 + g, 64);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = S[k * kE512Ld2 + hi * 8 + m];
+    dft8_fwd(a);
+    float2* xr = Xf + (size_t)r * 512;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) xr[l + 64 * k] = a[k];
+    named_sync(1 + g, 64);  // S2 fully read before the next row
+  }
+}
+
+// Columns + residual: a CTA owns 8 adjacent columns of one position (512
+// threads: column c = tid & 7, t = tid >> 3), transforms them and accumulates
+// sum (|X| - d)^2 (d natural, float) into partial[f * 64 + blockIdx.x].
+__global__ void __launch_bounds__(512) ke_cols512_eval(const float2* __restrict__ X, const float* __restrict__ d,
+                                                      const float2* __restrict__ tw, double* __restrict__ partial) {
+  constexpr int CS = kE512Buf + 2;  // per-column buffer stride (== 2 mod 16 banks of 8-byte words)
+  __shared__ float2 tws[256];
+  __shared__ __align__(16) float2 sbuf[8 * CS];
+  __shared__ double red[16];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tws[i] = tw[i];
+  const int c = threadIdx.x & 7, t = threadIdx.x >> 3;
+  const int m = t & 7, hi = t >> 3;
+  const int f = blockIdx.y, c0 = blockIdx.x * 8;
+  const float2* Xf = X + (size_t)f * 512 * 512 + c0 + c;
+  const float* df = d + (size_t)f * 512 * 512 + c0 + c;
+  float2 a[8];
+  float dv[8];  // measured magnitudes of this thread's outputs, loaded up front
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    a[k] = Xf[(size_t)(t + 64 * k) * 512];
+    dv[k] = df[(size_t)(t + 64 * k) * 512];
+  }
+  __syncthreads();  // tws ready
+  dft8_fwd(a);
+#pragma unroll
+  for (int k = 1; k < 8; ++k) a[k] = cmul(a[k], w512(tws, t * k));
+  float2* S = sbuf + c * CS;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) S[k * kE512Ld1 + t] = a[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = S[m * kE512Ld1 + hi + 8 * k];
+  dft8_fwd(a);
+#pragma unroll
+  for (int k = 1; k < 8; ++k) a[k] = cmul(a[k], w512(tws, 8 * hi * k));
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) S[hi * kE512Ld2 + k * 8 + m] = a[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = S[k * kE512Ld2 + hi * 8 + m];
+  dft8_fwd(a);
+  // output k1 = m + 8 hi + 64 j1 = t + 64 j1 (natural row index of the spectrum)
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double e = (double)hypotf(a[k].x, a[k].y) - (double)dv[k];
+    acc += e * e;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 16; ++w) s += red[w];
+    partial[(size_t)f * 64 + blockIdx.x] = s;
+  }
+}
+
+}  // namespace pftg
