@@ -219,17 +219,23 @@ __device__ __forceinline__ void fft_dif(C (&x)[S][NB], int len, int P, int lig, 
       }
     }
   }
-  // cross-lane stages: h = P/2 ... 1
+  // cross-lane stages: h = P/2 ... 1. Branch-free butterfly: x' = (s x + o) w'
+  // with s = -1, w' = w on the upper lane and s = +1, w' = 1 on the lower one
+  // (bit-identical to the select form for finite values: o - x and x + o are
+  // single roundings, and a product with (1, 0) is exact).
+  using Rr = typename RT<C>::R;
 #pragma unroll
   for (int h = P / 2; h >= 1; h >>= 1) {
     const bool upper = (lig & h) != 0;
-    const C w = twiddle(tw, (lig & (h - 1)) * (len / (2 * h)), sign);
+    C w = twiddle(tw, (lig & (h - 1)) * (len / (2 * h)), sign);
+    if (!upper) w = CT<Rr>::mk(Rr(1), Rr(0));
+    const Rr sg = upper ? Rr(-1) : Rr(1);
 #pragma unroll
     for (int s = 0; s < S; ++s)
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         const C o = shfl_xor(x[s][b], h);
-        x[s][b] = upper ? cmul(csub(o, x[s][b]), w) : cadd(x[s][b], o);
+        x[s][b] = cmul(cfmar(x[s][b], sg, o), w);
       }
   }
 }
@@ -238,18 +244,21 @@ __device__ __forceinline__ void fft_dif(C (&x)[S][NB], int len, int P, int lig, 
 template <int S, int NB, class C>
 __device__ __forceinline__ void fft_dit(C (&x)[S][NB], int len, int P, int lig, const C* tw,
                                         int sign) {
+  using Rr = typename RT<C>::R;
 #pragma unroll
   for (int h = 1; h < P; h <<= 1) {
     const bool upper = (lig & h) != 0;
-    const C w = twiddle(tw, (lig & (h - 1)) * (len / (2 * h)), sign);
+    C w = twiddle(tw, (lig & (h - 1)) * (len / (2 * h)), sign);
+    if (!upper) w = CT<Rr>::mk(Rr(1), Rr(0));
+    const Rr sg = upper ? Rr(-1) : Rr(1);
 #pragma unroll
     for (int s = 0; s < S; ++s)
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
-        // lower: a + w*c ; upper: a - w*c, where c is the upper element
-        const C mine = upper ? cmul(x[s][b], w) : x[s][b];
+        // lower: a + w*c ; upper: a - w*c, where c is the upper element (branch-free, see fft_dif)
+        const C mine = cmul(x[s][b], w);
         const C o = shfl_xor(mine, h);
-        x[s][b] = upper ? csub(o, mine) : cadd(mine, o);
+        x[s][b] = cfmar(mine, sg, o);
       }
   }
 #pragma unroll

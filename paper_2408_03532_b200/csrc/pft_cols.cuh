@@ -243,18 +243,25 @@ __global__ void __launch_bounds__(kColsThreads, 2)
 // outputs of a row are stored as one 64-byte segment.
 
 // Radix-2 DIF over N values held by one thread: natural in, bit-reversed out.
-template <int N, class C>
-__device__ __forceinline__ void fft_dif_local(C (&x)[N], const C (&w)[N / 2], int sign) {
+// Twiddle index 0 (w = 1 exactly) skips the multiply: bit-identical for finite
+// values. W: register array or shared-memory pointer of the N/2 twiddles.
+template <int N, class C, class W>
+__device__ __forceinline__ void fft_dif_local(C (&x)[N], const W& w, int sign) {
 #pragma unroll
   for (int h = N / 2; h >= 1; h >>= 1) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       if ((i & h) == 0) {
-        C tw = w[(i & (h - 1)) * (N / (2 * h))];
-        if (sign > 0) tw.y = -tw.y;
+        const int ti = (i & (h - 1)) * (N / (2 * h));
         const C a = x[i], c = x[i + h];
         x[i] = cadd(a, c);
-        x[i + h] = cmul(csub(a, c), tw);
+        if (ti == 0) {
+          x[i + h] = csub(a, c);
+        } else {
+          C tw = w[ti];
+          if (sign > 0) tw.y = -tw.y;
+          x[i + h] = cmul(csub(a, c), tw);
+        }
       }
     }
   }
@@ -429,7 +436,7 @@ template <class R>
 __host__ __device__ inline size_t cols_adj_local_smem(int r, int M1) {
   using C = typename CT<R>::C;
   const size_t b = sizeof(C) * ((size_t)M1 * (kStripNB + 1) + (size_t)r * kStripNB * (kLocalP + 1) +
-                                (size_t)kLocalP * (r * kStripNB + 1));
+                                (size_t)kLocalP * (r * kStripNB + 1) + kLocalP / 2);
   return ((b + 15) & ~size_t(15)) + 128;
 }
 
@@ -438,14 +445,15 @@ __host__ __device__ inline size_t cols_adj_local_smem(int r, int M1) {
 template <class R, int RR>
 __global__ void __launch_bounds__(kColsThreads, 2)
     kc_adj_cols_local(PftDev<R> pl, const typename CT<R>::C* __restrict__ band, typename CT<R>::C* __restrict__ Gt,
-                      int nstrips_field, int ntotal) {
+                      int nstrips_field, int ntotal, int dbg) {
   using C = typename CT<R>::C;
   constexpr int P = kLocalP;
   constexpr int LDY = kStripNB + 1;
   constexpr int NSEQ = RR * kStripNB;
   constexpr int LDS_ = P + 1;              // Xs[(j1, bb)][u]
   constexpr int GREC = RR * kStripNB + 1;  // Gs[k1][j1 * 8 + bb]
-  constexpr int MAXIT = 8;
+  constexpr int MAXIT = 4;  // band strip prefetch: M1 * 4 float4 over 256 threads (launcher: M1 <= 256)
+  // (3 CTAs per SM with shared-memory twiddles measured slower: 35.9 -> 41.4 us per 64 cfg2 fields)
   static_assert(sizeof(R) == 4, "lane-local cols pass: complex64");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int M1 = pl.M1, M2 = pl.M2, mt1 = pl.mt1;
@@ -494,8 +502,8 @@ __global__ void __launch_bounds__(kColsThreads, 2)
   for (int sg = blockIdx.x; sg < ntotal; sg += gridDim.x) {
     const int f = sg / nstrips_field, b0 = (sg % nstrips_field) * kStripNB;
     const bool more = sg + (int)gridDim.x < ntotal;
-    if (more) prefetch(sg + gridDim.x);  // in flight during the transform below
-    if (t < P * kStripNB) {
+    if (more && !(dbg & 8)) prefetch(sg + gridDim.x);  // in flight during the transform below (dbg 8: off)
+    if (t < P * kStripNB && !(dbg & 1)) {  // dbg 1: profiling switch, no gather
       C x[RR];
 #pragma unroll
       for (int j = 0; j < RR; ++j) x[j] = czero<C>();
@@ -505,7 +513,8 @@ __global__ void __launch_bounds__(kColsThreads, 2)
       for (int j = 0; j < RR; ++j) Xs[(size_t)(j * kStripNB + gbb) * LDS_ + gu] = x[j];
     }
     __syncthreads();  // Ys consumed, Xs complete
-    if (t < NSEQ) {
+    if (more && !(dbg & 8)) park();  // before the FFT: the prefetch registers are free for the transform
+    if (t < NSEQ && !(dbg & 2)) {  // dbg 2: no FFT
       C x[P];
 #pragma unroll
       for (int uu = 0; uu < P; ++uu) x[uu] = Xs[(size_t)t * LDS_ + uu];
@@ -516,10 +525,9 @@ __global__ void __launch_bounds__(kColsThreads, 2)
         Gs[(size_t)((__brev((unsigned)pos) >> (32 - LP)) & (P - 1)) * GREC + t] = x[pos];
       }
     }
-    if (more) park();
     __syncthreads();  // Gs complete, Ys refilled
     C* gf = Gt + (size_t)f * P * RR * M2 + b0;
-    for (int e = threadIdx.x; e < P * RR * (kStripNB / 2); e += blockDim.x) {
+    for (int e = threadIdx.x; e < ((dbg & 4) ? 0 : P * RR * (kStripNB / 2)); e += blockDim.x) {  // dbg 4: no stores
       const int kj = e / (kStripNB / 2), cc = (e % (kStripNB / 2)) * 2;
       const int k1 = kj / RR, j = kj % RR;
       const C v0 = Gs[(size_t)k1 * GREC + j * kStripNB + cc], v1 = Gs[(size_t)k1 * GREC + j * kStripNB + cc + 1];

@@ -478,10 +478,12 @@ void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, t
       const int nsf = pd.M2 / kStripNB, total = nsf * batch;
       const int grid = std::min(total, 2 * sm_count());
       if constexpr (P == kLocalP && sizeof(R_) == 4) {
-        if (!std::getenv("PFTG_NO_LOCAL_COLS")) {
+        if (!std::getenv("PFTG_NO_LOCAL_COLS") && pd.M1 <= 256) {
           auto kl = kc_adj_cols_local<R_, RR>;
           allow_smem(kl);
-          launch_pdl(kl, grid, kColsThreads, cols_adj_local_smem<R_>(RR, pd.M1), st, pd, band, Gt, nsf, total);
+          const char* dc = std::getenv("PFTG_DEBUG_ADJCOLS");
+          launch_pdl(kl, grid, kColsThreads, cols_adj_local_smem<R_>(RR, pd.M1), st, pd, band, Gt, nsf, total,
+                     dc ? std::atoi(dc) : 0);
           return;
         }
       }
