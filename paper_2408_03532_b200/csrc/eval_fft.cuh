@@ -52,6 +52,169 @@ __device__ __forceinline__ float2 w512(const float2* tw, int e) {
   return (e & 256) ? make_float2(-w.x, -w.y) : w;
 }
 
+__device__ __forceinline__ float2 cswapri(float2 v) { return make_float2(v.y, v.x); }
+
+// 8-point DFT of either sign: the +1 transform is swap(DFT_-1(swap(x))), swap(a + ib) = b + ia.
+template <int SIGN>
+__device__ __forceinline__ void dft8(float2 (&a)[8]) {
+  if constexpr (SIGN < 0) {
+    dft8_fwd(a);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = cswapri(a[k]);
+    dft8_fwd(a);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = cswapri(a[k]);
+  }
+}
+
+template <int SIGN>
+__device__ __forceinline__ float2 w512s(const float2* tw, int e) {
+  float2 w = w512(tw, e);
+  if (SIGN > 0) w.y = -w.y;
+  return w;
+}
+
+// One unnormalized 512-point DFT (sign SIGN) held by a group of 64 threads,
+// thread role l in [0, 64): in a[k] = x[l + 64 k], out a[j] = X[l + 64 j]
+// (natural order on both sides, so a forward and an inverse transform chain
+// without an exchange). S: >= kE512Buf complex of shared memory private to the
+// group; sync(): barrier over the group. The caller syncs before reusing S.
+template <int SIGN, class Sync>
+__device__ __forceinline__ void fft512(float2 (&a)[8], float2* S, const float2* tws, int l, Sync&& sync) {
+  const int m = l & 7, hi = l >> 3;
+  dft8<SIGN>(a);
+#pragma unroll
+  for (int k = 1; k < 8; ++k) a[k] = cmul(a[k], w512s<SIGN>(tws, l * k));
+#pragma unroll
+  for (int k = 0; k < 8; ++k) S[k * kE512Ld1 + l] = a[k];
+  sync();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = S[m * kE512Ld1 + hi + 8 * k];
+  dft8<SIGN>(a);
+#pragma unroll
+  for (int k = 1; k < 8; ++k) a[k] = cmul(a[k], w512s<SIGN>(tws, 8 * hi * k));
+  sync();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) S[hi * kE512Ld2 + k * 8 + m] = a[k];
+  sync();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = S[k * kE512Ld2 + hi * 8 + m];
+  dft8<SIGN>(a);
+}
+
+// ---- full-FFT ePIE stage for 512 x 512 complex64 windows (solver.cpp:237-262) ----
+// Same operator sequence as the lane-group kernels (fft_kernels.cuh): rows
+// forward -> cols forward + modulus projection + inverse -> rows inverse x 1/n
+// with the object update (+ the forward row transform of the new exit wave,
+// blind mode) -> cols -> rows inverse with the probe update; the spectrum is
+// in natural order, so the projection reads the measured magnitudes d as is.
+enum { E512_FWD = 0, E512_OBJ = 1, E512_PROBE = 2 };
+
+// grid 128, block 256 (four 64-thread groups, one window row each).
+// frame + *off: the window (row stride ld); X: rows in, X2: fused forward out (E512_OBJ).
+template <int MODE>
+__global__ void __launch_bounds__(256) ke_rows512_epie(const float2* __restrict__ tw, float2* frame, long long ld,
+                                                       const long long* __restrict__ off, float2* probe,
+                                                       float2* X, float2* X2, float scale, float step, int fuse) {
+  __shared__ float2 tws[256];
+  __shared__ __align__(16) float2 sbuf[4][kE512Buf];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tws[i] = tw[i];
+  __syncthreads();
+  const int g = threadIdx.x >> 6, l = threadIdx.x & 63;
+  const int r = blockIdx.x * 4 + g;
+  float2* S = sbuf[g];
+  auto gsync = [&]() { named_sync(1 + g, 64); };
+  float2* orow = frame + *off + (long long)r * ld;
+  float2* prow = probe + (size_t)r * 512;
+  float2 a[8];
+  if (MODE == E512_FWD) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = cmul(prow[l + 64 * k], orow[l + 64 * k]);
+    fft512<-1>(a, S, tws, l, gsync);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) X[(size_t)r * 512 + l + 64 * k] = a[k];
+    return;
+  }
+  const float2* xin = (MODE == E512_OBJ ? X : X2) + (size_t)r * 512;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = xin[l + 64 * k];
+  fft512<+1>(a, S, tws, l, gsync);
+  if (MODE == E512_OBJ) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c = l + 64 * k;
+      float2 proj = a[k];
+      proj.x *= scale;
+      proj.y *= scale;
+      const float2 pv = prow[c];
+      float2 o = orow[c];
+      const float2 resid = csub(cmul(pv, o), proj);  // probe*z - projected
+      const float2 gr = cmulc(pv, resid);
+      o.x -= step * gr.x;
+      o.y -= step * gr.y;
+      orow[c] = o;
+      a[k] = cmul(pv, o);  // new exit wave (solver.cpp:256)
+    }
+    if (fuse) {
+      gsync();  // S free
+      fft512<-1>(a, S, tws, l, gsync);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) X2[(size_t)r * 512 + l + 64 * k] = a[k];
+    }
+    return;
+  }
+  // E512_PROBE
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int c = l + 64 * k;
+    float2 proj = a[k];
+    proj.x *= scale;
+    proj.y *= scale;
+    float2 pv = prow[c];
+    const float2 o = orow[c];
+    const float2 resid = csub(cmul(pv, o), proj);
+    const float2 gr = cmulc(o, resid);
+    pv.x -= step * gr.x;
+    pv.y -= step * gr.y;
+    prow[c] = pv;
+  }
+}
+
+// Columns: forward DFT, modulus projection X <- d X/|X| (|X| = 0 -> d;
+// solver.cpp:35-42) against the natural-order magnitudes, inverse DFT
+// (unnormalized; the row pass scales), in place. grid 512 / NCOL, block 64 NCOL.
+template <int NCOL>
+__global__ void __launch_bounds__(64 * NCOL) ke_cols512_proj(float2* X, const float* __restrict__ d,
+                                                             const float2* __restrict__ tw) {
+  constexpr int CS = kE512Buf + 2;
+  __shared__ float2 tws[256];
+  __shared__ __align__(16) float2 sbuf[NCOL * CS];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tws[i] = tw[i];
+  const int c = threadIdx.x % NCOL, t = threadIdx.x / NCOL;
+  const int col = blockIdx.x * NCOL + c;
+  float2 a[8];
+  float dv[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    a[k] = X[(size_t)(t + 64 * k) * 512 + col];
+    dv[k] = d[(size_t)(t + 64 * k) * 512 + col];
+  }
+  __syncthreads();  // tws ready
+  float2* S = sbuf + c * CS;
+  auto bsync = []() { __syncthreads(); };
+  fft512<-1>(a, S, tws, t, bsync);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float mag = hypotf(a[k].x, a[k].y);
+    a[k] = mag > 0.f ? make_float2(dv[k] * (a[k].x / mag), dv[k] * (a[k].y / mag)) : make_float2(dv[k], 0.f);
+  }
+  __syncthreads();  // S free
+  fft512<+1>(a, S, tws, t, bsync);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) X[(size_t)(t + 64 * k) * 512 + col] = a[k];
+}
+
 // Rows: x[r][c] = probe[r][c] * frame[offs[f] + r * ld + c]; X[f][r][:] =
 // DFT_512 of the row, natural order. grid (512 / (4 * RPG), positions), block
 // 256 = four 64-thread groups, each transforming RPG rows.
@@ -115,7 +278,7 @@ __global__ void __launch_bounds__(256, 3) ke_rows512(const float2* __restrict__ 
 // Columns + residual: a CTA owns 8 adjacent columns of one position (512
 // threads: column c = tid & 7, t = tid >> 3), transforms them and accumulates
 // sum (|X| - d)^2 (d natural, float) into partial[f * 64 + blockIdx.x].
-__global__ void __launch_bounds__(512) ke_cols512_eval(const float2* __restrict__ X, const float* __restrict__ d,
+static __global__ void __launch_bounds__(512) ke_cols512_eval(const float2* __restrict__ X, const float* __restrict__ d,
                                                       const float2* __restrict__ tw, double* __restrict__ partial) {
   constexpr int CS = kE512Buf + 2;  // per-column buffer stride (== 2 mod 16 banks of 8-byte words)
   __shared__ float2 tws[256];

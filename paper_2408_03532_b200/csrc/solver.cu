@@ -29,6 +29,7 @@
 #include <stdexcept>
 #include <vector>
 
+#include "eval_fft.cuh"
 #include "../../include/pftg.h"
 #include "internal.hpp"
 
@@ -153,6 +154,13 @@ namespace {
 template <class R>
 using Cx = typename CT<R>::C;
 
+// Full-FFT stage and objective on the radix-8 register FFT kernels (eval_fft.cuh):
+// complex64 512 x 512 windows. PFTG_EPIE_LANEFFT=1 keeps the lane-group kernels.
+inline bool use_fft512(const pftg_solver& s) {
+  static const bool off = std::getenv("PFTG_EPIE_LANEFFT") != nullptr;
+  return !off && s.wr == 512 && s.wc == 512;
+}
+
 template <class R>
 void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
   const cudaStream_t st = s.st;
@@ -189,6 +197,42 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
     }
     return;
   }
+  if constexpr (sizeof(R) == 4) {
+    if (use_fft512(s)) {
+      // 512 x 512 complex64 windows (BASELINE configs[3]): radix-8 register FFTs, natural-order spectrum
+      const float2* tw = fft_twiddles<float>(512);
+      float2* fr = reinterpret_cast<float2*>(frame);
+      float2* pr = reinterpret_cast<float2*>(probe);
+      float2* X = static_cast<float2*>(s.X);
+      float2* X2 = static_cast<float2*>(s.X2);
+      const float* dn = static_cast<const float*>(s.d) + (long long)j * n;
+      const float scale = 1.0f / static_cast<float>(n);
+      {
+        ProfScope prof(st, K_FFT_ROWS);
+        ke_rows512_epie<E512_FWD><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, 1.f, 0.f, 0);
+      }
+      {
+        ProfScope prof(st, K_FFT_COLS);
+        ke_cols512_proj<4><<<128, 256, 0, st>>>(X, dn, tw);
+      }
+      {
+        ProfScope prof(st, K_FFT_ROWS);
+        ke_rows512_epie<E512_OBJ><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, scale,
+                                                       (float)s.cfg.beta, blind ? 1 : 0);
+      }
+      if (blind) {
+        {
+          ProfScope prof(st, K_FFT_COLS);
+          ke_cols512_proj<4><<<128, 256, 0, st>>>(X2, dn, tw);
+        }
+        ProfScope prof(st, K_FFT_ROWS);
+        ke_rows512_epie<E512_PROBE><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, scale,
+                                                         (float)s.cfg.gamma, 0);
+      }
+      PFTG_LAUNCH_CHECK();
+      return;
+    }
+  }
   const R* dp = static_cast<const R*>(s.dperm) + (long long)j * n;
   RowSrc<R> src{frame, (long long)s.fc, 0, doff, probe};
   RowEpiArgs ep{};
@@ -222,9 +266,27 @@ double objective(pftg_solver& s) {
   // (1/N) sum_j (1/n) sum_k (|X_jk| - d_jk)^2  (Parseval form of solver.cpp:89-102)
   const int n1 = (int)s.wr, n2 = (int)s.wc;
   const long long n = (long long)n1 * n2;
-  const int strips = fft_cols_strips<R>(n2);
+  const bool f512 = sizeof(R) == 4 && use_fft512(s);
+  const int strips = f512 ? 64 : fft_cols_strips<R>(n2);
   for (std::size_t c0 = 0; c0 < s.npos; c0 += s.eval_chunk) {
     const int nb = (int)std::min(s.eval_chunk, s.npos - c0);
+    if constexpr (sizeof(R) == 4) {
+      if (f512) {
+        const float2* tw = fft_twiddles<float>(512);
+        {
+          ProfScope prof(s.st, K_FFT_ROWS);
+          ke_rows512<8><<<dim3(16, nb), 256, 0, s.st>>>(static_cast<const float2*>(s.frame), (long long)s.fc,
+                                                         s.doffs + c0, static_cast<const float2*>(s.probe), tw,
+                                                         static_cast<float2*>(s.Xe));
+        }
+        ProfScope prof(s.st, K_FFT_COLS);
+        ke_cols512_eval<<<dim3(64, nb), 512, 0, s.st>>>(static_cast<const float2*>(s.Xe),
+                                                        static_cast<const float*>(s.d) + c0 * n, tw,
+                                                        s.part + c0 * strips);
+        PFTG_LAUNCH_CHECK();
+        continue;
+      }
+    }
     RowSrc<R> src{static_cast<const Cx<R>*>(s.frame), (long long)s.fc, 0, s.doffs + c0,
                   static_cast<const Cx<R>*>(s.probe)};
     RowEpiArgs ep{};
@@ -381,7 +443,8 @@ void create(pftg_solver& s, const void* frame, const void* probe, const int64_t*
   PFTG_CUDA(cudaMalloc(&s.X2, sizeof(Cx<R>) * pn));
   s.eval_chunk = std::max<std::size_t>(1, std::min<std::size_t>(s.npos, (64u << 20) / (sizeof(Cx<R>) * pn)));
   PFTG_CUDA(cudaMalloc(&s.Xe, sizeof(Cx<R>) * pn * s.eval_chunk));
-  PFTG_CUDA(cudaMalloc(&s.part, sizeof(double) * fft_cols_strips<R>((int)s.wc) * std::max<std::size_t>(s.npos, 1)));
+  PFTG_CUDA(cudaMalloc(&s.part, sizeof(double) * std::max(64, fft_cols_strips<R>((int)s.wc)) *
+                                    std::max<std::size_t>(s.npos, 1)));
   PFTG_CUDA(cudaMalloc(&s.red, sizeof(double) * 2 * kRedBlocks));
   (void)fft_twiddles<R>((int)s.wr);
   (void)fft_twiddles<R>((int)s.wc);

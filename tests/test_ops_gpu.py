@@ -192,10 +192,12 @@ def test_cfg3_full_problem_one_band_one_fft_sweep(ref):
 
 
 
-@pytest.mark.parametrize("w,dtype,pft", [(64, np.complex128, 1), (128, np.complex128, 0), (64, np.complex64, 1)])
+@pytest.mark.parametrize("w,dtype,pft", [(64, np.complex128, 1), (128, np.complex128, 0), (64, np.complex64, 1),
+                                         (512, np.complex64, 1)])
 def test_hybrid_solve_shuffled_matches_reference(ref, w, dtype, pft):
     """Shuffled visit order (the reference's mt19937_64 Fisher-Yates stream,
-    solver.cpp:164-169) through the band and full-FFT stages, blind."""
+    solver.cpp:164-169) through the band and full-FFT stages, blind. w = 512
+    complex64 runs the radix-8 register FFT stage and objective (eval_fft.cuh)."""
     rng = np.random.default_rng(31)
     obj, probe, offs = _small_problem(rng, n=2 * w + 32, w=w, npos=9)
     d = ref.simulate(obj, probe, offs)

@@ -166,3 +166,22 @@ def test_cfg2_kernel_shape_well_conditioned(ref, dtype, tol):
     for b in (0, 17, 36):
         assert rel_l2(band[b], r.apply(z[b].astype(np.complex128))) <= tol
         assert rel_l2(back[b], r.adjoint(band[b].astype(np.complex128))) <= tol
+
+
+@pytest.mark.gpu
+def test_cfg2_kernel_shape_two_chunks_c64(ref, monkeypatch):
+    """Batch 75 of 1024^2 complex64 on the cfg2 kernel shape: two equal chunks
+    (38 + 37 fields) share one G workspace, and the four kernels of each chunk
+    run as a programmatic-dependent-launch chain, so chunk 2's rows pass
+    overwrites G right behind chunk 1's cols pass. Fields on both sides of the
+    chunk boundary are checked against the reference."""
+    g, r = _plans(ref, DATA / "scope_table_v1.txt", 1024, 1024, 40, 40, 32, 32, 1e-3)
+    # 8 MB of G per chunk (~205 KB per field for this plan) -> 2 chunks of 38 + 37
+    monkeypatch.setenv("PFTG_CHUNK_MB", "8")
+    rng = np.random.default_rng(23)
+    z = cnormal(rng, (75, 1024, 1024), np.complex64)
+    band = P.pft_apply_2d(g, torch.from_numpy(z).cuda()).cpu().numpy()
+    back = P.pft_adjoint_2d(g, torch.from_numpy(band).cuda()).cpu().numpy()
+    for b in (0, 37, 38, 74):
+        assert rel_l2(band[b], r.apply(z[b].astype(np.complex128))) <= TOL64, b
+        assert rel_l2(back[b], r.adjoint(band[b].astype(np.complex128))) <= TOL64, b
