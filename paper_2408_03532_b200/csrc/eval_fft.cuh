@@ -215,6 +215,178 @@ __global__ void __launch_bounds__(64 * NCOL) ke_cols512_proj(float2* X, const fl
   for (int k = 0; k < 8; ++k) X[(size_t)(t + 64 * k) * 512 + col] = a[k];
 }
 
+// ---- 256-point variant (BASELINE configs[2] windows) ----
+// 256 = 8 x (8 x 4): a group of 32 threads (one warp) holds one transform,
+// thread l owns x[l + 32 k]. pass 1: DFT8 over k, twiddle W256^(l m);
+// pass 2: thread (m, t1) = (l & 7, l >> 3) runs DFT8 over t2 of y[t1 + 4 t2][m],
+// twiddle W32^(t1 j2); pass 3: thread l runs two DFT4s over t1 for
+// (m, j2) = (l & 7, (l >> 3) + 4 h), h = 0, 1, and ends holding X[l + 32 k]
+// (K = m + 8 j2 + 64 j1 = l + 32 (h + 2 j1)): natural order in and out.
+constexpr int kE256Ld1 = 33, kE256Ld2 = 9, kE256Buf = 32 * kE256Ld2;
+
+__device__ __forceinline__ void dft4_fwd(float2& a0, float2& a1, float2& a2, float2& a3) {
+  const float2 b0 = cadd(a0, a2), b1 = csub(a0, a2), b2 = cadd(a1, a3), e3 = csub(a1, a3);
+  const float2 b3 = make_float2(e3.y, -e3.x);  // * (-i)
+  a0 = cadd(b0, b2);
+  a2 = csub(b0, b2);
+  a1 = cadd(b1, b3);
+  a3 = csub(b1, b3);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft4(float2& a0, float2& a1, float2& a2, float2& a3) {
+  if constexpr (SIGN < 0) {
+    dft4_fwd(a0, a1, a2, a3);
+  } else {
+    a0 = cswapri(a0); a1 = cswapri(a1); a2 = cswapri(a2); a3 = cswapri(a3);
+    dft4_fwd(a0, a1, a2, a3);
+    a0 = cswapri(a0); a1 = cswapri(a1); a2 = cswapri(a2); a3 = cswapri(a3);
+  }
+}
+
+// W256^e for e in [0, 256) from the half table tw[k] = W256^k, k < 128.
+template <int SIGN>
+__device__ __forceinline__ float2 w256s(const float2* tw, int e) {
+  float2 w = tw[e & 127];
+  if (e & 128) w = make_float2(-w.x, -w.y);
+  if (SIGN > 0) w.y = -w.y;
+  return w;
+}
+
+template <int SIGN, class Sync>
+__device__ __forceinline__ void fft256(float2 (&a)[8], float2* S, const float2* tws, int l, Sync&& sync) {
+  const int m = l & 7, hi = l >> 3;  // hi in [0, 4)
+  dft8<SIGN>(a);
+#pragma unroll
+  for (int k = 1; k < 8; ++k) a[k] = cmul(a[k], w256s<SIGN>(tws, l * k));
+#pragma unroll
+  for (int k = 0; k < 8; ++k) S[k * kE256Ld1 + l] = a[k];
+  sync();
+  // pass 2: (m, t1 = hi), t = t1 + 4 t2
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = S[m * kE256Ld1 + hi + 4 * k];
+  dft8<SIGN>(a);
+#pragma unroll
+  for (int k = 1; k < 8; ++k) a[k] = cmul(a[k], w256s<SIGN>(tws, 8 * hi * k));
+  sync();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) S[(m * 4 + hi) * kE256Ld2 + k] = a[k];  // z[m][t1][j2]
+  sync();
+  // pass 3: (m, j2 = hi + 4 h), DFT4 over t1 -> X[m + 8 j2 + 64 j1] = X[l + 32 (h + 2 j1)]
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int j2 = hi + 4 * h;
+    float2 v0 = S[(m * 4 + 0) * kE256Ld2 + j2], v1 = S[(m * 4 + 1) * kE256Ld2 + j2];
+    float2 v2 = S[(m * 4 + 2) * kE256Ld2 + j2], v3 = S[(m * 4 + 3) * kE256Ld2 + j2];
+    dft4<SIGN>(v0, v1, v2, v3);
+    a[h] = v0;
+    a[h + 2] = v1;
+    a[h + 4] = v2;
+    a[h + 6] = v3;
+  }
+}
+
+// ePIE full-FFT stage rows for 256 x 256 windows: grid 64, block 128 (four
+// warps, one window row each; the group barrier is a warp barrier).
+template <int MODE>
+__global__ void __launch_bounds__(128) ke_rows256_epie(const float2* __restrict__ tw, float2* frame, long long ld,
+                                                       const long long* __restrict__ off, float2* probe,
+                                                       float2* X, float2* X2, float scale, float step, int fuse) {
+  __shared__ float2 tws[128];
+  __shared__ __align__(16) float2 sbuf[4][kE256Buf];
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) tws[i] = tw[i];
+  __syncthreads();
+  const int g = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int r = blockIdx.x * 4 + g;
+  float2* S = sbuf[g];
+  auto wsync = []() { __syncwarp(); };
+  float2* orow = frame + *off + (long long)r * ld;
+  float2* prow = probe + (size_t)r * 256;
+  float2 a[8];
+  if (MODE == E512_FWD) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = cmul(prow[l + 32 * k], orow[l + 32 * k]);
+    fft256<-1>(a, S, tws, l, wsync);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) X[(size_t)r * 256 + l + 32 * k] = a[k];
+    return;
+  }
+  const float2* xin = (MODE == E512_OBJ ? X : X2) + (size_t)r * 256;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = xin[l + 32 * k];
+  fft256<+1>(a, S, tws, l, wsync);
+  if (MODE == E512_OBJ) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c = l + 32 * k;
+      float2 proj = a[k];
+      proj.x *= scale;
+      proj.y *= scale;
+      const float2 pv = prow[c];
+      float2 o = orow[c];
+      const float2 resid = csub(cmul(pv, o), proj);
+      const float2 gr = cmulc(pv, resid);
+      o.x -= step * gr.x;
+      o.y -= step * gr.y;
+      orow[c] = o;
+      a[k] = cmul(pv, o);
+    }
+    if (fuse) {
+      __syncwarp();
+      fft256<-1>(a, S, tws, l, wsync);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) X2[(size_t)r * 256 + l + 32 * k] = a[k];
+    }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int c = l + 32 * k;
+    float2 proj = a[k];
+    proj.x *= scale;
+    proj.y *= scale;
+    float2 pv = prow[c];
+    const float2 o = orow[c];
+    const float2 resid = csub(cmul(pv, o), proj);
+    const float2 gr = cmulc(o, resid);
+    pv.x -= step * gr.x;
+    pv.y -= step * gr.y;
+    prow[c] = pv;
+  }
+}
+
+// Columns for 256 x 256: forward, projection, inverse, in place. grid 256 / NCOL, block 32 NCOL.
+template <int NCOL>
+__global__ void __launch_bounds__(32 * NCOL) ke_cols256_proj(float2* X, const float* __restrict__ d,
+                                                             const float2* __restrict__ tw) {
+  constexpr int CS = kE256Buf + 1;
+  __shared__ float2 tws[128];
+  __shared__ __align__(16) float2 sbuf[NCOL * CS];
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) tws[i] = tw[i];
+  const int c = threadIdx.x % NCOL, t = threadIdx.x / NCOL;
+  const int col = blockIdx.x * NCOL + c;
+  float2 a[8];
+  float dv[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    a[k] = X[(size_t)(t + 32 * k) * 256 + col];
+    dv[k] = d[(size_t)(t + 32 * k) * 256 + col];
+  }
+  __syncthreads();
+  float2* S = sbuf + c * CS;
+  auto bsync = []() { __syncthreads(); };
+  fft256<-1>(a, S, tws, t, bsync);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float mag = hypotf(a[k].x, a[k].y);
+    a[k] = mag > 0.f ? make_float2(dv[k] * (a[k].x / mag), dv[k] * (a[k].y / mag)) : make_float2(dv[k], 0.f);
+  }
+  __syncthreads();
+  fft256<+1>(a, S, tws, t, bsync);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) X[(size_t)(t + 32 * k) * 256 + col] = a[k];
+}
+
 // Rows: x[r][c] = probe[r][c] * frame[offs[f] + r * ld + c]; X[f][r][:] =
 // DFT_512 of the row, natural order. grid (512 / (4 * RPG), positions), block
 // 256 = four 64-thread groups, each transforming RPG rows.

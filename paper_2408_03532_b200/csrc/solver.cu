@@ -160,6 +160,11 @@ inline bool use_fft512(const pftg_solver& s) {
   static const bool off = std::getenv("PFTG_EPIE_LANEFFT") != nullptr;
   return !off && s.wr == 512 && s.wc == 512;
 }
+// The same for the per-position FFT stage of 256 x 256 windows (BASELINE configs[2]).
+inline bool use_fft256(const pftg_solver& s) {
+  static const bool off = std::getenv("PFTG_EPIE_LANEFFT") != nullptr;
+  return !off && s.wr == 256 && s.wc == 256;
+}
 
 template <class R>
 void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
@@ -228,6 +233,39 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
         ProfScope prof(st, K_FFT_ROWS);
         ke_rows512_epie<E512_PROBE><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, scale,
                                                          (float)s.cfg.gamma, 0);
+      }
+      PFTG_LAUNCH_CHECK();
+      return;
+    }
+    if (use_fft256(s)) {
+      const float2* tw = fft_twiddles<float>(256);
+      float2* fr = reinterpret_cast<float2*>(frame);
+      float2* pr = reinterpret_cast<float2*>(probe);
+      float2* X = static_cast<float2*>(s.X);
+      float2* X2 = static_cast<float2*>(s.X2);
+      const float* dn = static_cast<const float*>(s.d) + (long long)j * n;
+      const float scale = 1.0f / static_cast<float>(n);
+      {
+        ProfScope prof(st, K_FFT_ROWS);
+        ke_rows256_epie<E512_FWD><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, 1.f, 0.f, 0);
+      }
+      {
+        ProfScope prof(st, K_FFT_COLS);
+        ke_cols256_proj<4><<<64, 128, 0, st>>>(X, dn, tw);
+      }
+      {
+        ProfScope prof(st, K_FFT_ROWS);
+        ke_rows256_epie<E512_OBJ><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, scale,
+                                                      (float)s.cfg.beta, blind ? 1 : 0);
+      }
+      if (blind) {
+        {
+          ProfScope prof(st, K_FFT_COLS);
+          ke_cols256_proj<4><<<64, 128, 0, st>>>(X2, dn, tw);
+        }
+        ProfScope prof(st, K_FFT_ROWS);
+        ke_rows256_epie<E512_PROBE><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, scale,
+                                                        (float)s.cfg.gamma, 0);
       }
       PFTG_LAUNCH_CHECK();
       return;

@@ -193,7 +193,7 @@ def test_cfg3_full_problem_one_band_one_fft_sweep(ref):
 
 
 @pytest.mark.parametrize("w,dtype,pft", [(64, np.complex128, 1), (128, np.complex128, 0), (64, np.complex64, 1),
-                                         (512, np.complex64, 1)])
+                                         (256, np.complex64, 0), (512, np.complex64, 1)])
 def test_hybrid_solve_shuffled_matches_reference(ref, w, dtype, pft):
     """Shuffled visit order (the reference's mt19937_64 Fisher-Yates stream,
     solver.cpp:164-169) through the band and full-FFT stages, blind. w = 512
