@@ -339,8 +339,13 @@ __device__ __forceinline__ void cols_forward(const PftDev<R>& pl, ColsSmem<R>& s
 #pragma unroll
     for (int s = 0; s < S1; ++s) {
       const int u1 = bitrev(s * P1 + lig, pl.lp1);
-      band_contract<RB>(sm.W1s, M1, mod_nonneg(u1 + pl.mt1, pl.p1), pl.p1, r1, x[s],
-                        [&](int a, C v) { sm.Ys[(size_t)a * (nb + 1) + bb] = v; });
+      auto emit = [&](int a, C v) { sm.Ys[(size_t)a * (nb + 1) + bb] = v; };
+      if constexpr (sizeof(R) == 4) {
+        // complex64: Horner form of the band rows (band_horner, pft_fast.cuh); padded x[j >= r1] are 0
+        band_horner<RB>(sm.W1s, M1, mod_nonneg(u1 + pl.mt1, pl.p1), pl.p1, pl.mt1, R(1) / R(pl.p1), x[s], emit);
+      } else {
+        band_contract<RB>(sm.W1s, M1, mod_nonneg(u1 + pl.mt1, pl.p1), pl.p1, r1, x[s], emit);
+      }
     }
   }
 }
@@ -367,9 +372,14 @@ __device__ __forceinline__ void cols_adjoint(const PftDev<R>& pl, ColsSmem<R>& s
         const int u1 = s * P1 + lig;
         for (int a = mod_nonneg(u1 + pl.mt1, pl.p1); a < M1; a += pl.p1) {
           const C y = sm.Ys[(size_t)a * (nb + 1) + bb];
+          if constexpr (sizeof(R) == 4) {
+            // complex64: Horner-form D-dagger term (gather_horner); padded j >= r1 are never stored
+            gather_horner<RB>(x[s], sm.W1s[a], static_cast<R>(a - pl.mt1) * (R(1) / R(pl.p1)), y);
+          } else {
 #pragma unroll
-          for (int j = 0; j < RB; ++j)
-            if (j < r1) cmacc(x[s][j], __ldg(sm.W1s + j * M1 + a), y);
+            for (int j = 0; j < RB; ++j)
+              if (j < r1) cmacc(x[s][j], __ldg(sm.W1s + j * M1 + a), y);
+          }
         }
       }
     }
