@@ -395,6 +395,79 @@ __device__ __forceinline__ void cols_adjoint(const PftDev<R>& pl, ColsSmem<R>& s
   }
 }
 
+// Single-column strips (nb == 1: one ePIE position spread over >= 64 CTAs).
+// The column's r1 transforms are spread over the CTA's lane groups (one j1
+// per group, in place in Gs) instead of one lane group carrying all r1, and
+// the band rows / D-dagger gathers run one thread per row / per u1.
+template <class R, int S1, int RB>
+__device__ __forceinline__ void cols_forward_j1(const PftDev<R>& pl, ColsSmem<R>& sm) {
+  using C = typename CT<R>::C;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int P1 = pl.p1 < 32 ? pl.p1 : 32;
+  const int gpw = 32 / P1;
+  const int lig = lane & (P1 - 1), grp = warp * gpw + lane / P1, ngrp = nwarps * gpw;
+  const int ld = pl.p1 + 1, M1 = pl.M1, r1 = pl.r1;
+  for (int j = grp; j < r1; j += ngrp) {
+    C x[S1][1];
+#pragma unroll
+    for (int s = 0; s < S1; ++s) x[s][0] = sm.Gs[(size_t)j * ld + s * P1 + lig];
+    fft_dif<S1, 1>(x, pl.p1, P1, lig, sm.tw1s, -1);
+#pragma unroll
+    for (int s = 0; s < S1; ++s) sm.Gs[(size_t)j * ld + bitrev(s * P1 + lig, pl.lp1)] = x[s][0];  // X[j][u1]
+  }
+  __syncthreads();
+  for (int a = threadIdx.x; a < M1; a += blockDim.x) {
+    const int u1 = mod_nonneg(a - pl.mt1, pl.p1);
+    C acc = czero<C>();
+    if constexpr (sizeof(R) == 4) {
+      const R base = static_cast<R>(a - pl.mt1) * (R(1) / R(pl.p1));
+      acc = sm.Gs[(size_t)(r1 - 1) * ld + u1];
+      for (int j = r1 - 2; j >= 0; --j) acc = cfmar(acc, base, sm.Gs[(size_t)j * ld + u1]);
+      acc = cmul(sm.W1s[a], acc);
+    } else {
+      for (int j = 0; j < r1; ++j) cmac(acc, __ldg(sm.W1s + j * M1 + a), sm.Gs[(size_t)j * ld + u1]);
+    }
+    sm.Ys[(size_t)a * 2] = acc;  // Ys stride nb + 1 = 2
+  }
+}
+
+template <class R, int S1, int RB>
+__device__ __forceinline__ void cols_adjoint_j1(const PftDev<R>& pl, ColsSmem<R>& sm) {
+  using C = typename CT<R>::C;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int P1 = pl.p1 < 32 ? pl.p1 : 32;
+  const int gpw = 32 / P1;
+  const int lig = lane & (P1 - 1), grp = warp * gpw + lane / P1, ngrp = nwarps * gpw;
+  const int ld = pl.p1 + 1, M1 = pl.M1, r1 = pl.r1;
+  for (int u1 = threadIdx.x; u1 < pl.p1; u1 += blockDim.x) {
+    C x[RB];
+#pragma unroll
+    for (int j = 0; j < RB; ++j) x[j] = czero<C>();
+    for (int a = mod_nonneg(u1 + pl.mt1, pl.p1); a < M1; a += pl.p1) {
+      const C y = sm.Ys[(size_t)a * 2];
+      if constexpr (sizeof(R) == 4) {
+        gather_horner<RB>(x, sm.W1s[a], static_cast<R>(a - pl.mt1) * (R(1) / R(pl.p1)), y);
+      } else {
+#pragma unroll
+        for (int j = 0; j < RB; ++j)
+          if (j < r1) cmacc(x[j], __ldg(sm.W1s + j * M1 + a), y);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < RB; ++j)
+      if (j < r1) sm.Gs[(size_t)j * ld + u1] = x[j];
+  }
+  __syncthreads();
+  for (int j = grp; j < r1; j += ngrp) {
+    C x[S1][1];
+#pragma unroll
+    for (int s = 0; s < S1; ++s) x[s][0] = sm.Gs[(size_t)j * ld + s * P1 + lig];
+    fft_dif<S1, 1>(x, pl.p1, P1, lig, sm.tw1s, +1);
+#pragma unroll
+    for (int s = 0; s < S1; ++s) sm.Gs[(size_t)j * ld + bitrev(s * P1 + lig, pl.lp1)] = x[s][0];  // Gs[j][k1]
+  }
+}
+
 template <class R>
 __device__ __forceinline__ void cols_store_g(const PftDev<R>& pl, ColsSmem<R>& sm,
                                              typename CT<R>::C* Gf, int b0, int nb, int nbv) {
@@ -483,7 +556,8 @@ __global__ void __launch_bounds__(256, 3) k_fwd_cols(PftDev<R> pl, const typenam
   const C* Gf = G + (size_t)f * pl.p1 * pl.r1 * pl.M2;
   cols_load_g(pl, sm, Gf, b0, nb, nbv);
   __syncthreads();
-  cols_forward<R, S1, RB>(pl, sm, nb);
+  if (nb == 1) cols_forward_j1<R, S1, RB>(pl, sm);
+  else cols_forward<R, S1, RB>(pl, sm, nb);
   __syncthreads();
   if (band) {
     C* bf = band + (size_t)f * pl.M1 * pl.M2;
@@ -501,7 +575,8 @@ __global__ void __launch_bounds__(256, 3) k_fwd_cols(PftDev<R> pl, const typenam
   }
   project_strip(pl, sm, nb, nbv, dc, b0, true, nullptr);
   __syncthreads();
-  cols_adjoint<R, S1, RB>(pl, sm, nb);
+  if (nb == 1) cols_adjoint_j1<R, S1, RB>(pl, sm);
+  else cols_adjoint<R, S1, RB>(pl, sm, nb);
   __syncthreads();
   cols_store_g(pl, sm, Gout + (size_t)f * pl.p1 * pl.r1 * pl.M2, b0, nb, nbv);
 }
@@ -522,7 +597,8 @@ __global__ void __launch_bounds__(256, 3) k_adj_cols(PftDev<R> pl, const typenam
     sm.Ys[(size_t)a * (nb + 1) + bb] = bb < nbv ? bf[(size_t)a * pl.M2 + b0 + bb] : czero<C>();
   });
   __syncthreads();
-  cols_adjoint<R, S1, RB>(pl, sm, nb);
+  if (nb == 1) cols_adjoint_j1<R, S1, RB>(pl, sm);
+  else cols_adjoint<R, S1, RB>(pl, sm, nb);
   __syncthreads();
   cols_store_g(pl, sm, Gt + (size_t)f * pl.p1 * pl.r1 * pl.M2, b0, nb, nbv);
 }
