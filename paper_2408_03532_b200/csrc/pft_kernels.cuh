@@ -407,13 +407,18 @@ __device__ __forceinline__ void cols_forward_j1(const PftDev<R>& pl, ColsSmem<R>
   const int gpw = 32 / P1;
   const int lig = lane & (P1 - 1), grp = warp * gpw + lane / P1, ngrp = nwarps * gpw;
   const int ld = pl.p1 + 1, M1 = pl.M1, r1 = pl.r1;
-  for (int j = grp; j < r1; j += ngrp) {
+  // warp-uniform loop: the lane-group FFT shuffles over the full warp
+  for (int base = warp * gpw; base < r1; base += ngrp) {
+    const int j = base + (grp - warp * gpw);
+    const bool valid = j < r1;
     C x[S1][1];
 #pragma unroll
-    for (int s = 0; s < S1; ++s) x[s][0] = sm.Gs[(size_t)j * ld + s * P1 + lig];
+    for (int s = 0; s < S1; ++s) x[s][0] = valid ? sm.Gs[(size_t)j * ld + s * P1 + lig] : czero<C>();
     fft_dif<S1, 1>(x, pl.p1, P1, lig, sm.tw1s, -1);
+    if (valid) {
 #pragma unroll
-    for (int s = 0; s < S1; ++s) sm.Gs[(size_t)j * ld + bitrev(s * P1 + lig, pl.lp1)] = x[s][0];  // X[j][u1]
+      for (int s = 0; s < S1; ++s) sm.Gs[(size_t)j * ld + bitrev(s * P1 + lig, pl.lp1)] = x[s][0];  // X[j][u1]
+    }
   }
   __syncthreads();
   for (int a = threadIdx.x; a < M1; a += blockDim.x) {
@@ -458,13 +463,17 @@ __device__ __forceinline__ void cols_adjoint_j1(const PftDev<R>& pl, ColsSmem<R>
       if (j < r1) sm.Gs[(size_t)j * ld + u1] = x[j];
   }
   __syncthreads();
-  for (int j = grp; j < r1; j += ngrp) {
+  for (int base = warp * gpw; base < r1; base += ngrp) {  // warp-uniform (full-warp shuffles)
+    const int j = base + (grp - warp * gpw);
+    const bool valid = j < r1;
     C x[S1][1];
 #pragma unroll
-    for (int s = 0; s < S1; ++s) x[s][0] = sm.Gs[(size_t)j * ld + s * P1 + lig];
+    for (int s = 0; s < S1; ++s) x[s][0] = valid ? sm.Gs[(size_t)j * ld + s * P1 + lig] : czero<C>();
     fft_dif<S1, 1>(x, pl.p1, P1, lig, sm.tw1s, +1);
+    if (valid) {
 #pragma unroll
-    for (int s = 0; s < S1; ++s) sm.Gs[(size_t)j * ld + bitrev(s * P1 + lig, pl.lp1)] = x[s][0];  // Gs[j][k1]
+      for (int s = 0; s < S1; ++s) sm.Gs[(size_t)j * ld + bitrev(s * P1 + lig, pl.lp1)] = x[s][0];  // Gs[j][k1]
+    }
   }
 }
 
