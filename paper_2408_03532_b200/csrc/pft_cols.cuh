@@ -286,6 +286,7 @@ static_assert(32 * kFftWarps * (kColsRegFft - kColsRegLaunch) <= 32 * kBandWarps
               "register hand-over must balance");
 constexpr int kStripBufs = 2;  // strips in flight (G is L2-resident between the passes)
 constexpr int kBandLd = 10;    // staged band rows: 80-byte stride, 16-byte aligned, conflict-light
+constexpr int kAdjLdy = 10;    // adjoint cols band strip rows: 80-byte stride (16-byte cp.async targets)
 
 template <class R>
 __host__ __device__ inline size_t cols_fwd_local_smem(int r, int M1) {
@@ -435,74 +436,61 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
 template <class R>
 __host__ __device__ inline size_t cols_adj_local_smem(int r, int M1) {
   using C = typename CT<R>::C;
-  const size_t b = sizeof(C) * ((size_t)M1 * (kStripNB + 1) + (size_t)r * kStripNB * (kLocalP + 1) +
-                                (size_t)kLocalP * (r * kStripNB + 1) + kLocalP / 2);
+  const size_t b = sizeof(C) * (2 * (size_t)M1 * kAdjLdy + (size_t)r * kStripNB * (kLocalP + 1));
   return ((b + 15) & ~size_t(15)) + 128;
 }
 
+// 16-byte global -> shared asynchronous copy (LDGSTS), bypassing registers.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // Adjoint: gather over the band rows of each u1 (thread (u1, bb)), then one
-// thread per (j1, bb) runs the inverse 32-point FFT; Gt row-block layout.
+// thread per (j1, bb) runs the inverse 32-point FFT and stores its 32 values
+// straight to Gt (row-block layout; per k1 a warp writes 4 j1 x 64-byte
+// segments). The band strip of the next iteration streams into the other Ys
+// buffer with cp.async while this one is transformed (no register staging).
 template <class R, int RR>
 __global__ void __launch_bounds__(kColsThreads, 2)
     kc_adj_cols_local(PftDev<R> pl, const typename CT<R>::C* __restrict__ band, typename CT<R>::C* __restrict__ Gt,
                       int nstrips_field, int ntotal, int dbg) {
   using C = typename CT<R>::C;
   constexpr int P = kLocalP;
-  constexpr int LDY = kStripNB + 1;
+  constexpr int LDY = kAdjLdy;             // Ys[a][bb], 80-byte rows (16-byte aligned pairs)
   constexpr int NSEQ = RR * kStripNB;
   constexpr int LDS_ = P + 1;              // Xs[(j1, bb)][u]
-  constexpr int GREC = RR * kStripNB + 1;  // Gs[k1][j1 * 8 + bb]
-  constexpr int MAXIT = 4;  // band strip prefetch: M1 * 4 float4 over 256 threads (launcher: M1 <= 256)
-  // (3 CTAs per SM with shared-memory twiddles measured slower: 35.9 -> 41.4 us per 64 cfg2 fields)
   static_assert(sizeof(R) == 4, "lane-local cols pass: complex64");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int M1 = pl.M1, M2 = pl.M2, mt1 = pl.mt1;
-  C* Ys = reinterpret_cast<C*>(smem_raw);  // [M1][LDY]
-  C* Xs = Ys + (size_t)M1 * LDY;           // [NSEQ][LDS_]
-  C* Gs = Xs + (size_t)NSEQ * LDS_;        // [P][GREC]
+  C* Ys0 = reinterpret_cast<C*>(smem_raw);  // [2][M1][LDY]
+  C* Xs = Ys0 + 2 * (size_t)M1 * LDY;       // [NSEQ][LDS_]
   C w[P / 2];
 #pragma unroll
   for (int k = 0; k < P / 2; ++k) w[k] = pl.tw1[k];
-  const int items = M1 * (kStripNB / 2);
-  C pre[MAXIT][2];
-  auto prefetch = [&](int sg) {
+  const int items = M1 * (kStripNB / 2);  // 16-byte pairs per strip
+  auto fetch = [&](int sg, C* Ys) {
     const int f = sg / nstrips_field, b0 = (sg % nstrips_field) * kStripNB;
     const C* bf = band + (size_t)f * M1 * M2 + b0;
-#pragma unroll
-    for (int it = 0; it < MAXIT; ++it) {
-      const int e = threadIdx.x + it * kColsThreads;
-      if (e < items) {
-        const int aa = e / (kStripNB / 2), cc = (e % (kStripNB / 2)) * 2;
-        const float4 v = __ldg(reinterpret_cast<const float4*>(bf + (size_t)aa * M2 + cc));
-        pre[it][0] = CT<R>::mk(v.x, v.y);
-        pre[it][1] = CT<R>::mk(v.z, v.w);
-      }
+    for (int e = threadIdx.x; e < items; e += blockDim.x) {
+      const int aa = e / (kStripNB / 2), cc = (e % (kStripNB / 2)) * 2;
+      cp_async16(Ys + (size_t)aa * LDY + cc, bf + (size_t)aa * M2 + cc);
     }
-  };
-  auto park = [&]() {
-#pragma unroll
-    for (int it = 0; it < MAXIT; ++it) {
-      const int e = threadIdx.x + it * kColsThreads;
-      if (e < items) {
-        const int aa = e / (kStripNB / 2), cc = (e % (kStripNB / 2)) * 2;
-        Ys[(size_t)aa * LDY + cc] = pre[it][0];
-        Ys[(size_t)aa * LDY + cc + 1] = pre[it][1];
-      }
-    }
+    cp_async_commit();
   };
   griddep_launch_dependents();
   griddep_wait();  // PDL: the band is the previous kernel's output
-  if ((int)blockIdx.x < ntotal) {
-    prefetch(blockIdx.x);
-    park();
-  }
-  __syncthreads();
+  if ((int)blockIdx.x < ntotal) fetch(blockIdx.x, Ys0);
   const int t = threadIdx.x;
   const int gu = t >> 3, gbb = t & 7;  // gather thread (u1, bb), t < P * kStripNB
-  for (int sg = blockIdx.x; sg < ntotal; sg += gridDim.x) {
+  uint32_t i = 0;
+  for (int sg = blockIdx.x; sg < ntotal; sg += gridDim.x, ++i) {
     const int f = sg / nstrips_field, b0 = (sg % nstrips_field) * kStripNB;
-    const bool more = sg + (int)gridDim.x < ntotal;
-    if (more && !(dbg & 8)) prefetch(sg + gridDim.x);  // in flight during the transform below (dbg 8: off)
+    C* Ys = Ys0 + (size_t)(i & 1) * M1 * LDY;
+    cp_async_wait_all();
+    __syncthreads();  // Ys[i & 1] landed for every thread; Xs free (previous FFT done)
+    if (sg + (int)gridDim.x < ntotal && !(dbg & 8)) fetch(sg + gridDim.x, Ys0 + (size_t)((i + 1) & 1) * M1 * LDY);
     if (t < P * kStripNB && !(dbg & 1)) {  // dbg 1: profiling switch, no gather
       C x[RR];
 #pragma unroll
@@ -512,29 +500,25 @@ __global__ void __launch_bounds__(kColsThreads, 2)
 #pragma unroll
       for (int j = 0; j < RR; ++j) Xs[(size_t)(j * kStripNB + gbb) * LDS_ + gu] = x[j];
     }
-    __syncthreads();  // Ys consumed, Xs complete
-    if (more && !(dbg & 8)) park();  // before the FFT: the prefetch registers are free for the transform
+    __syncthreads();  // Xs complete
     if (t < NSEQ && !(dbg & 2)) {  // dbg 2: no FFT
       C x[P];
 #pragma unroll
       for (int uu = 0; uu < P; ++uu) x[uu] = Xs[(size_t)t * LDS_ + uu];
       fft_dif_local<P>(x, w, +1);
+      // sequence t = (j1, bb): Gt[f][k1][j1][b0 + bb]
+      C* gcol = Gt + (size_t)f * P * RR * M2 + (size_t)(t / kStripNB) * M2 + b0 + (t % kStripNB);
+      if (!(dbg & 4)) {  // dbg 4: no stores
 #pragma unroll
-      for (int pos = 0; pos < P; ++pos) {
-        constexpr int LP = 5;
-        Gs[(size_t)((__brev((unsigned)pos) >> (32 - LP)) & (P - 1)) * GREC + t] = x[pos];
+        for (int pos = 0; pos < P; ++pos) {
+          constexpr int LP = 5;
+          const int k1 = (__brev((unsigned)pos) >> (32 - LP)) & (P - 1);
+          gcol[(size_t)k1 * RR * M2] = x[pos];
+        }
       }
     }
-    __syncthreads();  // Gs complete, Ys refilled
-    C* gf = Gt + (size_t)f * P * RR * M2 + b0;
-    for (int e = threadIdx.x; e < ((dbg & 4) ? 0 : P * RR * (kStripNB / 2)); e += blockDim.x) {  // dbg 4: no stores
-      const int kj = e / (kStripNB / 2), cc = (e % (kStripNB / 2)) * 2;
-      const int k1 = kj / RR, j = kj % RR;
-      const C v0 = Gs[(size_t)k1 * GREC + j * kStripNB + cc], v1 = Gs[(size_t)k1 * GREC + j * kStripNB + cc + 1];
-      *reinterpret_cast<float4*>(gf + (size_t)kj * M2 + cc) = make_float4(v0.x, v0.y, v1.x, v1.y);
-    }
-    __syncthreads();  // Gs drained
   }
+  cp_async_wait_all();
 }
 
 }  // namespace pftg
