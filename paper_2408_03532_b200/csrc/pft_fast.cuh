@@ -262,9 +262,10 @@ __device__ __forceinline__ void expand_pairs_sm(const R* __restrict__ btab, cons
 
 // Strip-major layout of the rows -> cols intermediate used by the persistent
 // cols pass (pft_cols.cuh): G[f][b / kStripNB][k1][j1 * kStripNB + b % kStripNB],
-// each (strip, k1) record padded by one element (conflict-free k1-strided reads).
+// each (strip, k1) record padded by two elements: records start on 16-byte
+// boundaries, so the forward rows pass stores them with 1-D bulk copies.
 constexpr int kStripNB = 8;
-__host__ __device__ constexpr int strip_rec(int r) { return r * kStripNB + 1; }
+__host__ __device__ constexpr int strip_rec(int r) { return r * kStripNB + 2; }
 
 // Stage B (+ FFT over k2 + axis-2 band) from T in shared memory, pairing over l2.
 // Output: Gblk[j1][b] (row-block layout) or, when gstrip != nullptr, the

@@ -322,6 +322,8 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P>(RA > 0), 1)
           }
         }
       }
+      // the previous tile's G records (bulk stores below) have left the staging block
+      if (HORNER && gstride > 0 && threadIdx.x == AT) bulk_wait_read();
       named_sync(2, BT);  // group B is done reading T: group A may overwrite it
       if (threadIdx.x == AT) mbar_arrive(tfree);
       if (dbg & 8) {  // profiling experiment: stage B only
@@ -349,18 +351,17 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P>(RA > 0), 1)
         const int tb = threadIdx.x - AT;
         constexpr int NREC = RR * kStripNB;
         const int nrec = M2 / kStripNB;
+        if (dbg & 32) continue;  // profiling experiment: band staged, no G stores
         if (gstride > 0) {
-          C* gstrip = G + (size_t)f * gstride + (size_t)k1 * REC;
-          if constexpr (BT % NREC == 0) {  // fixed record offset w per thread: no index division
-            constexpr int RSTEP = BT / NREC;
-            const int w = tb % NREC;
+          // one 1-D bulk store per (strip, k1) record (16-byte aligned: strip_rec); the
+          // staging block is reused after bulk_wait_read() at the next tile's stage B
+          if (threadIdx.x == AT) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            C* gstrip = G + (size_t)f * gstride + (size_t)k1 * REC;
             const size_t gstep = (size_t)pl.p1 * REC;
-            for (int rr = tb / NREC; rr < nrec; rr += RSTEP) gstrip[rr * gstep + w] = Gst[rr * REC + w];
-          } else {
-            for (int e = tb; e < nrec * NREC; e += BT) {
-              const int rr = e / NREC, w = e - rr * NREC;
-              gstrip[(size_t)rr * pl.p1 * REC + w] = Gst[(size_t)rr * REC + w];
-            }
+            for (int rr = 0; rr < nrec; ++rr)
+              bulk_s2g(gstrip + rr * gstep, Gst + (size_t)rr * REC, (uint32_t)(NREC * sizeof(C)));
+            bulk_commit();
           }
         } else {
           C* Gblk = G + ((size_t)f * pl.p1 + k1) * RR * M2;
@@ -387,6 +388,7 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P>(RA > 0), 1)
         }
       }
     }
+    if (HORNER && gstride > 0 && threadIdx.x == AT) bulk_wait_all();  // G records written before exit
     return;
   }
 
