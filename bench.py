@@ -53,6 +53,10 @@ WORKLOADS = {
 }
 
 
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4
+FLOPS_PER_POSITION_CFG5 = 46.4e6 + 23.6e6  # factored PFT band (r = 9) + 5 n log2 n FFT
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -497,6 +501,7 @@ def run_evaluator(args):
     pb, pe = shard_range(npos, rank, world)
     alg = (pe - pb) * (w * w * 8 + w * w * 4 + (2 * mt) ** 2 * 4) * args.steps
     achieved_step = alg / (ms / 1e3) / 1e9
+    flops_step = (pe - pb) * FLOPS_PER_POSITION_CFG5
     if rank == 0:
         line = {
             "metric": "evaluator_positions_per_sec", "value": value, "unit": "positions/s", "n_gpus": world,
@@ -510,6 +515,13 @@ def run_evaluator(args):
                          "achieved": achieved_step, "peak": hbm, "unit": "GB/s", "frac": achieved_step / hbm,
                          "traffic": None, "peak_kind": peak_kind, "dominant_kernel": kname,
                          "kernel_ms": prof.ms},
+            # this workload is compute-bound on the CUDA cores
+            # (PFT band r = 9 at 46.4 MFLOP + 512^2 FFT at 23.6 MFLOP per position)
+            "flop_roofline": {"bound": "fp32", "achieved": flops_step / (ms / args.steps / 1e3) / 1e12,
+                              "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                              "frac": flops_step / (ms / args.steps / 1e3) / 1e12 / FP32_PEAK_TFLOPS,
+                              "flops_per_position": FLOPS_PER_POSITION_CFG5,
+                              "peak_kind": "nominal: 148 SMs x 128 FP32 lanes x 2 FLOP x 1965 MHz"},
             "gpu_launches": sum(prof.launches.values()), "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
