@@ -313,7 +313,7 @@ double objective(pftg_solver& s) {
         const float2* tw = fft_twiddles<float>(512);
         {
           ProfScope prof(s.st, K_FFT_ROWS);
-          ke_rows512<8><<<dim3(16, nb), 256, 0, s.st>>>(static_cast<const float2*>(s.frame), (long long)s.fc,
+          ke_rows512<4><<<dim3(32, nb), 256, 0, s.st>>>(static_cast<const float2*>(s.frame), (long long)s.fc,
                                                          s.doffs + c0, static_cast<const float2*>(s.probe), tw,
                                                          static_cast<float2*>(s.Xe));
         }
