@@ -50,9 +50,14 @@ __global__ void __launch_bounds__(kColsThreads, 2)
   uint64_t* full = smem_after<uint64_t>(smem_raw, tw1s + P / 2 + 1, 16);
   const uint32_t strip_bytes = (uint32_t)(sbytes_e * sizeof(C));
   for (int i = threadIdx.x; i < P / 2; i += blockDim.x) tw1s[i] = pl.tw1[i];
-  auto strip_src = [&](int sg) {
+  // strip sg = (field, st): record k1 of the strip sits at G[f][k1][st] (tile-major
+  // layout written by the rows pass); P record copies land as buf[k1][REC]
+  auto load_strip = [&](int sg, C* dst, uint64_t* bar) {
     const int f = sg / nstrips_field, st = sg % nstrips_field;
-    return G + (size_t)f * gstride + (size_t)st * sbytes_e;
+    const C* src = G + (size_t)f * gstride + (size_t)st * REC;
+    mbar_arrive_expect_tx(bar, strip_bytes);
+    for (int k1 = 0; k1 < P; ++k1)
+      bulk_g2s(dst + (size_t)k1 * REC, src + (size_t)k1 * nstrips_field * REC, (uint32_t)(REC * sizeof(C)), bar);
   };
   if (threadIdx.x == 0) {
     mbar_init(&full[0], 1);
@@ -61,8 +66,7 @@ __global__ void __launch_bounds__(kColsThreads, 2)
     for (int s = 0; s < 2; ++s) {
       const int sg = blockIdx.x + s * gridDim.x;
       if (sg < ntotal) {
-        mbar_arrive_expect_tx(&full[s], strip_bytes);
-        bulk_g2s(buf + (size_t)s * sbytes_e, strip_src(sg), strip_bytes, &full[s]);
+        load_strip(sg, buf + (size_t)s * sbytes_e, &full[s]);
       }
     }
   }
@@ -96,8 +100,7 @@ __global__ void __launch_bounds__(kColsThreads, 2)
     __syncthreads();  // strip buffer s consumed, Ys complete
     if (threadIdx.x == 0 && sg + 2 * (int)gridDim.x < ntotal) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect_tx(&full[s], strip_bytes);
-      bulk_g2s(buf + (size_t)s * sbytes_e, strip_src(sg + 2 * gridDim.x), strip_bytes, &full[s]);
+      load_strip(sg + 2 * gridDim.x, buf + (size_t)s * sbytes_e, &full[s]);
     }
     // band rows a, columns b0 .. b0+7: 4 threads x 2 columns per row (64-byte segments)
     C* bf = band + (size_t)f * M1 * M2 + b0;
@@ -321,9 +324,14 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
   uint64_t* xready = bars + kStripBufs;  // FFT -> band warps
   uint64_t* xfree = xready + 2;          // band -> FFT warps
   const uint32_t strip_bytes = (uint32_t)(sbytes_e * sizeof(C));
-  auto strip_src = [&](int sg) {
+  // strip sg = (field, st): record k1 of the strip sits at G[f][k1][st] (tile-major
+  // layout written by the rows pass); P record copies land as buf[k1][REC]
+  auto load_strip = [&](int sg, C* dst, uint64_t* bar) {
     const int f = sg / nstrips_field, st = sg % nstrips_field;
-    return G + (size_t)f * gstride + (size_t)st * sbytes_e;
+    const C* src = G + (size_t)f * gstride + (size_t)st * REC;
+    mbar_arrive_expect_tx(bar, strip_bytes);
+    for (int k1 = 0; k1 < P; ++k1)
+      bulk_g2s(dst + (size_t)k1 * REC, src + (size_t)k1 * nstrips_field * REC, (uint32_t)(REC * sizeof(C)), bar);
   };
   griddep_launch_dependents();
   griddep_wait();  // PDL: G is the previous kernel's output
@@ -337,8 +345,7 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
     for (int s = 0; s < kStripBufs; ++s) {
       const int sg = blockIdx.x + s * gridDim.x;
       if (sg < ntotal) {
-        mbar_arrive_expect_tx(&full[s], strip_bytes);
-        bulk_g2s(buf + (size_t)s * sbytes_e, strip_src(sg), strip_bytes, &full[s]);
+        load_strip(sg, buf + (size_t)s * sbytes_e, &full[s]);
       }
     }
   }
@@ -372,8 +379,7 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
         mbar_arrive(&xready[s]);
         if (!(dbg & 4) && sg + kStripBufs * (int)gridDim.x < ntotal) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive_expect_tx(&full[sbi], strip_bytes);
-          bulk_g2s(buf + (size_t)sbi * sbytes_e, strip_src(sg + kStripBufs * gridDim.x), strip_bytes, &full[sbi]);
+          load_strip(sg + kStripBufs * gridDim.x, buf + (size_t)sbi * sbytes_e, &full[sbi]);
         }
       }
     }

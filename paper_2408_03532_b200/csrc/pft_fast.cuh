@@ -260,10 +260,11 @@ __device__ __forceinline__ void expand_pairs_sm(const R* __restrict__ btab, cons
   }
 }
 
-// Strip-major layout of the rows -> cols intermediate used by the persistent
-// cols pass (pft_cols.cuh): G[f][b / kStripNB][k1][j1 * kStripNB + b % kStripNB],
-// each (strip, k1) record padded by two elements: records start on 16-byte
-// boundaries, so the forward rows pass stores them with 1-D bulk copies.
+// Tile-major record layout of the rows -> cols intermediate used by the
+// persistent cols pass (pft_cols.cuh): G[f][k1][b / kStripNB][j1 * kStripNB + b % kStripNB],
+// each (k1, strip) record padded by two elements (16-byte aligned records):
+// a rows tile (f, k1) writes its records as one contiguous bulk store, a cols
+// strip gathers its p1 records with p1 bulk loads.
 constexpr int kStripNB = 8;
 __host__ __device__ constexpr int strip_rec(int r) { return r * kStripNB + 2; }
 
@@ -319,7 +320,7 @@ __device__ __forceinline__ void fast_stage_b_to_g(const PftDev<R>& pl, const BPa
       if (gstrip) {
         constexpr int REC = strip_rec(RR);
         band_contract<RR>(W2s, M2, (u2 + mt2) & (P - 1), P, RR, x[s], [&](int b, C v) {
-          gstrip[((size_t)(b / kStripNB) * pl.p1 + k1) * REC + j1 * kStripNB + (b % kStripNB)] = v;
+          gstrip[((size_t)k1 * (M2 / kStripNB) + b / kStripNB) * REC + j1 * kStripNB + (b % kStripNB)] = v;
         });
       } else {
         band_contract<RR>(W2s, M2, (u2 + mt2) & (P - 1), P, RR, x[s],

@@ -357,10 +357,8 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P>(RA > 0), 1)
           // staging block is reused after bulk_wait_read() at the next tile's stage B
           if (threadIdx.x == AT) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            C* gstrip = G + (size_t)f * gstride + (size_t)k1 * REC;
-            const size_t gstep = (size_t)pl.p1 * REC;
-            for (int rr = 0; rr < nrec; ++rr)
-              bulk_s2g(gstrip + rr * gstep, Gst + (size_t)rr * REC, (uint32_t)(NREC * sizeof(C)));
+            // tile-major layout G[f][k1][strip][REC]: the tile's records are one contiguous block
+            bulk_s2g(G + (size_t)f * gstride + (size_t)k1 * nrec * REC, Gst, (uint32_t)(nrec * REC * sizeof(C)));
             bulk_commit();
           }
         } else {
@@ -378,7 +376,7 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P>(RA > 0), 1)
           if (gstride > 0) {
             C* gstrip = G + (size_t)f * gstride;
             band_contract<RR>(W2s, M2, (u2 + mt2) & (P - 1), P, RR, x[ss], [&](int b, C v) {
-              gstrip[((size_t)(b / kStripNB) * pl.p1 + k1) * REC + j1 * kStripNB + (b % kStripNB)] = v;
+              gstrip[((size_t)k1 * (M2 / kStripNB) + b / kStripNB) * REC + j1 * kStripNB + (b % kStripNB)] = v;
             });
           } else {
             C* Gblk = G + ((size_t)f * pl.p1 + k1) * RR * M2;
