@@ -66,12 +66,12 @@ def peaks():
 
 
 # ncu --set full capture of the dominant kernel committed under profiles/
-# (tools/profile_r2.sh r3: the first launch of each cfg2 kernel in tools/prof_pft.py,
+# (tools/profile_r2.sh r5: the first launch of each cfg2 kernel in tools/prof_pft.py,
 # 64 fields per launch). Returns DRAM bytes (read + write) per field, or None.
-PROFILE_CAPTURES = {"pft_rows_fwd": ("profiles/r3_kt2_fwd_rows_raw.csv", 64),
-                    "pft_rows_adj": ("profiles/r3_kt_adj_rows_raw.csv", 64),
-                    "pft_cols_fwd": ("profiles/r3_kc_fwd_cols_local_raw.csv", 64),
-                    "pft_cols_adj": ("profiles/r3_kc_adj_cols_local_raw.csv", 64)}
+PROFILE_CAPTURES = {"pft_rows_fwd": ("profiles/r5_kt2_fwd_rows_raw.csv", 64),
+                    "pft_rows_adj": ("profiles/r5_kt_adj_rows_raw.csv", 64),
+                    "pft_cols_fwd": ("profiles/r5_kc_fwd_cols_local_raw.csv", 64),
+                    "pft_cols_adj": ("profiles/r5_kc_adj_cols_local_raw.csv", 64)}
 
 
 def captured_traffic_per_field(kname):
@@ -345,7 +345,7 @@ def run_ours(args):
                          "traffic": (None if captured_traffic_per_field(kname) is None
                                      else captured_traffic_per_field(kname) * fields_per_launch),
                          "traffic_source": "ncu --set full DRAM read+write of the committed capture "
-                                           "(profiles/r3_*_raw.csv), per field x fields per launch; "
+                                           "(profiles/r5_*_raw.csv), per field x fields per launch; "
                                            "algorithmic bytes per launch = %.4g" % (kbytes * fields_per_launch),
                          "peak_kind": peak_kind, "kernel_avg_ms": k_avg_ms,
                          "kernel_ms": prof.ms, "kernel_launches": prof.count,
