@@ -306,13 +306,13 @@ bool tma_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, c
       constexpr int P2T = 256, NT = adj_rows_threads<RR, P, P2T>(true);
       constexpr int L = (65536 / NT) & ~7, RB = L < 72 ? L : 72;
       constexpr int RA0 = L + (((NT - P2T) * (L - RB) / P2T) & ~7), RA = RA0 > 248 ? 248 : RA0;
-      if (pd.n2 == P2T * 4 && !dbg && !std::getenv("PFTG_NO_WIDE")) {
+      if (pd.n2 == P2T * 4 && (!dbg || std::getenv("PFTG_DEBUG_WIDE_ADJ")) && !std::getenv("PFTG_NO_WIDE")) {
         auto k = kt_adj_rows<R_, Q, RR, P, 4, P2T, RA, RB>;
         cudaFuncAttributes fa{};
         PFTG_CUDA(cudaFuncGetAttributes(&fa, k));
         if (fa.numRegs >= RB && fa.numRegs <= RA && P2T * (RA - fa.numRegs) <= (NT - P2T) * (fa.numRegs - RB)) {
           allow_smem(k);
-          launch_pdl(k, grid, NT, smem, st, pd, bp, Gt, out, ntiles, 0);
+          launch_pdl(k, grid, NT, smem, st, pd, bp, Gt, out, ntiles, dbg);
           launched = true;
           return;
         }
