@@ -59,6 +59,8 @@ __global__ void __launch_bounds__(kColsThreads, 2)
     for (int k1 = 0; k1 < P; ++k1)
       bulk_g2s(dst + (size_t)k1 * REC, src + (size_t)k1 * nstrips_field * REC, (uint32_t)(REC * sizeof(C)), bar);
   };
+  griddep_launch_dependents();
+  griddep_wait();  // PDL: G is the previous kernel's output
   if (threadIdx.x == 0) {
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);

@@ -26,6 +26,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace pftg {
 
@@ -601,6 +602,8 @@ __global__ void __launch_bounds__(256, 3) k_adj_cols(PftDev<R> pl, const typenam
   const int f = blockIdx.y, b0 = blockIdx.x * nb;
   const int nbv = min(nb, pl.M2 - b0);
   cols_load_tables(pl, sm);
+  griddep_launch_dependents();
+  griddep_wait();  // PDL (API path): the band is the previous kernel's output
   const C* bf = band + (size_t)f * pl.M1 * pl.M2;
   strip_for(pl.M1, nb, [&](int a, int bb) {
     sm.Ys[(size_t)a * (nb + 1) + bb] = bb < nbv ? bf[(size_t)a * pl.M2 + b0 + bb] : czero<C>();

@@ -70,6 +70,9 @@ void allow_smem(K kernel) {
 template <class... KA, class... A>
 void launch_pdl(void (*kernel)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
   static const bool off = std::getenv("PFTG_NO_PDL") != nullptr;
+  // not inside stream capture: the per-position ePIE graphs measured slower with programmatic edges
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  const bool capturing = cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -77,7 +80,7 @@ void launch_pdl(void (*kernel)(KA...), dim3 grid, dim3 block, size_t smem, cudaS
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  at[0].val.programmaticStreamSerializationAllowed = (off || capturing) ? 0 : 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   PFTG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...));
@@ -250,13 +253,13 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
       auto k = kt2_fwd_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
       if (vc == 2) {
         allow_smem(k);
-        k<<<grid, NT, smem2, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride, dbg2, src.offs,
-                                   src.probe);
+        launch_pdl(k, grid, NT, smem2, st, pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride, dbg2,
+                   src.offs, src.probe);
       } else {
         auto k1 = kt2_fwd_rows<R_, Q, RR, P, 1>;
         allow_smem(k1);
-        k1<<<grid, NT, smem2, st>>>(pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride, dbg2, src.offs,
-                                    src.probe);
+        launch_pdl(k1, grid, NT, smem2, st, pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride, dbg2,
+                   src.offs, src.probe);
       }
       launched = true;
       return;
@@ -321,7 +324,7 @@ bool tma_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, c
     constexpr int NT = 32 * (adj_p1_warps<RR, P>() + kAdjP2Warps);
     auto k = kt_adj_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
     allow_smem(k);
-    k<<<grid, NT, smem, st>>>(pd, bp, Gt, out, ntiles, dbg);
+    launch_pdl(k, grid, NT, smem, st, pd, bp, Gt, out, ntiles, dbg);
     launched = true;
   });
   return matched && launched;
@@ -429,7 +432,7 @@ void launch_fwd_cols<R_>(const PftDev<R_>& pd, int mode, const typename CT<R_>::
       const size_t smem = cols_fwd_smem<R_>(P, RR, pd.M1);
       auto k = kc_fwd_cols<R_, RR, P>;
       allow_smem(k);
-      k<<<grid, kColsThreads, smem, st>>>(pd, G, strip_field_elems(pd), band, nsf, total);
+      launch_pdl(k, grid, kColsThreads, smem, st, pd, G, (long long)strip_field_elems(pd), band, nsf, total);
     });
     if (!ok) throw std::logic_error("pftg: strip-major G for an unspecialized plan");
     PFTG_LAUNCH_CHECK();
@@ -490,7 +493,7 @@ void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, t
       const size_t smem = cols_adj_smem<R_>(P, RR, pd.M1);
       auto k = kc_adj_cols<R_, RR, P>;
       allow_smem(k);
-      k<<<grid, kColsThreads, smem, st>>>(pd, band, Gt, nsf, total);
+      launch_pdl(k, grid, kColsThreads, smem, st, pd, band, Gt, nsf, total);
     });
     PFTG_LAUNCH_CHECK();
     return;
@@ -503,7 +506,7 @@ void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, t
     auto k = k_adj_cols<R_, decltype(s)::value, decltype(rb)::value>;
     static bool once = (allow_smem(k), true);
     (void)once;
-    k<<<dim3(cols_strips(pl), batch), 256, smem, st>>>(pl, band, Gt);
+    launch_pdl(k, dim3(cols_strips(pl), batch), 256, smem, st, pl, band, Gt);
   });
   PFTG_LAUNCH_CHECK();
 }
