@@ -388,45 +388,28 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
     return;
   }
   // ---------------- band warps ----------------
+  // thread (u1, column) = (tb / 8, tb % 8): reads its r1 spectrum values once and
+  // evaluates the M1 / p1 band rows a = u1 + mt1 (mod p1) of that column by
+  // Horner (one shared-memory read per value instead of one per (row, value))
+  static_assert(BT == P * kStripNB, "one band thread per (u1, column)");
   const int tb = t - FT;
-  const int a0 = tb, a1 = tb + BT;
-  const bool v0 = a0 < M1, v1 = a1 < M1;
-  // Horner band (band_horner): W1[j][a] = tw(a) base_a^j
-  const C tw0 = v0 ? __ldg(pl.W1t + a0) : czero<C>(), tw1 = v1 ? __ldg(pl.W1t + a1) : czero<C>();
-  const R base0 = static_cast<R>(a0 - mt1) * (R(1) / R(P)), base1 = static_cast<R>(a1 - mt1) * (R(1) / R(P));
-  const int ua = (a0 - mt1) & (P - 1);  // == (a1 - mt1) & (P - 1): BT is a multiple of P
+  const int ub = tb / kStripNB, bbt = tb % kStripNB;
   uint32_t i = 0;
   for (int sg = blockIdx.x; sg < ntotal; sg += gridDim.x, ++i) {
     const int s = i & 1;
     const int f = sg / nstrips_field, b0 = (sg % nstrips_field) * kStripNB;
-    const C* xr = Xs + (size_t)s * P * LDX + (size_t)ua * LDX;
     mbar_wait(&xready[s], (i >> 1) & 1);
-    if (v0 && !(dbg & 2)) {
-      // band rows a0, a1, columns b0 .. b0+7: sum_j W1[j][a] X_j[u1] (band_contract order)
-      C out0[kStripNB], out1[kStripNB];
+    if (!(dbg & 2)) {
+      const C* xr = Xs + (size_t)s * P * LDX + (size_t)ub * LDX;
+      C xv[RR];
 #pragma unroll
-      for (int bb = 0; bb < kStripNB; ++bb) {
-        C acc0 = xr[(RR - 1) * kStripNB + bb], acc1 = acc0;
+      for (int j = 0; j < RR; ++j) xv[j] = xr[j * kStripNB + bbt];
+      for (int a = (ub + mt1) & (P - 1); a < M1; a += P) {
+        const R base = static_cast<R>(a - mt1) * (R(1) / R(P));
+        C acc = xv[RR - 1];
 #pragma unroll
-        for (int j = RR - 2; j >= 0; --j) {
-          const C xv = xr[j * kStripNB + bb];
-          acc0 = cfmar(acc0, base0, xv);
-          acc1 = cfmar(acc1, base1, xv);
-        }
-        out0[bb] = cmul(tw0, acc0);
-        out1[bb] = cmul(tw1, acc1);
-      }
-      // stage the rows in shared memory: the strip's 8 columns are 64 contiguous
-      // bytes per band row, stored below as 4 rows x 64 B per 16 lanes (whole sectors)
-#pragma unroll
-      for (int bb = 0; bb < kStripNB; bb += 2)
-        *reinterpret_cast<float4*>(Bs + (size_t)a0 * kBandLd + bb) =
-            make_float4(out0[bb].x, out0[bb].y, out0[bb + 1].x, out0[bb + 1].y);
-      if (v1) {
-#pragma unroll
-        for (int bb = 0; bb < kStripNB; bb += 2)
-          *reinterpret_cast<float4*>(Bs + (size_t)a1 * kBandLd + bb) =
-              make_float4(out1[bb].x, out1[bb].y, out1[bb + 1].x, out1[bb + 1].y);
+        for (int j = RR - 2; j >= 0; --j) acc = cfmar(acc, base, xv[j]);
+        Bs[(size_t)a * kBandLd + bbt] = cmul(__ldg(pl.W1t + a), acc);
       }
     }
     named_sync(2, BT);  // X[s] fully read, Bs complete
