@@ -247,6 +247,23 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
         }
       }
     }
+    if constexpr (sizeof(R_) == 4 && P == 64) {
+      // q = 8 plans (p2 = 64, n2 = 512): two group-B warps per j1 (slot split); group A
+      // becomes 256 threads x 2 columns so the block stays within 1024 threads
+      constexpr int AT = 256, NT = fwd_rows_threads<AT, RR, P, 2>(false);
+      const size_t smem2 = tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, wp);
+      if (pd.n2 == 2 * AT && NT <= 1024 && !dbg && !std::getenv("PFTG_NO_WS") && !std::getenv("PFTG_NO_SPLIT") &&
+          smem2 <= 227 * 1024) {
+        auto k = kt2_fwd_rows<R_, Q, RR, P, 2, AT, 0, 0, 2>;
+        {
+          allow_smem(k);
+          launch_pdl(k, grid, NT, smem2, st, pd, bp, src.base, src.ld, src.bstride, ntiles, ns2, G, gstride, dbg2,
+                     src.offs, src.probe);
+          launched = true;
+          return;
+        }
+      }
+    }
     if (!dbg && !std::getenv("PFTG_NO_WS") && tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, wp) <= 227 * 1024) {
       const size_t smem2 = tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, wp);
       constexpr int NT = kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32;

@@ -184,21 +184,28 @@ __host__ __device__ inline size_t tma2_rows_smem(int n2, int q, int r, int M2, i
 // the warpgroups hand registers over with setmaxnreg: group A grows to RA, the
 // group-B + producer warpgroups shrink to RB (the block is padded to whole
 // warpgroups). RA = 0: no register redistribution.
-template <int AT, int RR, int P>
+// SPL = 2 (p2 = 64, two slots per lane): two group-B warps per j1, each
+// keeping one half of the 64-point transform after its first (in-thread)
+// stage -- halves the per-tile FFT + band chain of the q = 8 plans (scan
+// windows of the ePIE band stage and the evaluator). The register hand-over
+// then runs the other way: group A (one column per thread) shrinks to RA,
+// group B grows to RB.
+template <int AT, int RR, int P, int SPL = 1>
 constexpr int fwd_rows_threads(bool wg_aligned) {
-  const int n = AT + 32 * fwd_b_warps<RR, P>() + 32;
+  const int n = AT + 32 * fwd_b_warps<RR, P>() * SPL + 32;
   return wg_aligned ? (n + 127) / 128 * 128 : n;
 }
 
-template <class R, int Q, int RR, int P, int VC, int AT = kTmaConsumers, int RA = 0, int RB = 0>
-__global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P>(RA > 0), 1)
+template <class R, int Q, int RR, int P, int VC, int AT = kTmaConsumers, int RA = 0, int RB = 0, int SPL = 1>
+__global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P, SPL>(RA > 0), 1)
     kt2_fwd_rows(PftDev<R> pl, BPar<R, Q, RR> bp, const typename CT<R>::C* __restrict__ z, long long ld,
                  long long bstride, int ntiles, int NS, typename CT<R>::C* __restrict__ G, long long gstride,
                  int dbg, const long long* __restrict__ offs, const typename CT<R>::C* __restrict__ probe) {
   using C = typename CT<R>::C;
-  constexpr int NBW = fwd_b_warps<RR, P>();
+  constexpr int NBW = fwd_b_warps<RR, P>() * SPL;
   constexpr int BT = 32 * NBW;
   static_assert(VC != 4 || sizeof(R) == 4, "VC = 4: complex64 only");
+  static_assert(SPL == 1 || (SPL == 2 && P == 64 && sizeof(R) == 4), "slot split: complex64, p2 = 64 only");
   static_assert(RA == 0 || AT % 128 == 0, "setmaxnreg needs warpgroup-aligned roles");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int n2 = pl.n2;
@@ -240,9 +247,12 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P>(RA > 0), 1)
   griddep_wait();  // PDL: the previous kernel's writes (and reads of our outputs) are complete
   const uint32_t row_bytes = (uint32_t)(n2 * sizeof(C));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if constexpr (RA > 0) {
+  if constexpr (RA > 0 && RA >= RB) {
     if (threadIdx.x < AT) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RA));
     else asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RB));
+  } else if constexpr (RA > 0) {
+    if (threadIdx.x < AT) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RA));
+    else asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RB));
   }
 
   if (threadIdx.x >= AT + BT) {
@@ -287,7 +297,9 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P>(RA > 0), 1)
     constexpr int GPW = 32 / PL;
     constexpr int LP = (P >= 128) ? 7 : (P >= 64) ? 6 : (P >= 32) ? 5 : (P >= 16) ? 4 : (P >= 8) ? 3 : (P >= 4) ? 2 : 1;
     const int lig = lane & (PL - 1), giw = lane / PL;
-    const int j1 = (warp - AT / 32) * GPW + giw;  // NBW * GPW >= RR: one j1 per lane group
+    const int wb = warp - AT / 32;
+    const int half = wb % SPL;                      // SPL = 2: which slot this warp keeps
+    const int j1 = (wb / SPL) * GPW + giw;  // NBW * GPW >= RR * SPL: one j1 per lane group (pair)
     const bool valid = j1 < RR;
     const int M2 = pl.M2, mt2 = pl.mt2;
     uint32_t i = 0;
@@ -330,15 +342,35 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P>(RA > 0), 1)
         if (x[0][0].x == 1234.5f) G[0] = x[0][1];
         continue;
       }
-      fft_dif<S, RR>(x, P, PL, lig, tw2s, -1);
-      if (dbg & 4) {  // profiling experiment: stage B + FFT, no band
-        if (x[0][0].x == 1234.5f) G[0] = x[0][1];
-        continue;
+      if constexpr (SPL == 2) {
+        // first DIF stage (slot pair, h = 32) in-thread, then this warp keeps one slot:
+        // the remaining cross-lane stages use the same twiddles as the S = 2 transform
+        C xh[1][RR];
+        const C w = twiddle(tw2s, lig, -1);
+#pragma unroll
+        for (int j = 0; j < RR; ++j) xh[0][j] = half ? cmul(csub(x[0][j], x[1][j]), w) : cadd(x[0][j], x[1][j]);
+        fft_dif<1, RR>(xh, P, PL, lig, tw2s, -1);
+        if (dbg & 4) {  // profiling experiment: stage B + FFT, no band
+          if (xh[0][0].x == 1234.5f) G[0] = xh[0][1];
+          continue;
+        }
+        if (valid) {
+          const int u2 = bitrev(half * PL + lig, LP);
+          band_horner<RR>(W2s, M2, (u2 + mt2) & (P - 1), P, mt2, R(1) / R(P), xh[0], [&](int b, C v) {
+            Gst[(size_t)(b / kStripNB) * REC + j1 * kStripNB + (b % kStripNB)] = v;
+          });
+        }
+      } else {
+        fft_dif<S, RR>(x, P, PL, lig, tw2s, -1);
+        if (dbg & 4) {  // profiling experiment: stage B + FFT, no band
+          if (x[0][0].x == 1234.5f) G[0] = x[0][1];
+          continue;
+        }
       }
       if constexpr (HORNER) {
         // band by Horner into the staging block, then coalesced record copies:
         // this tile owns record (strip, k1) = 80 contiguous elements of every strip
-        if (valid) {
+        if (SPL == 1 && valid) {
 #pragma unroll
           for (int ss = 0; ss < S; ++ss) {
             const int u2 = bitrev(ss * PL + lig, LP);
@@ -427,13 +459,21 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P>(RA > 0), 1)
           b[2 * hh] = CT<R>::mk(tb.x, tb.y);
           b[2 * hh + 1] = CT<R>::mk(tb.z, tb.w);
         }
-      } else if constexpr (VC == 2 && sizeof(C) == 8) {  // host guarantees sh == 0 here
-        const float4 ta = *reinterpret_cast<const float4*>(slot + c0);
-        const float4 tb = *reinterpret_cast<const float4*>(slot + lds + c0);
-        a[0] = CT<R>::mk(ta.x, ta.y);
-        a[VC - 1] = CT<R>::mk(ta.z, ta.w);
-        b[0] = CT<R>::mk(tb.x, tb.y);
-        b[VC - 1] = CT<R>::mk(tb.z, tb.w);
+      } else if constexpr (VC == 2 && sizeof(C) == 8) {
+        if (sh == 0) {  // 16-byte phase (plain fields, even window offsets)
+          const float4 ta = *reinterpret_cast<const float4*>(slot + c0);
+          const float4 tb = *reinterpret_cast<const float4*>(slot + lds + c0);
+          a[0] = CT<R>::mk(ta.x, ta.y);
+          a[VC - 1] = CT<R>::mk(ta.z, ta.w);
+          b[0] = CT<R>::mk(tb.x, tb.y);
+          b[VC - 1] = CT<R>::mk(tb.z, tb.w);
+        } else {
+#pragma unroll
+          for (int v = 0; v < VC; ++v) {
+            a[v] = slot[sh + c0 + v];
+            b[v] = slot[lds + sh + c0 + v];
+          }
+        }
       } else {
 #pragma unroll
         for (int v = 0; v < VC; ++v) {
