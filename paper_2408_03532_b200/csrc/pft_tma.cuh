@@ -726,7 +726,6 @@ __global__ void __launch_bounds__(adj_rows_threads<RR, P, P2T_>(RA > 0), 1)
           for (int j = 0; j < RR; ++j) tv[v][j] = T[(size_t)j * ldT + tc];
         }
         auto store = [&](int l, const C (&z)[VC]) {
-          if ((dbg & 2) && z[0].x != R(12345.5)) return;
           if constexpr (VC == 2 && sizeof(C) == 8) {
             *reinterpret_cast<float4*>(o + (size_t)l * n2 + c) = make_float4(z[0].x, z[0].y, z[VC - 1].x, z[VC - 1].y);
           } else {
