@@ -214,23 +214,40 @@ def run_ours(args):
     import paper_2408_03532_b200 as P
     from paper_2408_03532_b200._lib import KernelProfile
 
+    from paper_2408_03532_b200.dist import make_fields, pft_fwd_adj_sharded, shard_range
+
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    table, n, mt, p, dt, batch, desc = WORKLOADS[args.workload]
+    table, n, mt, p, dt, global_batch, desc = WORKLOADS[args.workload]
     cdt = torch.complex64 if dt == "c64" else torch.complex128
     plan = P.pft_plan_2d(n, n, mt, mt, p, p, 1.0, P.ScopeTable.load(DATA / table))
     M = 2 * mt
     esize = 8 if dt == "c64" else 16
-    g = torch.Generator(device="cuda").manual_seed(1000 + rank)
-    z = torch.complex(torch.randn((batch, n, n), device="cuda", generator=g),
-                      torch.randn((batch, n, n), device="cuda", generator=g)).to(cdt)
+    # E1: strong scaling by default -- the global batch of
+    # BASELINE configs[1] (64 fields) is split into contiguous blocks of
+    # 64/N fields per rank; --weak keeps 64 fields per rank (replicas). Every
+    # field is generated from (seed, global index), so rank blocks are slices
+    # of the same global batch.
+    if args.weak:
+        fb, fe = rank * global_batch, (rank + 1) * global_batch
+    else:
+        fb, fe = shard_range(global_batch, rank, world)
+    batch = fe - fb
+    total_fields = global_batch * world if args.weak else global_batch
+    z = make_fields(1000, fb, fe, n, n, cdt, "cuda")
+    # inputs larger than L2 between timed steps: when a rank's block is smaller
+    # than 2 x L2 (N >= 4 at 64/N fields), steps rotate over identical copies
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    ncopy = max(1, -(-2 * l2 // max(1, batch * n * n * esize)))
+    zs = [z] + [z.clone() for _ in range(ncopy - 1)]
     stream = torch.cuda.current_stream()
+    it = [0]
 
     def step():
-        band = P.pft_apply_2d(plan, z)
-        return P.pft_adjoint_2d(plan, band)
+        it[0] += 1
+        return pft_fwd_adj_sharded(plan, zs[it[0] % ncopy])[1]
 
     def barrier():
         if world > 1:
@@ -271,7 +288,7 @@ def run_ours(args):
         ms = float(t.item())
     ms_per_step = ms / args.steps
     transforms_per_step = 2 * batch
-    value = world * transforms_per_step * args.steps / (ms / 1e3)
+    value = 2 * total_fields * args.steps / (ms / 1e3)  # all ranks' transforms / max-over-ranks time
     alg_bytes_step = transforms_per_step * (n * n + M * M) * esize
 
     # dominant kernel roofline (per-launch algorithmic bytes / event time)
@@ -311,7 +328,7 @@ def run_ours(args):
         t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_e2e = float(t.item())
-    e2e_value = world * transforms_per_step * e2e_steps / t_e2e
+    e2e_value = 2 * total_fields * e2e_steps / t_e2e
     h2d = batch * (n * n + M * M) * esize
     d2h = batch * (M * M + n * n) * esize
 
@@ -333,13 +350,19 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "transforms/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
             "dtype": "f32" if dt == "c64" else "f64",
-            "data": "synthetic (seeded standard-normal fields)",
-            "config": {"workload": args.workload, "description": desc, "fields_per_rank": batch,
-                       "band": [M, M], "l2": "inputs larger than L2 (no flush)",
+            "data": "synthetic (seeded standard-normal fields, field f from (seed, f))",
+            "config": {"workload": args.workload, "description": desc, "global_batch": total_fields,
+                       "fields_per_rank": batch,
+                       "band": [M, M],
+                       "l2": ("inputs larger than L2 (no flush)" if ncopy == 1 else
+                              f"inputs larger than L2: steps rotate over {ncopy} copies of the rank's "
+                              f"{batch}-field block ({ncopy * batch * n * n * esize / 1e6:.0f} MB > 2 x L2)"),
                        "gb_per_s_algorithmic": alg_bytes_step * args.steps / (ms / 1e3) / 1e9 * world,
-                       "parallelism": f"weak-scaled replicas x{world}, no data-path collective"},
+                       "parallelism": (f"weak-scaled replicas x{world}" if args.weak else
+                                       f"batch {global_batch} sharded {global_batch}/{world} per rank")
+                                      + ", no data-path collective (NCCL: scalar max of the step time)"},
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": (None if captured_traffic_per_field(kname) is None
@@ -529,6 +552,20 @@ def run_evaluator(args):
         dist.destroy_process_group()
 
 
+def spawn_ranks(n):
+    """`python bench.py --gpus N` outside torchrun: launch N ranks (one per GPU)
+    through torch.distributed.run on 127.0.0.1; rank 0 prints the JSON line."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())]
+    cmd += sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -537,7 +574,11 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", choices=tuple(WORKLOADS) + ("cfg3", "cfg4", "cfg5"), default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--weak", action="store_true",
+                    help="cfg2: 64 fields per rank (replicas) instead of the 64-field batch sharded over ranks")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(spawn_ranks(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     elif args.workload in ("cfg3", "cfg4"):

@@ -117,8 +117,10 @@ int pftg_crop_centered_dev(int dtype, const void* spectrum, void* out, size_t ro
 
 /* ---- scan geometry and updates ---------------------------------------------- */
 /* window_slice / set_window (scan.hpp:40-42): patches [batch][wr][wc] at
- * (offsets[2k], offsets[2k+1]) of a fr x fc frame. No bounds check on offsets,
- * like the reference (scan.cpp:14-22). offsets are HOST int64 pairs. */
+ * (offsets[2k], offsets[2k+1]) of a fr x fc frame. offsets are HOST int64
+ * pairs. Unlike the reference (scan.cpp:14-22, unchecked) every window is
+ * bounds-checked: PFTG_ERANGE if it leaves the frame (a device-side overrun
+ * would leave the CUDA context unusable). */
 int pftg_window_slice_dev(int dtype, const void* frame, size_t fr, size_t fc, void* patches,
                           size_t wr, size_t wc, const int64_t* offsets, size_t npos, void* stream);
 int pftg_set_window_dev(int dtype, void* frame, size_t fr, size_t fc, const void* patch, size_t wr,

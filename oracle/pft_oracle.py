@@ -129,53 +129,75 @@ def _u(M, mt, p):
     return (np.arange(M) - mt) % p
 
 
-def pft_apply_2d(plan: Plan2D, z):
+def _ctype(dtype):
+    """oracle<double> (complex128, the default) or oracle<float> (complex64):
+    every stage below runs in that precision -- tables rounded once, products and
+    sums (einsum), the slice DFT (numpy.fft keeps complex64) -- so the float
+    variant measures the deviation an exact-order single-precision evaluation of
+    the reference's algorithm has from the double one (the complex64 parity floor,
+    SURVEY §8(c) C5)."""
+    ct = np.dtype(dtype)
+    if ct not in (np.complex64, np.complex128):
+        raise TypeError("oracle dtype must be complex64 or complex128")
+    return ct
+
+
+def pft_apply_2d(plan: Plan2D, z, dtype=np.complex128):
     """pft_apply_2d (pft.cpp:119-172), same four stages in the same order."""
     a1, a2 = plan.a1, plan.a2
-    z = np.asarray(z, np.complex128)
+    ct = _ctype(dtype)
+    z = np.asarray(z).astype(ct)
     if z.shape != (a1.n, a2.n):
         raise ValueError("pft_apply_2d: z shape must match the plan")
+    B1, B2 = a1.B.astype(ct), a2.B.astype(ct)
+    W1, W2 = a1.W[: 2 * a1.mt].astype(ct), a2.W[: 2 * a2.mt].astype(ct)
     Z = z.reshape(a1.p, a1.q, a2.n)
     # stage A (133-136): T[k1] = B1^T Z_blk
-    T = np.einsum("lj,kln->kjn", a1.B, Z)
+    T = np.einsum("lj,kln->kjn", B1, Z)
     # stage B (137-144): C[k1,k2,j1,j2] = sum_l2 T[k1,j1,k2*q2+l2] B2[l2,j2]
-    C = np.einsum("kjpl,lm->kpjm", T.reshape(a1.p, a1.r, a2.p, a2.q), a2.B)
+    C = np.einsum("kjpl,lm->kpjm", T.reshape(a1.p, a1.r, a2.p, a2.q), B2)
     # stage C (147): unnormalized 2-D DFT over (k1, k2)
     Ch = np.fft.fft2(C, axes=(0, 1))
     # stage D (149-170): out[a,b] = sum_j1 W1[a,j1] sum_j2 Ch[u1,u2,j1,j2] W2[b,j2]
     u1, u2 = _u(2 * a1.mt, a1.mt, a1.p), _u(2 * a2.mt, a2.mt, a2.p)
     S = Ch[u1][:, u2]  # (M1, M2, r1, r2)
-    inner = np.einsum("abjm,bm->abj", S, a2.W[: 2 * a2.mt])
-    return np.einsum("aj,abj->ab", a1.W[: 2 * a1.mt], inner)
+    inner = np.einsum("abjm,bm->abj", S, W2)
+    return np.einsum("aj,abj->ab", W1, inner)
 
 
-def pft_adjoint_2d(plan: Plan2D, band):
-    """pft_adjoint_2d (pft.cpp:174-226): D-dagger scatter, backward DFT, B-dagger, A-dagger."""
+def pft_adjoint_2d(plan: Plan2D, band, dtype=np.complex128):
+    """pft_adjoint_2d (pft.cpp:174-226): D-dagger scatter, backward DFT, B-dagger, A-dagger.
+    ``dtype`` as in pft_apply_2d (complex64 = oracle<float>)."""
     a1, a2 = plan.a1, plan.a2
-    y = np.asarray(band, np.complex128)
+    ct = _ctype(dtype)
+    y = np.asarray(band).astype(ct)
     if y.shape != (2 * a1.mt, 2 * a2.mt):
         raise ValueError("pft_adjoint_2d: band shape must match the plan")
+    W1c = np.conj(a1.W[: 2 * a1.mt]).astype(ct)
+    W2c = np.conj(a2.W[: 2 * a2.mt]).astype(ct)
     u1, u2 = _u(2 * a1.mt, a1.mt, a1.p), _u(2 * a2.mt, a2.mt, a2.p)
-    contrib = np.einsum("aj,ab,bm->abjm", np.conj(a1.W[: 2 * a1.mt]), y,
-                        np.conj(a2.W[: 2 * a2.mt]))
-    C = np.zeros((a1.p, a2.p, a1.r, a2.r), np.complex128)
+    # D-dagger: contribution of band element (a, b) to (u1, u2, j1, j2), in the
+    # reference's order c1 = conj(W1[a,j1]) y(a,b), then c1 conj(W2[b,j2]) (184-203)
+    c1 = np.einsum("aj,ab->abj", W1c, y)
+    contrib = np.einsum("abj,bm->abjm", c1, W2c)
+    C = np.zeros((a1.p, a2.p, a1.r, a2.r), ct)
     np.add.at(C, (u1[:, None], u2[None, :]), contrib)  # scatter-accumulate (184-203)
-    C = np.fft.ifft2(C, axes=(0, 1)) * (a1.p * a2.p)     # unnormalized backward (205)
-    M = np.einsum("kpjm,lm->kjpl", C, np.conj(a2.B))     # M = Cslice B2^H (213-220)
+    C = (np.fft.ifft2(C, axes=(0, 1)) * (a1.p * a2.p)).astype(ct)  # unnormalized backward (205)
+    M = np.einsum("kpjm,lm->kjpl", C, np.conj(a2.B).astype(ct))  # M = Cslice B2^H (213-220)
     T = M.reshape(a1.p, a1.r, a2.n)
-    Z = np.einsum("lj,kjn->kln", np.conj(a1.B), T)        # Zblk = conj(B1) T (221-223)
+    Z = np.einsum("lj,kjn->kln", np.conj(a1.B).astype(ct), T)  # Zblk = conj(B1) T (221-223)
     return Z.reshape(a1.n, a2.n)
 
 
 # ---------------------------------------------------------------- transforms
-def fast_fft2(z):
+def fast_fft2(z, dtype=np.complex128):
     """fast_fft2 (fft.cpp:175-178): unnormalized forward."""
-    return np.fft.fft2(np.asarray(z, np.complex128))
+    return np.fft.fft2(np.asarray(z).astype(_ctype(dtype)))
 
 
-def fast_ifft2(z):
+def fast_ifft2(z, dtype=np.complex128):
     """fast_ifft2 (fft.cpp:180-183): inverse with 1/n."""
-    return np.fft.ifft2(np.asarray(z, np.complex128))
+    return np.fft.ifft2(np.asarray(z).astype(_ctype(dtype)))
 
 
 def naive_dft2(z):
@@ -208,16 +230,17 @@ def _phase_unit(v):
     return out
 
 
-def project_modulus(exit_wave, d):
+def project_modulus(exit_wave, d, dtype=np.complex128):
     """project_modulus (solver.cpp:35-42)."""
-    spec = fast_fft2(exit_wave)
-    return fast_ifft2(np.asarray(d) * _phase_unit(spec))
+    spec = fast_fft2(exit_wave, dtype)
+    return fast_ifft2(np.asarray(d).astype(spec.real.dtype) * _phase_unit(spec), dtype)
 
 
-def band_residual(plan, exit_wave, d_crop):
+def band_residual(plan, exit_wave, d_crop, dtype=np.complex128):
     """band_residual (solver.cpp:61-69)."""
-    band = pft_apply_2d(plan, exit_wave)
-    return pft_adjoint_2d(plan, band - np.asarray(d_crop) * _phase_unit(band))
+    band = pft_apply_2d(plan, exit_wave, dtype)
+    return pft_adjoint_2d(plan, band - np.asarray(d_crop).astype(band.real.dtype) * _phase_unit(band),
+                          dtype)
 
 
 def pie_object_update(zj, probe, projected, beta):
@@ -232,13 +255,13 @@ def epie_probe_update(probe, zj, projected, gamma, blind=True):
     return probe - gamma * np.conj(zj) * (probe * zj - projected)
 
 
-def objective_value(frame, probe, offsets, d):
+def objective_value(frame, probe, offsets, d, dtype=np.complex128):
     """objective_value (solver.cpp:89-102)."""
     wr, wc = probe.shape
     acc = 0.0
     for j, (r0, c0) in enumerate(offsets):
         ex = frame[r0:r0 + wr, c0:c0 + wc] * probe
-        acc += float(np.sum(np.abs(ex - project_modulus(ex, d[j])) ** 2))
+        acc += float(np.sum(np.abs(ex - project_modulus(ex, d[j], dtype)).astype(np.float64) ** 2))
     return acc / len(offsets)
 
 
@@ -254,13 +277,59 @@ def evaluate_shard(frame, probe, offsets, d, begin, end):
     return acc
 
 
+class Mt19937_64:
+    """std::mt19937_64 (the C++ standard's parameters; default-seeded like
+    ``std::mt19937_64 rng(seed)``), for the shuffled visit order."""
+
+    def __init__(self, seed):
+        m = (1 << 64) - 1
+        self.mt = [seed & m]
+        for i in range(1, 312):
+            prev = self.mt[-1]
+            self.mt.append((6364136223846793005 * (prev ^ (prev >> 62)) + i) & m)
+        self.i = 312
+
+    def __call__(self):
+        m = (1 << 64) - 1
+        if self.i >= 312:
+            mt = self.mt
+            for k in range(312):
+                y = (mt[k] & 0xFFFFFFFF80000000) | (mt[(k + 1) % 312] & 0x7FFFFFFF)
+                v = mt[(k + 156) % 312] ^ (y >> 1)
+                if y & 1:
+                    v ^= 0xB5026F5AA96619E9
+                mt[k] = v
+            self.i = 0
+        y = self.mt[self.i]
+        self.i += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & m
+
+
+def shuffle_order(order, rng):
+    """shuffle_order (solver.cpp:164-169): Fisher-Yates with rng() % i draws."""
+    for i in range(len(order), 1, -1):
+        j = rng() % i
+        order[i - 1], order[j] = order[j], order[i - 1]
+
+
 def hybrid_solve(frame, probe, offsets, d, *, pft_sweeps, fft_sweeps, table=None, beta=1.0,
-                 gamma=1.0, beta_pft=1e-3, gamma_pft=1e-3, eps_pft=1e-3, mt=0, p=0, blind=False):
+                 gamma=1.0, beta_pft=1e-3, gamma_pft=1e-3, eps_pft=1e-3, mt=0, p=0, blind=False,
+                 shuffled=False, seed=0, dtype=np.complex128):
     """hybrid_solve (solver.cpp:173-302), sequential order, no TV, tol = 0.
+    ``dtype=np.complex64`` is oracle<float>: frame, probe, measurements and every
+    operator in single precision (the reference of the complex64 ePIE tolerance).
 
     Returns (frame, probe, objectives)."""
-    frame = np.array(frame, np.complex128)
-    probe = np.array(probe, np.complex128)
+    ct = _ctype(dtype)
+    rt = np.float32 if ct == np.complex64 else np.float64
+    frame = np.array(frame).astype(ct)
+    probe = np.array(probe).astype(ct)
+    d = np.asarray(d).astype(rt)
+    beta, gamma, beta_pft, gamma_pft = (rt(v) for v in (beta, gamma, beta_pft, gamma_pft))
     wr, wc = probe.shape
     plan = dcrop = None
     if pft_sweeps > 0:
@@ -270,20 +339,25 @@ def hybrid_solve(frame, probe, offsets, d, *, pft_sweeps, fft_sweeps, table=None
         plan = plan_2d(wr, wc, mt1, mt2, p1, p2, eps_pft, table)
         dcrop = [crop_centered(dj, mt1, mt2) for dj in d]
     objs = []
+    rng = Mt19937_64(seed)
+    order = list(range(len(offsets)))
     for sweep in range(1, pft_sweeps + fft_sweeps + 1):
         band_stage = sweep <= pft_sweeps
-        for j, (r0, c0) in enumerate(offsets):
+        if shuffled:  # solver.cpp:222-236, the order persists across sweeps
+            shuffle_order(order, rng)
+        for j in order:
+            r0, c0 = offsets[j]
             zj = frame[r0:r0 + wr, c0:c0 + wc].copy()
             ex = probe * zj
             if band_stage:
-                zj = zj - beta_pft * np.conj(probe) * band_residual(plan, ex, dcrop[j])
+                zj = zj - beta_pft * np.conj(probe) * band_residual(plan, ex, dcrop[j], ct)
                 if blind:
-                    resid2 = band_residual(plan, probe * zj, dcrop[j])
+                    resid2 = band_residual(plan, probe * zj, dcrop[j], ct)
                     probe = probe - gamma_pft * np.conj(zj) * resid2
             else:
-                zj = pie_object_update(zj, probe, project_modulus(ex, d[j]), beta)
+                zj = pie_object_update(zj, probe, project_modulus(ex, d[j], ct), beta)
                 if blind:
-                    probe = epie_probe_update(probe, zj, project_modulus(probe * zj, d[j]), gamma)
+                    probe = epie_probe_update(probe, zj, project_modulus(probe * zj, d[j], ct), gamma)
             frame[r0:r0 + wr, c0:c0 + wc] = zj
-        objs.append(objective_value(frame, probe, offsets, d))
+        objs.append(objective_value(frame, probe, offsets, d, ct))
     return frame, probe, np.array(objs)

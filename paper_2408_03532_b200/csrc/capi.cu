@@ -24,6 +24,37 @@ thread_local std::string g_err;
 
 void set_error(const std::string& m) { g_err = m; }
 
+const Knobs& knobs() {
+  static const Knobs k = [] {
+    auto on = [](const char* n) { return std::getenv(n) != nullptr; };
+    auto num = [](const char* n) {
+      const char* v = std::getenv(n);
+      return v ? std::atoi(v) : 0;
+    };
+    Knobs o{};
+    o.no_pdl = on("PFTG_NO_PDL");
+    o.no_tma = on("PFTG_NO_TMA");
+    o.no_ws = on("PFTG_NO_WS");
+    o.no_wide = on("PFTG_NO_WIDE");
+    o.no_split = on("PFTG_NO_SPLIT");
+    o.no_local_cols = on("PFTG_NO_LOCAL_COLS");
+    o.eval_lanefft = on("PFTG_EVAL_LANEFFT");
+    o.epie_lanefft = on("PFTG_EPIE_LANEFFT");
+    o.tma_ns = num("PFTG_TMA_NS");
+    o.cols_grid = num("PFTG_COLS_GRID");
+#ifdef PFTG_PROFILING
+    o.debug_tma = num("PFTG_DEBUG_TMA");
+    o.debug_ws = num("PFTG_DEBUG_WS");
+    o.debug_adj = num("PFTG_DEBUG_ADJ");
+    o.debug_cols = num("PFTG_DEBUG_COLS");
+    o.debug_adjcols = num("PFTG_DEBUG_ADJCOLS");
+    o.debug_wide_adj = on("PFTG_DEBUG_WIDE_ADJ");
+#endif
+    return o;
+  }();
+  return k;
+}
+
 void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
   char buf[512];
   std::snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d in %s", cudaGetErrorName(e),
@@ -134,7 +165,13 @@ template <class T>
 T* dev_upload(const std::vector<T>& h) {
   T* d = nullptr;
   PFTG_CUDA(cudaMalloc(&d, sizeof(T) * std::max<std::size_t>(h.size(), 1)));
-  if (!h.empty()) PFTG_CUDA(cudaMemcpy(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+  // Stream-ordered copy + synchronize: a plain cudaMemcpy from pageable memory
+  // may return before the DMA lands, and the tables are then read by kernels on
+  // non-blocking streams that do not order after the legacy stream.
+  if (!h.empty()) {
+    PFTG_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, cudaStreamPerThread));
+    PFTG_CUDA(cudaStreamSynchronize(cudaStreamPerThread));
+  }
   return d;
 }
 
@@ -245,32 +282,36 @@ void free_tables(DevTables<R>& t) {
 
 }  // namespace
 
-template <>
-const PftDev<float>& plan_dev<float>(const pftg_plan& p) {
+namespace {
+template <class R>
+const PftDev<R>& plan_dev_impl(const pftg_plan& p, std::map<int, std::unique_ptr<DevPlan<R>>>& per_dev) {
   ensure_device();
   int dev = 0;
   PFTG_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(p.mu);
-  if (p.dev32 != dev) {
-    if (p.dev32 >= 0) free_tables(p.t32);
-    upload(p, p.t32, p.pd32);
-    p.dev32 = dev;
+  auto it = per_dev.find(dev);
+  if (it == per_dev.end()) {
+    auto dp = std::make_unique<DevPlan<R>>();
+    try {
+      upload(p, dp->t, dp->pd);
+    } catch (...) {
+      free_tables(dp->t);
+      throw;
+    }
+    it = per_dev.emplace(dev, std::move(dp)).first;
   }
-  return p.pd32;
+  return it->second->pd;  // stable address: entries are never erased while the plan lives
+}
+}  // namespace
+
+template <>
+const PftDev<float>& plan_dev<float>(const pftg_plan& p) {
+  return plan_dev_impl<float>(p, p.dev32);
 }
 
 template <>
 const PftDev<double>& plan_dev<double>(const pftg_plan& p) {
-  ensure_device();
-  int dev = 0;
-  PFTG_CUDA(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> lock(p.mu);
-  if (p.dev64 != dev) {
-    if (p.dev64 >= 0) free_tables(p.t64);
-    upload(p, p.t64, p.pd64);
-    p.dev64 = dev;
-  }
-  return p.pd64;
+  return plan_dev_impl<double>(p, p.dev64);
 }
 
 // ---------------------------------------------------------------- operators
@@ -497,6 +538,16 @@ __global__ void k_crop(const R* __restrict__ spec, R* __restrict__ out, int rows
   }
 }
 
+// The reference does not bounds-check scan offsets (scan.cpp:14-22); on the
+// device an out-of-frame window would be an illegal access that leaves the
+// CUDA context unusable, so every window is checked (std::out_of_range).
+void check_window(long long r0, long long c0, std::size_t wr, std::size_t wc, std::size_t fr, std::size_t fc) {
+  if (r0 < 0 || c0 < 0 || r0 + (long long)wr > (long long)fr || c0 + (long long)wc > (long long)fc)
+    throw std::out_of_range("scan: window (" + std::to_string(r0) + ", " + std::to_string(c0) + ") of " +
+                            std::to_string(wr) + " x " + std::to_string(wc) + " outside the " + std::to_string(fr) +
+                            " x " + std::to_string(fc) + " frame");
+}
+
 int grid_for(long long n) {
   long long g = (n + 255) / 256;
   return (int)std::max<long long>(1, std::min<long long>(g, 148LL * 32));
@@ -515,7 +566,10 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
   const long long n = (long long)n1 * n2;
   const std::size_t count = pe - pb;
   std::vector<long long> offs(count);
-  for (std::size_t j = 0; j < count; ++j) offs[j] = offsets[2 * (pb + j)] * (long long)fc + offsets[2 * (pb + j) + 1];
+  for (std::size_t j = 0; j < count; ++j) {
+    check_window(offsets[2 * (pb + j)], offsets[2 * (pb + j) + 1], wr, wc, fr, fc);
+    offs[j] = offsets[2 * (pb + j)] * (long long)fc + offsets[2 * (pb + j) + 1];
+  }
   const PftDev<R>* pd = plan ? &plan_dev<R>(*plan) : nullptr;
   if (pd && (pd->n1 != n1 || pd->n2 != n2))
     throw std::invalid_argument("band_residual: plan does not match the window shape");
@@ -524,7 +578,7 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
   if (count) PFTG_CUDA(cudaMemcpyAsync(doffs.p, offs.data(), sizeof(long long) * count, cudaMemcpyHostToDevice, st));
   Scratch X(sizeof(Cx<R>) * n * chunk, st);
   // complex64 512 x 512 windows (BASELINE configs[4]): radix-8 register FFT kernels (eval_fft.cuh)
-  const bool fast512 = sizeof(R) == 4 && n1 == 512 && n2 == 512 && !std::getenv("PFTG_EVAL_LANEFFT");
+  const bool fast512 = sizeof(R) == 4 && n1 == 512 && n2 == 512 && !knobs().eval_lanefft;
   const int nstrips = fast512 ? 64 : fft_cols_strips<R>(n2);
   Scratch part(sizeof(double) * nstrips * std::max<std::size_t>(count, 1), st);
   std::unique_ptr<Scratch> G, bpart;
@@ -600,8 +654,17 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
 }  // namespace pftg
 
 pftg_plan::~pftg_plan() {
-  if (dev32 >= 0) pftg::free_tables(t32);
-  if (dev64 >= 0) pftg::free_tables(t64);
+  int cur = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess) return;
+  for (auto& e : dev32) {
+    cudaSetDevice(e.first);
+    pftg::free_tables(e.second->t);
+  }
+  for (auto& e : dev64) {
+    cudaSetDevice(e.first);
+    pftg::free_tables(e.second->t);
+  }
+  cudaSetDevice(cur);
 }
 
 // ------------------------------------------------------------------ C ABI
@@ -877,11 +940,13 @@ int pftg_window_slice_dev(int dtype, const void* frame, size_t fr, size_t fc, vo
                           const int64_t* offsets, size_t npos, void* stream) {
   return guarded([&] {
     check_dtype(dtype);
-    (void)fr;
     if (npos == 0) return;
     ensure_device();
     std::vector<long long> offs(npos);
-    for (size_t j = 0; j < npos; ++j) offs[j] = offsets[2 * j] * (long long)fc + offsets[2 * j + 1];
+    for (size_t j = 0; j < npos; ++j) {
+      check_window(offsets[2 * j], offsets[2 * j + 1], wr, wc, fr, fc);
+      offs[j] = offsets[2 * j] * (long long)fc + offsets[2 * j + 1];
+    }
     Scratch d(sizeof(long long) * npos, S(stream));
     PFTG_CUDA(cudaMemcpyAsync(d.p, offs.data(), sizeof(long long) * npos, cudaMemcpyHostToDevice, S(stream)));
     const long long tot = (long long)wr * wc * npos;
@@ -903,7 +968,7 @@ int pftg_set_window_dev(int dtype, void* frame, size_t fr, size_t fc, const void
                         int64_t r0, int64_t c0, void* stream) {
   return guarded([&] {
     check_dtype(dtype);
-    (void)fr;
+    check_window(r0, c0, wr, wc, fr, fc);
     ensure_device();
     const long long off = r0 * (long long)fc + c0;
     const long long tot = (long long)wr * wc;
@@ -957,7 +1022,6 @@ int pftg_evaluate_dev(int dtype, const void* frame, size_t fr, size_t fc, const 
                       const pftg_plan* plan, const void* dcrop, double* fft_sum, double* band_sum, void* stream) {
   return guarded([&] {
     check_dtype(dtype);
-    (void)fr;
     ensure_device();
     if (dtype == PFTG_C64)
       evaluate_dev<float>(frame, fr, fc, probe, wr, wc, offsets, npos, pos_begin, pos_end, d, plan, dcrop, fft_sum,

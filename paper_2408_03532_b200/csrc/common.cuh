@@ -19,6 +19,16 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+// Profiling experiments (stage-skipping switches used to split a kernel's time
+// between its phases) exist only in a -DPFTG_PROFILING build of the library
+// (tools/); in the product build PFTG_DBG is a compile-time false and the
+// experiment branches are compiled out.
+#ifdef PFTG_PROFILING
+#define PFTG_DBG(d, m) ((((d) & (m)) != 0))
+#else
+#define PFTG_DBG(d, m) (false && (d))
+#endif
+
 namespace pftg {
 
 template <class R>

@@ -2,7 +2,9 @@
 // fft_launch_f32.cu / fft_launch_f64.cu (PFTG_REAL = float | double).
 #include <cmath>
 #include <mutex>
+#include <set>
 #include <type_traits>
+#include <utility>
 
 #include "internal.hpp"
 
@@ -28,7 +30,14 @@ void dispatch_slots(int S, F&& f) {
 
 template <class K>
 void allow_smem_fft(K kernel) {
-  PFTG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  // one-time (per kernel and device) opt-in to 227 KB of dynamic shared memory
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  PFTG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.insert({reinterpret_cast<const void*>(kernel), dev}).second)
+    PFTG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
 }
 
 int slots_for(int n) { return n <= 32 ? 1 : n / 32; }
@@ -57,7 +66,8 @@ const C_* fft_twiddles<R_>(int n) {
     }
     C_* d = nullptr;
     PFTG_CUDA(cudaMalloc(&d, sizeof(C_) * h));
-    PFTG_CUDA(cudaMemcpy(d, host.data(), sizeof(C_) * h, cudaMemcpyHostToDevice));
+    PFTG_CUDA(cudaMemcpyAsync(d, host.data(), sizeof(C_) * h, cudaMemcpyHostToDevice, cudaStreamPerThread));
+    PFTG_CUDA(cudaStreamSynchronize(cudaStreamPerThread));  // before any non-blocking stream reads it
     tabs[dev][lg] = d;
   }
   return tabs[dev][lg];
@@ -87,8 +97,7 @@ void launch_fft_rows<R_>(int mode, int epi, int n1, int n2, const RowSrc<R_>& sr
                                                                            x_bstride, sign, scale, ep);
     } else if (mode == ROW_DIT_NATURAL) {
       auto k = k_fft_rows<R_, SS, ROW_DIT_NATURAL, EPI_STORE>;
-      static bool once = (allow_smem_fft(k), true);
-      (void)once;
+      allow_smem_fft(k);
       k<<<grid, threads, smem, st>>>(n1, n2, ilog2(n2), tw, src, X, x_bstride, sign, scale, ep);
     } else if (epi == EPI_STORE) {
       k_fft_rows<R_, SS, ROW_DIT_PROJ, EPI_STORE><<<grid, threads, smem, st>>>(n1, n2, ilog2(n2), tw, src, X,
@@ -134,26 +143,22 @@ void launch_fft_cols<R_>(int mode, int n1, int n2, C_* X, long long x_bstride, c
     constexpr int SS = decltype(s)::value;
     if (mode == COL_PROJECT) {
       auto k = k_fft_cols<R_, SS, COL_PROJECT>;
-      static bool once = (allow_smem_fft(k), true);
-      (void)once;
+      allow_smem_fft(k);
       k<<<grid, threads, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
                                  dmode, sign, partial);
     } else if (mode == COL_EVAL) {
       auto k = k_fft_cols<R_, SS, COL_EVAL>;
-      static bool once = (allow_smem_fft(k), true);
-      (void)once;
+      allow_smem_fft(k);
       k<<<grid, threads, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
                                  dmode, sign, partial);
     } else if (mode == COL_EVAL_NAT) {
       auto k = k_fft_cols<R_, SS, COL_EVAL_NAT>;
-      static bool once = (allow_smem_fft(k), true);
-      (void)once;
+      allow_smem_fft(k);
       k<<<grid, threads, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
                                  dmode, sign, partial);
     } else {
       auto k = k_fft_cols<R_, SS, COL_NATURAL>;
-      static bool once = (allow_smem_fft(k), true);
-      (void)once;
+      allow_smem_fft(k);
       k<<<grid, threads, smem, st>>>(n1, n2, ilog2(n1), ilog2(n2), nc, tw, X, x_bstride, d, d_bstride, d_index,
                                  dmode, sign, partial);
     }

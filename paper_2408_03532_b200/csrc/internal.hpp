@@ -5,6 +5,8 @@
 
 #include <complex>
 #include <cstdint>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -29,6 +31,19 @@ void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
   } while (0)
 #define PFTG_LAUNCH_CHECK() PFTG_CUDA(cudaGetLastError())
 
+// Runtime switches, read from the environment ONCE per process (knobs()):
+// alternative (correct) kernel choices used for A/B measurements, and -- in a
+// -DPFTG_PROFILING build only -- the stage-skipping profiling experiments
+// (debug_*), which are forced to 0 in the product build. PFTG_CHUNK_MB (the G
+// budget per chunk) is the one knob read per call (chunk_fields in capi.cu).
+struct Knobs {
+  bool no_pdl, no_tma, no_ws, no_wide, no_split, no_local_cols, eval_lanefft, epie_lanefft;
+  int tma_ns, cols_grid;  // 0 = unset
+  int debug_tma, debug_ws, debug_adj, debug_cols, debug_adjcols;
+  bool debug_wide_adj;
+};
+const Knobs& knobs();
+
 template <class R>
 struct DevTables {
   R* Bv1 = nullptr;
@@ -41,15 +56,23 @@ struct DevTables {
 
 }  // namespace pftg
 
-// pft::PftPlan2D (pft.hpp:44-47): host tables + lazily uploaded device tables.
+namespace pftg {
+// Device copy of a plan's tables on one device, in one precision.
+template <class R>
+struct DevPlan {
+  DevTables<R> t;
+  PftDev<R> pd{};
+};
+}  // namespace pftg
+
+// pft::PftPlan2D (pft.hpp:44-47): host tables + lazily uploaded device tables,
+// one immutable copy per (device, precision): a plan shared by threads that
+// drive different GPUs never frees tables another thread may still read.
 struct pftg_plan {
   pftg::Axis a1, a2;
   mutable std::mutex mu;
-  mutable int dev32 = -1, dev64 = -1;  // device the tables live on (-1 = not uploaded)
-  mutable pftg::DevTables<float> t32;
-  mutable pftg::DevTables<double> t64;
-  mutable pftg::PftDev<float> pd32{};
-  mutable pftg::PftDev<double> pd64{};
+  mutable std::map<int, std::unique_ptr<pftg::DevPlan<float>>> dev32;
+  mutable std::map<int, std::unique_ptr<pftg::DevPlan<double>>> dev64;
   mutable std::vector<double> hbv1, hbv2;  // nonzero parts of B1, B2 (host; kernel-parameter tables)
   ~pftg_plan();
 };

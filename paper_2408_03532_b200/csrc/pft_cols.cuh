@@ -365,9 +365,9 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
       const int s = i & 1, sbi = (int)(i % kStripBufs);
       const C* sb = buf + (size_t)sbi * sbytes_e;
       C* X = Xs + (size_t)s * P * LDX;
-      if (!(dbg & 4) || i < kStripBufs) mbar_wait(&full[sbi], (i / kStripBufs) & 1);
+      if (!PFTG_DBG(dbg, 4) || i < kStripBufs) mbar_wait(&full[sbi], (i / kStripBufs) & 1);
       if (i >= 2) mbar_wait(&xfree[s], ((i >> 1) - 1) & 1);
-      if (t < NSEQ && !(dbg & 1)) {
+      if (t < NSEQ && !PFTG_DBG(dbg, 1)) {
         // sequence (j1, bb) = (t / 8, t % 8): FFT over k1, spectrum to X[u][t]
         C x[P];
 #pragma unroll
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
       named_sync(1, FT);  // strip buffer sbi consumed, X complete
       if (t == 0) {
         mbar_arrive(&xready[s]);
-        if (!(dbg & 4) && sg + kStripBufs * (int)gridDim.x < ntotal) {
+        if (!PFTG_DBG(dbg, 4) && sg + kStripBufs * (int)gridDim.x < ntotal) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           load_strip(sg + kStripBufs * gridDim.x, buf + (size_t)sbi * sbytes_e, &full[sbi]);
         }
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(32 * (kFftWarps + kBandWarps), 2)
     const int s = i & 1;
     const int f = sg / nstrips_field, b0 = (sg % nstrips_field) * kStripNB;
     mbar_wait(&xready[s], (i >> 1) & 1);
-    if (!(dbg & 2)) {
+    if (!PFTG_DBG(dbg, 2)) {
       const C* xr = Xs + (size_t)s * P * LDX + (size_t)ub * LDX;
       C xv[RR];
 #pragma unroll
@@ -481,8 +481,8 @@ __global__ void __launch_bounds__(kColsThreads, 2)
     C* Ys = Ys0 + (size_t)(i & 1) * M1 * LDY;
     cp_async_wait_all();
     __syncthreads();  // Ys[i & 1] landed for every thread; Xs free (previous FFT done)
-    if (sg + (int)gridDim.x < ntotal && !(dbg & 8)) fetch(sg + gridDim.x, Ys0 + (size_t)((i + 1) & 1) * M1 * LDY);
-    if (t < P * kStripNB && !(dbg & 1)) {  // dbg 1: profiling switch, no gather
+    if (sg + (int)gridDim.x < ntotal && !PFTG_DBG(dbg, 8)) fetch(sg + gridDim.x, Ys0 + (size_t)((i + 1) & 1) * M1 * LDY);
+    if (t < P * kStripNB && !PFTG_DBG(dbg, 1)) {  // dbg 1: profiling switch, no gather
       C x[RR];
 #pragma unroll
       for (int j = 0; j < RR; ++j) x[j] = czero<C>();
@@ -492,14 +492,14 @@ __global__ void __launch_bounds__(kColsThreads, 2)
       for (int j = 0; j < RR; ++j) Xs[(size_t)(j * kStripNB + gbb) * LDS_ + gu] = x[j];
     }
     __syncthreads();  // Xs complete
-    if (t < NSEQ && !(dbg & 2)) {  // dbg 2: no FFT
+    if (t < NSEQ && !PFTG_DBG(dbg, 2)) {  // dbg 2: no FFT
       C x[P];
 #pragma unroll
       for (int uu = 0; uu < P; ++uu) x[uu] = Xs[(size_t)t * LDS_ + uu];
       fft_dif_local<P>(x, w, +1);
       // sequence t = (j1, bb): Gt[f][k1][j1][b0 + bb]
       C* gcol = Gt + (size_t)f * P * RR * M2 + (size_t)(t / kStripNB) * M2 + b0 + (t % kStripNB);
-      if (!(dbg & 4)) {  // dbg 4: no stores
+      if (!PFTG_DBG(dbg, 4)) {  // dbg 4: no stores
 #pragma unroll
         for (int pos = 0; pos < P; ++pos) {
           constexpr int LP = 5;

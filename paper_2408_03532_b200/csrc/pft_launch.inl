@@ -69,7 +69,7 @@ void allow_smem(K kernel) {
 // griddep_wait() before touching global memory (tma.cuh). PFTG_NO_PDL=1: plain launch.
 template <class... KA, class... A>
 void launch_pdl(void (*kernel)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
-  static const bool off = std::getenv("PFTG_NO_PDL") != nullptr;
+  const bool off = knobs().no_pdl;
   // not inside stream capture: the per-position ePIE graphs measured slower with programmatic edges
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   const bool capturing = cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
@@ -198,7 +198,7 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
                        (src.bstride * sizeof(typename CT<R_>::C)) % 16 == 0 &&
                        (!src.probe || reinterpret_cast<uintptr_t>(src.probe) % 16 == 0);
   if (!base_ok) return false;
-  if (std::getenv("PFTG_NO_TMA")) return false;
+  if (knobs().no_tma) return false;
   int vc = 0;
   if (pd.n2 == kTmaConsumers) vc = 1;
   else if (sizeof(R_) == 4 && pd.n2 == 2 * kTmaConsumers) vc = 2;
@@ -216,24 +216,22 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
     PFTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     const int ntiles = pd.p1 * batch;
     const int grid = ntiles < nsm ? ntiles : nsm;
-    const char* dv = std::getenv("PFTG_DEBUG_TMA");
-    const int dbg = dv ? std::atoi(dv) : 0;
-    if (const char* e = std::getenv("PFTG_TMA_NS")) ns = std::min(ns, std::atoi(e));
+    const int dbg = knobs().debug_tma;
+    if (knobs().tma_ns) ns = std::min(ns, knobs().tma_ns);
     // warp-specialized version when the double-buffered T still leaves >= 3 ring slots
     const bool wp = src.probe != nullptr;
     int ns2 = 12;
     while (ns2 > 3 && tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, wp) > 227 * 1024) --ns2;
-    if (const char* e = std::getenv("PFTG_TMA_NS")) ns2 = std::max(3, std::min(ns2, std::atoi(e)));
-    const char* d2 = std::getenv("PFTG_DEBUG_WS");
-    const int dbg2 = d2 ? std::atoi(d2) : 0;
+    if (knobs().tma_ns) ns2 = std::max(3, std::min(ns2, knobs().tma_ns));
+    const int dbg2 = knobs().debug_ws;
     if constexpr (sizeof(R_) == 4 && Q == 32) {
       // wide variant: 256 group-A threads x 4 columns with setmaxnreg (plain complex64 fields, n2 = 1024)
       constexpr int AT = 256, NT = fwd_rows_threads<AT, RR, P>(true);
       constexpr int L = (65536 / NT) & ~7, RB = L < 72 ? L : 72;
       constexpr int RA0 = L + (((NT - AT) * (L - RB) / AT) & ~7), RA = RA0 > 248 ? 248 : RA0;
       const size_t smem2 = tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, false);
-      if (plain && src.vec_ok && pd.n2 == AT * 4 && !dbg && !std::getenv("PFTG_NO_WS") &&
-          !std::getenv("PFTG_NO_WIDE") && smem2 <= 227 * 1024) {
+      if (plain && src.vec_ok && pd.n2 == AT * 4 && !dbg && !knobs().no_ws && !knobs().no_wide &&
+          smem2 <= 227 * 1024) {
         auto k = kt2_fwd_rows<R_, Q, RR, P, 4, AT, RA, RB>;
         cudaFuncAttributes fa{};
         PFTG_CUDA(cudaFuncGetAttributes(&fa, k));
@@ -252,8 +250,7 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
       // becomes 256 threads x 2 columns so the block stays within 1024 threads
       constexpr int AT = 256, NT = fwd_rows_threads<AT, RR, P, 2>(false);
       const size_t smem2 = tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, wp);
-      if (pd.n2 == 2 * AT && NT <= 1024 && !dbg && !std::getenv("PFTG_NO_WS") && !std::getenv("PFTG_NO_SPLIT") &&
-          smem2 <= 227 * 1024) {
+      if (pd.n2 == 2 * AT && NT <= 1024 && !dbg && !knobs().no_ws && !knobs().no_split && smem2 <= 227 * 1024) {
         auto k = kt2_fwd_rows<R_, Q, RR, P, 2, AT, 0, 0, 2>;
         {
           allow_smem(k);
@@ -264,7 +261,7 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
         }
       }
     }
-    if (!dbg && !std::getenv("PFTG_NO_WS") && tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, wp) <= 227 * 1024) {
+    if (!dbg && !knobs().no_ws && tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, wp) <= 227 * 1024) {
       const size_t smem2 = tma2_rows_smem<R_>(pd.n2, Q, RR, pd.M2, P, ns2, wp);
       constexpr int NT = kTmaConsumers + 32 * fwd_b_warps<RR, P>() + 32;
       auto k = kt2_fwd_rows<R_, Q, RR, P, (sizeof(R_) == 4 ? 2 : 1)>;
@@ -303,7 +300,7 @@ bool tma_fwd_rows(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* 
 #if PFTG_PART_ADJ
 bool tma_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, const EpiArgs& ep, int batch,
                   cudaStream_t st) {
-  if (epi != 0 || !ep.vec_ok || std::getenv("PFTG_NO_TMA")) return false;
+  if (epi != 0 || !ep.vec_ok || knobs().no_tma) return false;
   // P2 owns column pairs (c64) or single columns (c128); any even n2 works
   const int vc = sizeof(R_) == 4 ? 2 : 1;
   if (pd.n2 % vc) return false;
@@ -319,14 +316,13 @@ bool tma_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, c
     const int ntiles = pd.p1 * batch;
     const int grid = ntiles < nsm ? ntiles : nsm;
     auto* out = reinterpret_cast<typename CT<R_>::C*>(ep.out);
-    const char* dv = std::getenv("PFTG_DEBUG_ADJ");
-    const int dbg = dv ? std::atoi(dv) : 0;
+    const int dbg = knobs().debug_adj;
     if constexpr (sizeof(R_) == 4 && Q == 32) {
       // wide variant: 8 P2 warps x 4 columns first, setmaxnreg hand-over (complex64, n2 = 1024)
       constexpr int P2T = 256, NT = adj_rows_threads<RR, P, P2T>(true);
       constexpr int L = (65536 / NT) & ~7, RB = L < 72 ? L : 72;
       constexpr int RA0 = L + (((NT - P2T) * (L - RB) / P2T) & ~7), RA = RA0 > 248 ? 248 : RA0;
-      if (pd.n2 == P2T * 4 && (!dbg || std::getenv("PFTG_DEBUG_WIDE_ADJ")) && !std::getenv("PFTG_NO_WIDE")) {
+      if (pd.n2 == P2T * 4 && (!dbg || knobs().debug_wide_adj) && !knobs().no_wide) {
         auto k = kt_adj_rows<R_, Q, RR, P, 4, P2T, RA, RB>;
         cudaFuncAttributes fa{};
         PFTG_CUDA(cudaFuncGetAttributes(&fa, k));
@@ -397,8 +393,7 @@ bool launch_fwd_rows<R_>(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R
   if (smem > 227 * 1024) throw std::invalid_argument("pftg: plan too large for the rows pass (smem)");
   dispatch_sr(slots_of(pd.p2), rb_of(std::max(pd.r1, pd.r2)), [&](auto s, auto rb) {
     auto k = k_fwd_rows<R_, decltype(s)::value, decltype(rb)::value>;
-    static bool once = (allow_smem(k), true);
-    (void)once;
+    allow_smem(k);
     k<<<dim3(pd.p1, batch), rows_threads<R_>(), smem, st>>>(pd, src, G);
   });
   PFTG_LAUNCH_CHECK();
@@ -432,17 +427,16 @@ void launch_fwd_cols<R_>(const PftDev<R_>& pd, int mode, const typename CT<R_>::
       constexpr int RR = decltype(r)::value, P = decltype(p)::value;
       const int nsf = pd.M2 / kStripNB, total = nsf * batch;
       int grid = std::min(total, 2 * sm_count());
-      if (const char* e = std::getenv("PFTG_COLS_GRID")) grid = std::min(total, std::atoi(e));
+      if (knobs().cols_grid) grid = std::min(total, knobs().cols_grid);
       if constexpr (P == kLocalP && sizeof(R_) == 4) {
         auto kl = kc_fwd_cols_local<R_, RR>;
         cudaFuncAttributes fa{};
         PFTG_CUDA(cudaFuncGetAttributes(&fa, kl));
         // setmaxnreg hand-over inside the kernel assumes the launch register count
-        if (!std::getenv("PFTG_NO_LOCAL_COLS") && fa.numRegs == kColsRegLaunch) {
+        if (!knobs().no_local_cols && fa.numRegs == kColsRegLaunch) {
           allow_smem(kl);
-          const char* dc = std::getenv("PFTG_DEBUG_COLS");
           launch_pdl(kl, grid, 32 * (kFftWarps + kBandWarps), cols_fwd_local_smem<R_>(RR, pd.M1), st, pd, G,
-                     (long long)strip_field_elems(pd), band, nsf, total, dc ? std::atoi(dc) : 0);
+                     (long long)strip_field_elems(pd), band, nsf, total, knobs().debug_cols);
           return;
         }
       }
@@ -470,18 +464,15 @@ void launch_fwd_cols<R_>(const PftDev<R_>& pd, int mode, const typename CT<R_>::
     constexpr int S = decltype(s)::value, RB = decltype(rb)::value;
     if (mode == 0) {
       auto k = k_fwd_cols<R_, S, RB, 0>;
-      static bool once = (allow_smem(k), true);
-      (void)once;
+      allow_smem(k);
       k<<<grid, 256, smem, st>>>(pl, G, band, dc, dstride, Gout, partial);
     } else if (mode == 1) {
       auto k = k_fwd_cols<R_, S, RB, 1>;
-      static bool once = (allow_smem(k), true);
-      (void)once;
+      allow_smem(k);
       k<<<grid, 256, smem, st>>>(pl, G, band, dc, dstride, Gout, partial);
     } else {
       auto k = k_fwd_cols<R_, S, RB, 2>;
-      static bool once = (allow_smem(k), true);
-      (void)once;
+      allow_smem(k);
       k<<<grid, 256, smem, st>>>(pl, G, band, dc, dstride, Gout, partial);
     }
   });
@@ -492,18 +483,17 @@ template <>
 void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, typename CT<R_>::C* Gt,
                          int batch, cudaStream_t st) {
   ProfScope prof(st, K_ADJ_COLS);
-  if (fast_cols_ok(pd) && (long long)(pd.M2 / kStripNB) * batch >= 64 && !std::getenv("PFTG_NO_TMA")) {
+  if (fast_cols_ok(pd) && (long long)(pd.M2 / kStripNB) * batch >= 64 && !knobs().no_tma) {
     dispatch_fast(pd, [&](auto q, auto r, auto p) {
       constexpr int RR = decltype(r)::value, P = decltype(p)::value;
       const int nsf = pd.M2 / kStripNB, total = nsf * batch;
       const int grid = std::min(total, 2 * sm_count());
       if constexpr (P == kLocalP && sizeof(R_) == 4) {
-        if (!std::getenv("PFTG_NO_LOCAL_COLS") && pd.M1 <= 256) {
+        if (!knobs().no_local_cols && pd.M1 <= 256) {
           auto kl = kc_adj_cols_local<R_, RR>;
           allow_smem(kl);
-          const char* dc = std::getenv("PFTG_DEBUG_ADJCOLS");
           launch_pdl(kl, grid, kColsThreads, cols_adj_local_smem<R_>(RR, pd.M1), st, pd, band, Gt, nsf, total,
-                     dc ? std::atoi(dc) : 0);
+                     knobs().debug_adjcols);
           return;
         }
       }
@@ -521,8 +511,7 @@ void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, t
   if (smem > 227 * 1024) throw std::invalid_argument("pftg: plan too large for the cols pass (smem)");
   dispatch_sr(slots_of(pd.p1), rb_of(std::max(pd.r1, pd.r2)), [&](auto s, auto rb) {
     auto k = k_adj_cols<R_, decltype(s)::value, decltype(rb)::value>;
-    static bool once = (allow_smem(k), true);
-    (void)once;
+    allow_smem(k);
     launch_pdl(k, dim3(cols_strips(pl), batch), 256, smem, st, pl, band, Gt);
   });
   PFTG_LAUNCH_CHECK();
@@ -546,18 +535,15 @@ void launch_adj_rows<R_>(const PftDev<R_>& pd, int epi, const typename CT<R_>::C
     const dim3 grid(pd.p1, batch);
     if (epi == 0) {
       auto k = k_adj_rows<R_, S, RB, 0>;
-      static bool once = (allow_smem(k), true);
-      (void)once;
+      allow_smem(k);
       k<<<grid, rows_threads<R_>(), smem, st>>>(pd, Gt, ep);
     } else if (epi == 1) {
       auto k = k_adj_rows<R_, S, RB, 1>;
-      static bool once = (allow_smem(k), true);
-      (void)once;
+      allow_smem(k);
       k<<<grid, rows_threads<R_>(), smem, st>>>(pd, Gt, ep);
     } else {
       auto k = k_adj_rows<R_, S, RB, 2>;
-      static bool once = (allow_smem(k), true);
-      (void)once;
+      allow_smem(k);
       k<<<grid, rows_threads<R_>(), smem, st>>>(pd, Gt, ep);
     }
   });

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      if (dbg & 2) {  // profiling experiment: pure streaming (keep the loads alive)
+      if PFTG_DBG(dbg, 2) {  // profiling experiment: pure streaming (keep the loads alive)
         if (a[0].x == 1234.5f && b[0].y == -1234.5f) acc[0][0].x += 1;
         continue;
       }
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1)
       for (int j = 0; j < RR; ++j) T[(size_t)j * ldT + tc] = acc[v][j];
     }
     named_sync(1, kTmaConsumers);
-    if (dbg & 1) continue;  // profiling experiment: streaming + stage A only
+    if PFTG_DBG(dbg, 1) continue;  // profiling experiment: streaming + stage A only
     C* Gblk = G + ((size_t)f * pl.p1 + k1) * RR * pl.M2;
     // gstride > 0: strip-major layout for the persistent cols pass (field stride gstride)
     fast_stage_b_to_g<R, Q, RR, P>(pl, bp, T, W2s, tw2s, Gblk, kTmaConsumers / 32,
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P, SPL>(RA > 0), 1)
     // ---------------- producer ----------------
     if (threadIdx.x != AT + BT) return;
     const uint64_t pol = l2_evict_first_policy();
-    const bool hint = !offs && !(dbg & 16);  // scan windows overlap (L2 reuse): no hint; dbg 16: profiling switch
+    const bool hint = !offs && !PFTG_DBG(dbg, 16);  // scan windows overlap (L2 reuse): no hint; dbg 16: profiling switch
     uint32_t seq = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int f = t / pl.p1, k1 = t % pl.p1;
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P, SPL>(RA > 0), 1)
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
       const int f = t / pl.p1, k1 = t % pl.p1;
       mbar_wait(tready, i & 1);
-      if (dbg & 1) {  // profiling experiment: group B only hands T back
+      if PFTG_DBG(dbg, 1) {  // profiling experiment: group B only hands T back
         named_sync(2, BT);
         if (threadIdx.x == AT) mbar_arrive(tfree);
         continue;
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P, SPL>(RA > 0), 1)
       if (HORNER && gstride > 0 && threadIdx.x == AT) bulk_wait_read();
       named_sync(2, BT);  // group B is done reading T: group A may overwrite it
       if (threadIdx.x == AT) mbar_arrive(tfree);
-      if (dbg & 8) {  // profiling experiment: stage B only
+      if PFTG_DBG(dbg, 8) {  // profiling experiment: stage B only
         if (x[0][0].x == 1234.5f) G[0] = x[0][1];
         continue;
       }
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P, SPL>(RA > 0), 1)
 #pragma unroll
         for (int j = 0; j < RR; ++j) xh[0][j] = half ? cmul(csub(x[0][j], x[1][j]), w) : cadd(x[0][j], x[1][j]);
         fft_dif<1, RR>(xh, P, PL, lig, tw2s, -1);
-        if (dbg & 4) {  // profiling experiment: stage B + FFT, no band
+        if PFTG_DBG(dbg, 4) {  // profiling experiment: stage B + FFT, no band
           if (xh[0][0].x == 1234.5f) G[0] = xh[0][1];
           continue;
         }
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P, SPL>(RA > 0), 1)
         }
       } else {
         fft_dif<S, RR>(x, P, PL, lig, tw2s, -1);
-        if (dbg & 4) {  // profiling experiment: stage B + FFT, no band
+        if PFTG_DBG(dbg, 4) {  // profiling experiment: stage B + FFT, no band
           if (x[0][0].x == 1234.5f) G[0] = x[0][1];
           continue;
         }
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P, SPL>(RA > 0), 1)
         const int tb = threadIdx.x - AT;
         constexpr int NREC = RR * kStripNB;
         const int nrec = M2 / kStripNB;
-        if (dbg & 32) continue;  // profiling experiment: band staged, no G stores
+        if PFTG_DBG(dbg, 32) continue;  // profiling experiment: band staged, no G stores
         if (gstride > 0) {
           // one 1-D bulk store per (strip, k1) record (16-byte aligned: strip_rec); the
           // staging block is reused after bulk_wait_read() at the next tile's stage B
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(fwd_rows_threads<AT, RR, P, SPL>(RA > 0), 1)
   // column of this thread's v-th accumulator
   auto colv = [&](int v) { return VC == 4 ? 2 * (int)threadIdx.x + (v & 1) + (v >> 1) * (n2 >> 1) : (int)threadIdx.x * VC + v; };
   const int c0 = threadIdx.x * VC;
-  const bool dbg_stream = VC != 4 && (dbg & 2) != 0;
+  const bool dbg_stream = VC != 4 && PFTG_DBG(dbg, 2) != 0;
   // shared-memory byte address of this thread's first column in slot 0 (VC = 4)
   const uint32_t abase = smem_u32(ring) + 16u * threadIdx.x;
   const uint32_t slot_bytes = (uint32_t)(slot_e * sizeof(C));
@@ -633,7 +633,7 @@ __global__ void __launch_bounds__(adj_rows_threads<RR, P, P2T_>(RA > 0), 1)
       C* T = Tb + (size_t)s * RR * ldT;
       mbar_wait(&gfull[s], (i >> 1) & 1);
       if (i >= 2) mbar_wait(&tfree[s], ((i >> 1) - 1) & 1);
-      if (!(dbg & 1)) {
+      if (!PFTG_DBG(dbg, 1)) {
         C x[S][RR];
 #pragma unroll
         for (int ss = 0; ss < S; ++ss) {
@@ -693,7 +693,7 @@ __global__ void __launch_bounds__(adj_rows_threads<RR, P, P2T_>(RA > 0), 1)
     const C* T = Tb + (size_t)s * RR * ldT;
     mbar_wait(&tready[s], (i >> 1) & 1);
     C* o = out + ((size_t)f * pl.n1 + (size_t)k1 * Q) * n2;
-    if (WIDE && (dbg & 4)) {
+    if (WIDE && PFTG_DBG(dbg, 4)) {
       // profiling experiment: P2 idle (P1 alone)
     } else if constexpr (WIDE) {
       // columns 2 tid + {0, 1} and 2 tid + n2 / 2 + {0, 1}; one pass covers the row
@@ -716,7 +716,7 @@ __global__ void __launch_bounds__(adj_rows_threads<RR, P, P2T_>(RA > 0), 1)
         store(l, zl);
         store(Q - l, zm);
       });
-    } else if (!(dbg & 4)) {
+    } else if (!PFTG_DBG(dbg, 4)) {
       for (int c = tid * VC; c < n2; c += P2T * VC) {
         C tv[VC][RR];
 #pragma unroll

@@ -157,12 +157,12 @@ using Cx = typename CT<R>::C;
 // Full-FFT stage and objective on the radix-8 register FFT kernels (eval_fft.cuh):
 // complex64 512 x 512 windows. PFTG_EPIE_LANEFFT=1 keeps the lane-group kernels.
 inline bool use_fft512(const pftg_solver& s) {
-  static const bool off = std::getenv("PFTG_EPIE_LANEFFT") != nullptr;
+  const bool off = knobs().epie_lanefft;
   return !off && s.wr == 512 && s.wc == 512;
 }
 // The same for the per-position FFT stage of 256 x 256 windows (BASELINE configs[2]).
 inline bool use_fft256(const pftg_solver& s) {
-  static const bool off = std::getenv("PFTG_EPIE_LANEFFT") != nullptr;
+  const bool off = knobs().epie_lanefft;
   return !off && s.wr == 256 && s.wc == 256;
 }
 
@@ -466,17 +466,19 @@ void create(pftg_solver& s, const void* frame, const void* probe, const int64_t*
   PFTG_CUDA(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
   PFTG_CUDA(cudaMalloc(&s.frame, sizeof(Cx<R>) * fn));
   PFTG_CUDA(cudaMalloc(&s.probe, sizeof(Cx<R>) * pn));
-  PFTG_CUDA(cudaMemcpy(s.frame, frame, sizeof(Cx<R>) * fn, cudaMemcpyHostToDevice));
-  PFTG_CUDA(cudaMemcpy(s.probe, probe, sizeof(Cx<R>) * pn, cudaMemcpyHostToDevice));
+  PFTG_CUDA(cudaMemcpyAsync(s.frame, frame, sizeof(Cx<R>) * fn, cudaMemcpyHostToDevice, s.st));
+  PFTG_CUDA(cudaMemcpyAsync(s.probe, probe, sizeof(Cx<R>) * pn, cudaMemcpyHostToDevice, s.st));
   if (s.cfg.tol > 0.0) PFTG_CUDA(cudaMalloc(&s.prev, sizeof(Cx<R>) * fn));
   PFTG_CUDA(cudaMalloc(&s.d, sizeof(R) * pn * s.npos));
-  PFTG_CUDA(cudaMemcpy(s.d, d, sizeof(R) * pn * s.npos, cudaMemcpyHostToDevice));
+  // uploads are ordered on s.st ahead of the kernels that read them
+  PFTG_CUDA(cudaMemcpyAsync(s.d, d, sizeof(R) * pn * s.npos, cudaMemcpyHostToDevice, s.st));
   PFTG_CUDA(cudaMalloc(&s.dperm, sizeof(R) * pn * s.npos));
   k_permute_d<R><<<148 * 16, 256, 0, s.st>>>(static_cast<const R*>(s.d), static_cast<R*>(s.dperm), (int)s.wr,
                                              (int)s.wc, ilog2((int)s.wr), ilog2((int)s.wc), (long long)s.npos);
   PFTG_LAUNCH_CHECK();
   PFTG_CUDA(cudaMalloc(&s.doffs, sizeof(long long) * std::max<std::size_t>(s.npos, 1)));
-  PFTG_CUDA(cudaMemcpy(s.doffs, s.offs.data(), sizeof(long long) * s.npos, cudaMemcpyHostToDevice));
+  PFTG_CUDA(cudaMemcpyAsync(s.doffs, s.offs.data(), sizeof(long long) * s.npos, cudaMemcpyHostToDevice, s.st));
+  PFTG_CUDA(cudaStreamSynchronize(s.st));
   PFTG_CUDA(cudaMalloc(&s.X, sizeof(Cx<R>) * pn));
   PFTG_CUDA(cudaMalloc(&s.X2, sizeof(Cx<R>) * pn));
   s.eval_chunk = std::max<std::size_t>(1, std::min<std::size_t>(s.npos, (64u << 20) / (sizeof(Cx<R>) * pn)));
@@ -591,8 +593,10 @@ int pftg_solver_result(const pftg_solver* s, void* frame, void* probe) {
     if (!s) throw std::invalid_argument("pftg: null solver");
     const std::size_t cs = s->dtype == PFTG_C64 ? 8 : 16;
     PFTG_CUDA(cudaStreamSynchronize(s->st));
-    if (frame) PFTG_CUDA(cudaMemcpy(frame, s->frame, cs * s->fr * s->fc, cudaMemcpyDeviceToHost));
-    if (probe) PFTG_CUDA(cudaMemcpy(probe, s->probe, cs * s->wr * s->wc, cudaMemcpyDeviceToHost));
+    // the solver's work runs on its non-blocking stream: read back in stream order
+    if (frame) PFTG_CUDA(cudaMemcpyAsync(frame, s->frame, cs * s->fr * s->fc, cudaMemcpyDeviceToHost, s->st));
+    if (probe) PFTG_CUDA(cudaMemcpyAsync(probe, s->probe, cs * s->wr * s->wc, cudaMemcpyDeviceToHost, s->st));
+    PFTG_CUDA(cudaStreamSynchronize(s->st));
   });
 }
 

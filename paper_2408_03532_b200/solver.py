@@ -30,6 +30,22 @@ from ._lib import PFTG_C64, PFTG_C128, SolverConfigC, check, lib
 from .pft import PftPlan2D, ScopeTable, _batch, _dev, _dtype_code, _ptr, _real_of, _stream
 
 
+def _inplace(t, what):
+    """In-place targets must be contiguous CUDA tensors (the kernels write raw memory)."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{what}: expected a CUDA torch tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{what}: in-place target must be contiguous")
+    return t
+
+
+def _match(ref, what, *others):
+    """Operands must share the reference tensor's dtype and device (no silent casts)."""
+    for o in others:
+        if not isinstance(o, torch.Tensor) or o.dtype != ref.dtype or o.device != ref.device:
+            raise ValueError(f"{what}: operands must have dtype {ref.dtype} on {ref.device}")
+
+
 def project_modulus(exit_wave, d):
     """F^-1[d .* exp(i arg(F x))]; zero spectrum bins keep phase 1 (solver.cpp:35-42)."""
     x = _dev(exit_wave)
@@ -47,9 +63,9 @@ def pie_object_update(zj, probe, projected, beta):
     """In place: zj -= beta conj(P) (P zj - proj) (solver.cpp:44-50)."""
     if zj.shape != probe.shape or zj.shape != projected.shape:
         raise ValueError("pie_object_update: shape mismatch")
+    _inplace(zj, "pie_object_update")
+    _match(zj, "pie_object_update", probe, projected)
     p, q = _dev(probe), _dev(projected)
-    if not zj.is_contiguous():
-        raise ValueError("pie_object_update: zj must be contiguous")
     check(lib().pftg_pie_object_update_dev(_dtype_code(zj), _ptr(zj), _ptr(p), _ptr(q), zj.numel(),
                                            float(beta), _stream()))
     return zj
@@ -61,6 +77,8 @@ def epie_probe_update(probe, zj, projected, gamma, blind):
         raise RuntimeError("epie_probe_update: probe updates need blind mode")
     if zj.shape != probe.shape or zj.shape != projected.shape:
         raise ValueError("epie_probe_update: shape mismatch")
+    _inplace(probe, "epie_probe_update")
+    _match(probe, "epie_probe_update", zj, projected)
     z, q = _dev(zj), _dev(projected)
     check(lib().pftg_epie_probe_update_dev(_dtype_code(probe), _ptr(probe), _ptr(z), _ptr(q),
                                            probe.numel(), float(gamma), int(blind), _stream()))
@@ -85,6 +103,10 @@ def window_slice(frame, offsets, wr, wc):
 
 def set_window(frame, offset, patch):
     """In place: frame[r0:r0+wr, c0:c0+wc] = patch (scan.cpp:111-121)."""
+    _inplace(frame, "set_window")
+    _match(frame, "set_window", patch)
+    if frame.dim() != 2 or patch.dim() != 2:
+        raise ValueError("set_window: frame and patch must be 2-D")
     p = _dev(patch)
     r0, c0 = (int(v) for v in offset)
     check(lib().pftg_set_window_dev(_dtype_code(frame), _ptr(frame), frame.shape[0], frame.shape[1],
@@ -101,13 +123,24 @@ def evaluate(frame, probe, offsets, d, pos_range=None, plan: PftPlan2D | None = 
     band_sum = sum_j || |PFT(P z_j)| - d_crop_j ||^2 (else None).
     """
     f, p = _dev(frame), _dev(probe)
+    _match(f, "evaluate", p)
     o = _offsets(offsets)
     dd = _dev(d).to(_real_of(f))
     b, e = pos_range if pos_range is not None else (0, len(o))
+    if not 0 <= b <= e <= len(o):
+        raise IndexError("evaluate: position range outside the scan")
+    wr, wc = p.shape[-2:]
+    if dd.dim() != 3 or tuple(dd.shape[1:]) != (wr, wc) or dd.shape[0] < e:
+        raise ValueError(f"evaluate: d must be (>= {e}, {wr}, {wc}), got {tuple(dd.shape)}")
     fs, bs = C.c_double(0.0), C.c_double(0.0)
     dc = None
     if plan is not None:
         dc = _dev(d_crop).to(_real_of(f))
+        if dc.dim() != 3 or tuple(dc.shape[1:]) != plan.band_shape or dc.shape[0] < e:
+            raise ValueError(f"evaluate: d_crop must be (>= {e}, {plan.band_shape[0]}, "
+                             f"{plan.band_shape[1]}), got {tuple(dc.shape)}")
+        if plan.field_shape != (wr, wc):
+            raise ValueError("band_residual: plan does not match the window shape")
     check(lib().pftg_evaluate_dev(
         _dtype_code(f), _ptr(f), f.shape[0], f.shape[1], _ptr(p), p.shape[0], p.shape[1],
         o.ctypes.data_as(C.POINTER(C.c_int64)), len(o), b, e, _ptr(dd),

@@ -70,3 +70,47 @@ def test_sharded_objective_gloo_world2():
         phi, count = out[r]
         assert count == len(offs)  # every position evaluated exactly once
         assert abs(phi - want) <= 1e-12 * want
+
+
+def _e1_worker(rank, ws, port, total, out):
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    from paper_2408_03532_b200.dist import checksum, make_fields, shard_range
+    b, e = shard_range(total, rank, ws)
+    mine = make_fields(5, b, e, 16, 24, torch.complex64, "cpu")
+    blocks = [None] * ws
+    dist.all_gather_object(blocks, (b, e, mine.numpy()))
+    cs = checksum(mine)
+    if rank == 0:
+        out["blocks"] = blocks
+        out["checksum"] = cs
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws,total", [(2, 64), (2, 7), (3, 64)])
+def test_e1_field_sharding_gloo(ws, total):
+    """E1 (BASELINE configs[1], batch sharded over ranks): the rank blocks
+    partition the global batch and their union is bit-identical to the
+    single-rank batch (fields depend only on (seed, global index)); the scalar
+    checksum all-reduce equals the single-rank value."""
+    import torch
+    from paper_2408_03532_b200.dist import make_fields
+    want = make_fields(5, 0, total, 16, 24, torch.complex64, "cpu").numpy()
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_e1_worker, args=(r, ws, port, total, out)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    blocks = out["blocks"]
+    got = np.concatenate([blk for (_, _, blk) in blocks])
+    assert [(b, e) for (b, e, _) in blocks] == [shard_range(total, r, ws) for r in range(ws)]
+    assert got.shape == want.shape and np.array_equal(got, want)
+    ref = float(np.sum(np.abs(want.astype(np.complex128)) ** 2))
+    assert abs(out["checksum"] - ref) <= 1e-9 * ref

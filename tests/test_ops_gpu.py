@@ -135,6 +135,25 @@ def test_hybrid_solve_c128_matches_reference(ref, blind):
     assert np.allclose(res.objective, obj_ref, rtol=1e-8)
 
 
+# complex64 ePIE gate: the GPU complex64 solve may deviate from
+# the reference (double) by at most EPIE_FLOOR_FACTOR x the deviation of
+# oracle<float> -- the reference's algorithm run entirely in complex64
+# (oracle/pft_oracle.hybrid_solve(dtype=complex64)) -- on the same problem,
+# measured inside each test, plus an absolute slack for the tiny-divergence case.
+EPIE_FLOOR_FACTOR = 4.0
+
+
+def _epie_float_floor(init, pinit, offs, d, f_ref, p_ref, **kw):
+    from oracle import pft_oracle as O
+    tab = O.load_scope_table(DATA / "scope_table_v1.txt")
+    ff, pf, _ = O.hybrid_solve(init, pinit, offs, d, table=tab, dtype=np.complex64, **kw)
+    return rel_l2(ff, f_ref), rel_l2(pf, p_ref)
+
+
+def _epie_gate(floor):
+    return EPIE_FLOOR_FACTOR * floor + 1e-6
+
+
 def test_hybrid_solve_c64_tracks_reference(ref):
     rng = np.random.default_rng(19)
     obj, probe, offs = _small_problem(rng)
@@ -144,9 +163,11 @@ def test_hybrid_solve_c64_tracks_reference(ref):
               gamma_pft=1.0 / 64 ** 2, eps_pft=1e-3, blind=True)
     f_ref, p_ref, obj_ref, _, _ = ref.hybrid_solve(init, probe, offs, d, table_path=DATA / "scope_table_v1.txt",
                                                    **kw)
+    ff, fp = _epie_float_floor(init, probe, offs, d, f_ref, p_ref, **kw)
     res = P.hybrid_solve(d, offs, probe, init, P.SolverConfig(**kw), dtype=np.complex64)
-    assert rel_l2(res.frame, f_ref) <= 1e-4
-    assert rel_l2(res.probe, p_ref) <= 1e-4
+    ef, ep = rel_l2(res.frame, f_ref), rel_l2(res.probe, p_ref)
+    assert ef <= _epie_gate(ff), (ef, ff)
+    assert ep <= _epie_gate(fp), (ep, fp)
 
 
 def test_evaluator_band_and_fft(ref):
@@ -169,8 +190,8 @@ def test_evaluator_band_and_fft(ref):
 def test_cfg3_full_problem_one_band_one_fft_sweep(ref):
     """BASELINE configs[2] problem (1024^2 object, 400 positions of 256^2, M=64),
     blind, stable steps: GPU c128 == reference hybrid_solve to 1e-10 after one
-    PFT sweep + one FFT sweep; c64 within 1e-3 (float rounding through 800
-    sequential dependent updates)."""
+    PFT sweep + one FFT sweep; c64 within EPIE_FLOOR_FACTOR x the oracle<float>
+    divergence (float rounding through 800 sequential dependent updates)."""
     from paper_2408_03532_b200 import problems as PR
     prob = PR.make_problem("cfg3", seed=0)
     n, w = prob.obj.shape[0], prob.probe.shape[0]
@@ -188,7 +209,9 @@ def test_cfg3_full_problem_one_band_one_fft_sweep(ref):
     assert rel_l2(r128.frame, fr) <= 1e-10 and rel_l2(r128.probe, pr) <= 1e-10
     assert np.allclose(r128.objective, objr, rtol=1e-10)
     r64 = P.hybrid_solve(d, prob.offsets, pinit, init, P.SolverConfig(mt1=32, mt2=32, **kw))
-    assert rel_l2(r64.frame, fr) <= 1e-3 and rel_l2(r64.probe, pr) <= 1e-3
+    ff, fp = _epie_float_floor(init, pinit, prob.offsets, d, fr, pr, mt=32, **kw)
+    ef, ep = rel_l2(r64.frame, fr), rel_l2(r64.probe, pr)
+    assert ef <= _epie_gate(ff) and ep <= _epie_gate(fp), (ef, ff, ep, fp)
 
 
 
@@ -207,8 +230,12 @@ def test_hybrid_solve_shuffled_matches_reference(ref, w, dtype, pft):
     got = P.hybrid_solve(d, offs, probe * 0.9, init, P.SolverConfig(**kw), dtype=dtype)
     f_ref, p_ref, _, _, _ = ref.hybrid_solve(init, probe * 0.9, offs, d, table_path=DATA / "scope_table_v1.txt",
                                              **kw)
-    tol = 1e-10 if dtype == np.complex128 else 1e-4
-    assert rel_l2(got.frame, f_ref) <= tol and rel_l2(got.probe, p_ref) <= tol
+    ef, ep = rel_l2(got.frame, f_ref), rel_l2(got.probe, p_ref)
+    if dtype == np.complex128:
+        assert ef <= 1e-10 and ep <= 1e-10
+    else:
+        ff, fp = _epie_float_floor(init, probe * 0.9, offs, d, f_ref, p_ref, **kw)
+        assert ef <= _epie_gate(ff) and ep <= _epie_gate(fp), (ef, ff, ep, fp)
 
 
 def test_evaluator_tma_windows_c64(ref):
@@ -235,3 +262,85 @@ def test_evaluator_tma_windows_c64(ref):
     want_f = ref.objective_value(o64, p64, offs, d.astype(np.float64)) * len(offs)
     assert abs(bs - want_b) <= 1e-5 * want_b
     assert abs(fs - want_f) <= 1e-5 * want_f
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_crop_centered_bit_exact(ref, dtype):
+    """crop_centered(RealField) (fft.cpp:206-232) is pure index work: bit-exact
+    against the reference, batched, odd band offsets and mt = n/2."""
+    rng = np.random.default_rng(40)
+    for (n1, n2, mt1, mt2) in ((512, 512, 64, 64), (64, 128, 5, 17), (32, 32, 16, 16), (16, 8, 1, 4)):
+        d = (np.abs(cnormal(rng, (3, n1, n2))) * 7).astype(dtype)
+        got = P.crop_centered(torch.from_numpy(d).cuda(), mt1, mt2).cpu().numpy()
+        assert got.dtype == dtype
+        for b in range(3):
+            want = ref.crop_centered(d[b].astype(np.float64), mt1, mt2).astype(dtype)
+            assert np.array_equal(got[b], want), (n1, n2, mt1, mt2, b)
+    with pytest.raises(ValueError):
+        P.crop_centered(torch.zeros((8, 8), device="cuda"), 5, 1)
+
+
+def test_concurrent_streams_and_threads_bit_identical():
+    """B4: plans are immutable and every call takes its own stream-ordered
+    scratch, so concurrent calls -- two host threads, each on its own CUDA
+    stream, plus the host-buffer entry points from both threads -- give results
+    bit-identical to the serial run."""
+    import threading
+    g = P.pft_plan_2d(1024, 1024, 40, 40, 32, 32, 1e-3)
+    g2 = P.pft_plan_2d(256, 256, 32, 32, 32, 32, 1e-3)
+    rng = np.random.default_rng(41)
+    zs = [torch.from_numpy(cnormal(rng, (6, 1024, 1024), np.complex64)).cuda() for _ in range(2)]
+    hs = [cnormal(rng, (5, 256, 256), np.complex64) for _ in range(2)]
+    serial = [P.pft_adjoint_2d(g, P.pft_apply_2d(g, z)) for z in zs]
+    serial_h = [P.pft_apply_2d(g2, h) for h in hs]
+    torch.cuda.synchronize()
+    out, out_h, errs = [None, None], [None, None], []
+
+    def work(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(4):
+                    out[k] = P.pft_adjoint_2d(g, P.pft_apply_2d(g, zs[k]))
+                    out_h[k] = P.pft_apply_2d(g2, hs[k])
+            s.synchronize()
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for k in range(2):
+        assert torch.equal(out[k], serial[k])
+        assert np.array_equal(out_h[k], serial_h[k])
+
+
+def test_window_bounds_and_operand_checks():
+    """Out-of-frame windows raise IndexError (std::out_of_range) instead of a
+    device fault; in-place operands must be contiguous and share dtype/device."""
+    frame = torch.zeros((100, 90), dtype=torch.complex64, device="cuda")
+    patch = torch.ones((32, 32), dtype=torch.complex64, device="cuda")
+    for off in ((69, 0), (0, 59), (-1, 0), (0, -3)):
+        with pytest.raises(IndexError):
+            P.set_window(frame, off, patch)
+        with pytest.raises(IndexError):
+            P.window_slice(frame, np.array([off]), 32, 32)
+    P.set_window(frame, (68, 58), patch)  # the last in-frame corner is fine
+    assert torch.count_nonzero(frame) == 32 * 32
+    with pytest.raises(ValueError):
+        P.set_window(frame, (0, 0), patch.to(torch.complex128))
+    with pytest.raises(ValueError):
+        P.set_window(frame.t(), (0, 0), patch)
+    z = torch.ones((16, 16), dtype=torch.complex64, device="cuda")
+    with pytest.raises(ValueError):
+        P.pie_object_update(z, z.to(torch.complex128), z, 0.5)
+    with pytest.raises(ValueError):
+        P.epie_probe_update(z, z, z.to(torch.complex128), 0.5, True)
+    d = torch.ones((2, 32, 32), device="cuda")
+    with pytest.raises(IndexError):
+        P.evaluate(frame, patch, np.array([[0, 0], [80, 0]]), d)
+    with pytest.raises(ValueError):
+        P.evaluate(frame, patch, np.array([[0, 0], [10, 0], [20, 0]]), d)

@@ -198,3 +198,58 @@ def test_golden_fixtures_reproduce_from_reference(ref):
     rp = ref.RefPlan.create(DATA / "scope_table_v1.txt", 64, 64, 8, 8, 8, 8, 1e-7)
     assert np.array_equal(rp.apply(g["z"]), g["band"])
     assert np.array_equal(rp.adjoint(g["y"]), g["adj"])
+
+
+def test_oracle_shuffled_solve_matches_reference(ref):
+    """The oracle's mt19937_64 Fisher-Yates visit order (solver.cpp:164-169,
+    222-236) reproduces the reference's shuffled hybrid_solve."""
+    rng = np.random.default_rng(50)
+    n, w = 96, 32
+    obj = np.exp(1j * rng.uniform(-1, 1, (n, n))) * (0.5 + 0.5 * rng.random((n, n)))
+    probe = np.exp(-((np.mgrid[0:w, 0:w] - 15.5) ** 2).sum(0) / 100.0).astype(np.complex128)
+    offs = np.array([[r, c] for r in (0, 20, 40, 64) for c in (0, 30, 64)], np.int64)
+    d = ref.simulate(obj, probe, offs)
+    init = np.ones((n, n), np.complex128) * 0.8
+    kw = dict(pft_sweeps=1, fft_sweeps=2, beta=0.5, gamma=0.05, beta_pft=0.25 / w ** 2,
+              gamma_pft=0.01 / w ** 2, eps_pft=1e-3, blind=True, shuffled=True, seed=11)
+    fr, pr, objr, _, _ = ref.hybrid_solve(init, probe, offs, d, table_path=DATA / "scope_table_v1.txt", **kw)
+    fo, po, objo = O.hybrid_solve(init, probe, offs, d, table=O.load_scope_table(DATA / "scope_table_v1.txt"),
+                                  **kw)
+    # FFT/GEMM summation-order differences (numpy vs the shims) grow through the
+    # blind updates to ~3e-10; a wrong visit order is off by many orders more
+    assert rel_l2(fo, fr) <= 1e-8 and rel_l2(po, pr) <= 1e-8
+    assert np.allclose(objo, objr, rtol=1e-8)
+    fs, _, _ = O.hybrid_solve(init, probe, offs, d, table=O.load_scope_table(DATA / "scope_table_v1.txt"),
+                              **{**kw, "shuffled": False})
+    assert rel_l2(fs, fr) > 1e-6
+
+
+def test_mt19937_64_known_answer():
+    """C++ standard [rand.predef]: the 10000th output of a default-constructed
+    mt19937_64 (seed 5489) is 9981545732273789042."""
+    r = O.Mt19937_64(5489)
+    for _ in range(9999):
+        r()
+    assert r() == 9981545732273789042
+
+
+def test_oracle_float_floor_literal_cfg2(ref):
+    """oracle<float> (complex64 evaluation of the reference's stage order):
+    on the literal cfg2 plan (xi = 4, r = 10) it deviates from the reference by
+    ~1.6e-3 forward / ~2.5e-3 adjoint (the ill-conditioning of SURVEY §9.1); on
+    the scope-1 companion (p = 128, q = 8, r = 13) by < 1e-6. Its complex128
+    evaluation matches the reference to 1e-11."""
+    for tab, p, eps, lo, hi in (("scope_table_xi4_r10.txt", 32, 1.0, 5e-4, 5e-3),
+                                ("scope_table_v1.txt", 128, 1e-7, 1e-8, 1e-6)):
+        po = O.plan_2d(1024, 1024, 128, 128, p, p, eps, O.load_scope_table(DATA / tab))
+        rp = ref.RefPlan.create(DATA / tab, 1024, 1024, 128, 128, p, p, eps)
+        rng = np.random.default_rng(51)
+        z = cnormal(rng, (1024, 1024), np.complex64)
+        want = rp.apply(z.astype(np.complex128))
+        assert rel_l2(O.pft_apply_2d(po, z), want) <= 1e-11
+        fwd = rel_l2(O.pft_apply_2d(po, z, np.complex64), want)
+        y = want.astype(np.complex64)
+        want_a = rp.adjoint(y.astype(np.complex128))
+        assert rel_l2(O.pft_adjoint_2d(po, y), want_a) <= 1e-11
+        adj = rel_l2(O.pft_adjoint_2d(po, y, np.complex64), want_a)
+        assert lo <= fwd <= hi and lo <= adj <= hi, (tab, fwd, adj)
