@@ -77,6 +77,16 @@ int pftg_table_min_degree(const pftg_table* t, double eps, double target_scope, 
  * B[l,j] = w_j (1-2l/q)^j, W[t,j] = (t/p)^j e^{-i pi t/p}  (pft.cpp:33-76). */
 int pftg_plan_2d(const pftg_table* t, size_t n1, size_t n2, size_t mt1, size_t mt2, size_t p1,
                  size_t p2, double eps, pftg_plan** out);
+/* PftPlan2D from in-memory tables (pft.hpp:25-47): per axis n, p, mt, r and
+ * the B (q x r, q = n/p) and W ((2mt+1) x r) tables, complex128 interleaved,
+ * row-major exactly as PftPlan1D::B / ::W store them. The tables are copied; the
+ * plan is immutable. Lets a C++ host that already holds a
+ * ptycho::pft::PftPlan2D (built by the reference's pft_plan_2d) mirror it with
+ * no file round trip. Shape rules as pft_plan_1d
+ * (pft.cpp:35-40): PFTG_EINVAL otherwise. */
+int pftg_plan_from_tables(size_t n1, size_t p1, size_t mt1, int r1, const double* B1, const double* W1,
+                          size_t n2, size_t p2, size_t mt2, int r2, const double* B2, const double* W2,
+                          double eps, pftg_plan** out);
 /* load_plan_2d / save_plan (pft.hpp:60-63), "pft-plan-2d v1" + PTYC blocks. */
 int pftg_plan_load(const char* path, pftg_plan** out);
 int pftg_plan_save(const pftg_plan* plan, const char* path);

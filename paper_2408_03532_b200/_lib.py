@@ -19,7 +19,7 @@ PFTG_C64, PFTG_C128 = 0, 1
 EXPORTS = (
     "pftg_version", "pftg_last_error", "pftg_device_ok", "pftg_profile_begin", "pftg_profile_end",
     "pftg_table_load", "pftg_table_free", "pftg_table_min_degree",
-    "pftg_plan_2d", "pftg_plan_load", "pftg_plan_save", "pftg_plan_free", "pftg_plan_info",
+    "pftg_plan_2d", "pftg_plan_from_tables", "pftg_plan_load", "pftg_plan_save", "pftg_plan_free", "pftg_plan_info",
     "pftg_plan_tables",
     "pftg_apply_2d_dev", "pftg_adjoint_2d_dev", "pftg_apply_2d_host", "pftg_adjoint_2d_host",
     "pftg_band_residual_dev",
@@ -66,6 +66,8 @@ def lib():
     L.pftg_table_free.restype = None
     L.pftg_table_min_degree.argtypes = [vp, C.c_double, C.c_double, C.POINTER(C.c_int)]
     L.pftg_plan_2d.argtypes = [vp, sz, sz, sz, sz, sz, sz, C.c_double, C.POINTER(vp)]
+    L.pftg_plan_from_tables.argtypes = [sz, sz, sz, C.c_int, dp, dp, sz, sz, sz, C.c_int, dp, dp,
+                                        C.c_double, C.POINTER(vp)]
     L.pftg_plan_load.argtypes = [C.c_char_p, C.POINTER(vp)]
     L.pftg_plan_save.argtypes = [vp, C.c_char_p]
     L.pftg_plan_free.argtypes = [vp]

@@ -783,6 +783,38 @@ int pftg_plan_2d(const pftg_table* t, size_t n1, size_t n2, size_t mt1, size_t m
   });
 }
 
+int pftg_plan_from_tables(size_t n1, size_t p1, size_t mt1, int r1, const double* B1, const double* W1, size_t n2,
+                          size_t p2, size_t mt2, int r2, const double* B2, const double* W2, double eps,
+                          pftg_plan** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("pftg_plan_from_tables: null output");
+    auto axis = [eps](size_t n, size_t p, size_t mt, int r, const double* B, const double* W) {
+      // pft_plan_1d's domain (pft.cpp:35-40)
+      if (p < 2 || p > n || n % p != 0) throw std::invalid_argument("pft_plan_1d: p must divide n, 2 <= p <= n");
+      if (n / p < 2) throw std::invalid_argument("pft_plan_1d: need q = n/p >= 2");
+      if (mt < 1 || 2 * mt > n) throw std::invalid_argument("pft_plan_1d: need 1 <= mt and 2*mt <= n");
+      if (r < 1) throw std::invalid_argument("pft_plan_1d: need r >= 1");
+      if (!B || !W) throw std::invalid_argument("pftg_plan_from_tables: null table");
+      Axis a;
+      a.n = n;
+      a.p = p;
+      a.q = n / p;
+      a.mt = mt;
+      a.r = r;
+      a.eps = eps;
+      const cd* b = reinterpret_cast<const cd*>(B);
+      const cd* w = reinterpret_cast<const cd*>(W);
+      a.B.assign(b, b + a.q * (size_t)r);
+      a.W.assign(w, w + (2 * mt + 1) * (size_t)r);
+      return a;
+    };
+    auto p = std::make_unique<pftg_plan>();
+    p->a1 = axis(n1, p1, mt1, r1, B1, W1);
+    p->a2 = axis(n2, p2, mt2, r2, B2, W2);
+    *out = p.release();
+  });
+}
+
 int pftg_plan_load(const char* path, pftg_plan** out) {
   return guarded([&] {
     auto p = std::make_unique<pftg_plan>();

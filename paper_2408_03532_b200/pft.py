@@ -112,6 +112,23 @@ class PftPlan2D:
         check(lib().pftg_plan_load(str(path).encode(), C.byref(h)))
         return cls(h.value)
 
+    @classmethod
+    def from_tables(cls, n1, p1, mt1, B1, W1, n2, p2, mt2, B2, W2, eps=0.0) -> "PftPlan2D":
+        """Plan from in-memory PftPlan1D tables (B: q x r, W: (2mt+1) x r, complex128)."""
+        def arr(a):
+            return np.ascontiguousarray(a, np.complex128)
+        B1, W1, B2, W2 = arr(B1), arr(W1), arr(B2), arr(W2)
+        r1, r2 = B1.shape[1], B2.shape[1]
+        if B1.shape != (n1 // p1, r1) or W1.shape != (2 * mt1 + 1, r1) or \
+                B2.shape != (n2 // p2, r2) or W2.shape != (2 * mt2 + 1, r2):
+            raise ValueError("pftg_plan_from_tables: table shapes do not match the plan")
+        dp = C.POINTER(C.c_double)
+        h = C.c_void_p()
+        check(lib().pftg_plan_from_tables(n1, p1, mt1, r1, B1.ctypes.data_as(dp), W1.ctypes.data_as(dp),
+                                          n2, p2, mt2, r2, B2.ctypes.data_as(dp), W2.ctypes.data_as(dp),
+                                          eps, C.byref(h)))
+        return cls(h.value)
+
     def save(self, path) -> None:
         check(lib().pftg_plan_save(self._h, str(path).encode()))
 

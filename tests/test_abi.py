@@ -110,3 +110,19 @@ def test_tv_is_rejected_not_ignored():
     with pytest.raises(ValueError, match="TV"):
         P.Solver(np.zeros((1, 32, 32)), [[0, 0]], np.ones((32, 32)), np.ones((32, 32)),
                  P.SolverConfig(tv_lambda_mag=1e-3))
+
+
+def test_plan_from_tables_equals_file_plan(tmp_path, ref):
+    """pftg_plan_from_tables (the façade's in-memory plan import, no file round
+    trip): the reference's own PftPlan2D tables give a plan whose saved file is
+    byte-identical to the reference's save_plan of that plan."""
+    rp = ref.RefPlan.create(DATA / "scope_table_v1.txt", 256, 128, 32, 16, 32, 16, 1e-3)
+    (B1, W1), (B2, W2) = rp.tables(1), rp.tables(2)
+    pl = P.PftPlan2D.from_tables(256, 32, 32, B1, W1, 128, 16, 16, B2, W2, 1e-3)
+    assert (pl.n1, pl.p1, pl.q1, pl.mt1, pl.r1, pl.n2, pl.p2, pl.q2, pl.mt2, pl.r2) == \
+        (rp.n1, rp.p1, rp.q1, rp.mt1, rp.r1, rp.n2, rp.p2, rp.q2, rp.mt2, rp.r2)
+    pl.save(tmp_path / "ours.plan")
+    rp.save(tmp_path / "ref.plan")
+    assert (tmp_path / "ours.plan").read_bytes() == (tmp_path / "ref.plan").read_bytes()
+    with pytest.raises(ValueError, match="p must divide n"):
+        P.PftPlan2D.from_tables(250, 32, 32, B1[:7], W1, 128, 16, 16, B2, W2)
