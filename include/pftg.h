@@ -118,6 +118,10 @@ int pftg_band_residual_dev(const pftg_plan* plan, int dtype, const void* exit_wa
 /* fast_fft2 / fast_ifft2 (fft.hpp:18-19): power-of-two rows, cols in [2, 1024]. */
 int pftg_fft2_dev(int dtype, const void* z, void* out, size_t rows, size_t cols, size_t batch,
                   int inverse, void* stream);
+/* Host-buffer fast_fft2 / fast_ifft2 (copies pipelined with compute over
+ * chunks of the batch), for hosts that keep fields in host memory (the C++
+ * façade of INTEGRATION.md). */
+int pftg_fft2_host(int dtype, const void* z, void* out, size_t rows, size_t cols, size_t batch, int inverse);
 /* project_modulus (solver.hpp:51): F^-1[d .* exp(i arg(F x))], phase 1 where F x == 0. */
 int pftg_project_modulus_dev(int dtype, const void* exit_wave, const void* d, void* out, size_t rows,
                              size_t cols, size_t batch, void* stream);

@@ -19,20 +19,40 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "_ref" / "libptycho_ref.so"
+# The same verbatim reference library with pft_apply_2d / pft_adjoint_2d /
+# fast_fft2 / fast_ifft2 provided by the C++ façade over libpftg
+# (paper_2408_03532_b200/facade/pft_gpu.cpp; oracle/Makefile): the drop-in
+# demonstration. Selected with ``with ref.facade(): ...``.
+FACADE_PATH = HERE / "_ref" / "libptycho_facade.so"
 
-_lib = None
+_libs = {}
+_active = [LIB_PATH]
 
 
 def available() -> bool:
     return LIB_PATH.exists()
 
 
+class facade:
+    """Context manager: route every wrapper below through libptycho_facade.so."""
+
+    def __enter__(self):
+        if not FACADE_PATH.exists():
+            raise RuntimeError(f"façade build missing: {FACADE_PATH} (run make -C oracle)")
+        _active.append(FACADE_PATH)
+        return self
+
+    def __exit__(self, *exc):
+        _active.pop()
+        return False
+
+
 def lib():
-    global _lib
-    if _lib is None:
-        if not LIB_PATH.exists():
-            raise RuntimeError(f"reference oracle not built: {LIB_PATH} (run make -C oracle)")
-        L = C.CDLL(str(LIB_PATH))
+    path = _active[-1]
+    if path not in _libs:
+        if not path.exists():
+            raise RuntimeError(f"reference oracle not built: {path} (run make -C oracle)")
+        L = C.CDLL(str(path))
         vp, dp, szt, i64p = C.c_void_p, C.POINTER(C.c_double), C.c_size_t, C.POINTER(C.c_int64)
         L.ref_last_error.restype = C.c_char_p
         L.ref_plan_create.restype = vp
@@ -62,8 +82,8 @@ def lib():
         L.ref_scope_table_compute.argtypes = [C.c_char_p, dp, C.c_int, C.c_int]
         L.ref_scope_table_single.argtypes = [C.c_char_p, C.c_double, C.c_int, C.c_double]
         L.ref_min_degree.argtypes = [C.c_char_p, C.c_double, C.c_double, C.POINTER(C.c_int)]
-        _lib = L
-    return _lib
+        _libs[path] = L
+    return _libs[path]
 
 
 class RefError(RuntimeError):
@@ -100,9 +120,10 @@ class RefPlan:
     def __init__(self, handle):
         if not handle:
             _check(1)
+        self._L = lib()  # the library that owns the handle (reference or façade build)
         self.h = C.c_void_p(handle)
         info = np.zeros(10, np.int64)
-        lib().ref_plan_info(self.h, info.ctypes.data_as(C.POINTER(C.c_int64)))
+        self._L.ref_plan_info(self.h, info.ctypes.data_as(C.POINTER(C.c_int64)))
         (self.n1, self.p1, self.q1, self.mt1, self.r1,
          self.n2, self.p2, self.q2, self.mt2, self.r2) = (int(v) for v in info)
 
@@ -118,18 +139,18 @@ class RefPlan:
 
     def save(self, plan_path):
         """save_plan (pft.cpp:277-289)."""
-        _check(lib().ref_plan_save(self.h, str(plan_path).encode()))
+        _check(self._L.ref_plan_save(self.h, str(plan_path).encode()))
 
     def tables(self, axis: int):
         q, r, mt = (self.q1, self.r1, self.mt1) if axis == 1 else (self.q2, self.r2, self.mt2)
         B = np.zeros((q, r), np.complex128)
         W = np.zeros((2 * mt + 1, r), np.complex128)
-        lib().ref_plan_tables(self.h, axis, _cptr(B), _cptr(W))
+        self._L.ref_plan_tables(self.h, axis, _cptr(B), _cptr(W))
         return B, W
 
     def __del__(self):
         try:
-            lib().ref_plan_free(self.h)
+            self._L.ref_plan_free(self.h)
         except Exception:
             pass
 
@@ -137,14 +158,14 @@ class RefPlan:
         """pft_apply_2d (pft.cpp:119-172)."""
         z = _c128(z)
         out = np.zeros((2 * self.mt1, 2 * self.mt2), np.complex128)
-        _check(lib().ref_pft_apply_2d(self.h, _cptr(z), z.shape[0], z.shape[1], _cptr(out)))
+        _check(self._L.ref_pft_apply_2d(self.h, _cptr(z), z.shape[0], z.shape[1], _cptr(out)))
         return out
 
     def adjoint(self, band):
         """pft_adjoint_2d (pft.cpp:174-226)."""
         band = _c128(band)
         out = np.zeros((self.n1, self.n2), np.complex128)
-        _check(lib().ref_pft_adjoint_2d(self.h, _cptr(band), band.shape[0], band.shape[1],
+        _check(self._L.ref_pft_adjoint_2d(self.h, _cptr(band), band.shape[0], band.shape[1],
                                         _cptr(out)))
         return out
 
@@ -153,7 +174,7 @@ class RefPlan:
         b = z.shape[0]
         band = np.zeros((b, 2 * self.mt1, 2 * self.mt2), np.complex128) if want else None
         back = np.zeros_like(z) if want else None
-        _check(lib().ref_pft_fwd_adj_batch(
+        _check(self._L.ref_pft_fwd_adj_batch(
             self.h, _cptr(z), b, self.n1, self.n2,
             _cptr(band) if want else None, _cptr(back) if want else None, threads))
         return band, back
@@ -162,7 +183,7 @@ class RefPlan:
         """band_residual (solver.cpp:61-69)."""
         e, d = _c128(exit_wave), _f64(dcrop)
         out = np.zeros_like(e)
-        _check(lib().ref_band_residual(self.h, _cptr(e), e.shape[0], e.shape[1], _cptr(d),
+        _check(self._L.ref_band_residual(self.h, _cptr(e), e.shape[0], e.shape[1], _cptr(d),
                                        d.shape[0], d.shape[1], _cptr(out)))
         return out
 

@@ -23,7 +23,7 @@ EXPORTS = (
     "pftg_plan_tables",
     "pftg_apply_2d_dev", "pftg_adjoint_2d_dev", "pftg_apply_2d_host", "pftg_adjoint_2d_host",
     "pftg_band_residual_dev",
-    "pftg_fft2_dev", "pftg_project_modulus_dev", "pftg_crop_centered_dev",
+    "pftg_fft2_dev", "pftg_fft2_host", "pftg_project_modulus_dev", "pftg_crop_centered_dev",
     "pftg_window_slice_dev", "pftg_set_window_dev", "pftg_pie_object_update_dev",
     "pftg_epie_probe_update_dev", "pftg_evaluate_dev",
     "pftg_solver_create", "pftg_solver_run", "pftg_solver_trace", "pftg_solver_result",
@@ -80,6 +80,7 @@ def lib():
     L.pftg_adjoint_2d_host.argtypes = [vp, C.c_int, vp, vp, sz]
     L.pftg_band_residual_dev.argtypes = [vp, C.c_int, vp, vp, vp, sz, vp]
     L.pftg_fft2_dev.argtypes = [C.c_int, vp, vp, sz, sz, sz, C.c_int, vp]
+    L.pftg_fft2_host.argtypes = [C.c_int, vp, vp, sz, sz, sz, C.c_int]
     L.pftg_project_modulus_dev.argtypes = [C.c_int, vp, vp, vp, sz, sz, sz, vp]
     L.pftg_crop_centered_dev.argtypes = [C.c_int, vp, vp, sz, sz, sz, sz, sz, vp]
     L.pftg_window_slice_dev.argtypes = [C.c_int, vp, sz, sz, vp, sz, sz, i64p, sz, vp]

@@ -937,6 +937,27 @@ int pftg_fft2_dev(int dtype, const void* z, void* out, size_t rows, size_t cols,
   });
 }
 
+int pftg_fft2_host(int dtype, const void* z, void* out, size_t rows, size_t cols, size_t batch, int inverse) {
+  return guarded([&] {
+    check_dtype(dtype);
+    if (rows == 0 || cols == 0) throw std::invalid_argument("fast_fft2: empty field");
+    check_fft_len(rows);
+    check_fft_len(cols);
+    if (batch == 0) return;
+    ensure_device();
+    const std::size_t n = rows * cols;
+    auto run = [&](auto tag) {
+      using R = decltype(tag);
+      const std::size_t chunk = host_chunk(batch, sizeof(Cx<R>) * n);
+      host_pipeline<R>(batch, n, n, z, out, chunk, [&](Cx<R>* din, Cx<R>* dout, std::size_t nbat, cudaStream_t s) {
+        fft2_dev<R>(din, dout, rows, cols, nbat, inverse, s);
+      });
+    };
+    if (dtype == PFTG_C64) run(float{});
+    else run(double{});
+  });
+}
+
 int pftg_project_modulus_dev(int dtype, const void* exit_wave, const void* d, void* out, size_t rows, size_t cols,
                              size_t batch, void* stream) {
   return guarded([&] {

@@ -126,3 +126,21 @@ def test_plan_from_tables_equals_file_plan(tmp_path, ref):
     assert (tmp_path / "ours.plan").read_bytes() == (tmp_path / "ref.plan").read_bytes()
     with pytest.raises(ValueError, match="p must divide n"):
         P.PftPlan2D.from_tables(250, 32, 32, B1[:7], W1, 128, 16, 16, B2, W2)
+
+
+def test_facade_library_links_gpu_operators():
+    """oracle/_ref/libptycho_facade.so (the reference built verbatim + the C++
+    façade) defines the four replaced operators itself and takes them from
+    libpftg: the renamed CPU versions are present but unused."""
+    import subprocess
+    from oracle import ref
+    if not ref.FACADE_PATH.exists():
+        pytest.skip("façade build missing (make -C oracle)")
+    syms = subprocess.run(["nm", "-DC", str(ref.FACADE_PATH)], capture_output=True, text=True).stdout
+    for f in ("ptycho::pft::pft_apply_2d(", "ptycho::pft::pft_adjoint_2d(", "ptycho::fast_fft2(",
+              "ptycho::fast_ifft2(", "ptycho::pft::cpu_pft_apply_2d(", "ptycho::cpu_fast_fft2("):
+        assert f in syms, f
+    for f in ("pftg_plan_from_tables", "pftg_apply_2d_host", "pftg_adjoint_2d_host", "pftg_fft2_host"):
+        assert f" U {f}" in syms, f
+    deps = subprocess.run(["ldd", str(ref.FACADE_PATH)], capture_output=True, text=True).stdout
+    assert "libpftg.so" in deps
