@@ -160,6 +160,33 @@ int pftg_evaluate_dev(int dtype, const void* frame, size_t fr, size_t fc, const 
                       const void* d, const pftg_plan* plan, const void* dcrop, double* fft_sum,
                       double* band_sum, void* stream);
 
+/* ---- measurement simulator (simulate.hpp:33-42) ------------------------------ */
+/* simulate (simulate.cpp:48-65): d[j] = |FFT2(probe .* window_j)| for the npos
+ * windows at HOST int64 offsets (r0, c0) of the fr x fc frame; d is real
+ * [npos][wr][wc] (float for PFTG_C64, double for PFTG_C128). Windows are
+ * bounds-checked (PFTG_ERANGE). Synchronizes the stream. build_cropped
+ * (simulate.cpp:81-89) is pftg_crop_centered_dev over the same d. */
+int pftg_simulate_dev(int dtype, const void* frame, size_t fr, size_t fc, const void* probe, size_t wr, size_t wc,
+                      const int64_t* offsets, size_t npos, void* d, void* stream);
+/* add_poisson_noise (simulate.cpp:67-79): d <- sqrt(Poisson(scale d^2) / scale)
+ * over n real elements, in place. Same law as the reference; the random stream
+ * is counter-based (Philox-4x32-10 keyed by seed, counter = element index;
+ * inversion for lambda < 10, Hoermann PTRS above), not libstdc++'s: results
+ * are reproducible for a given seed and independent of the launch shape.
+ * PFTG_EINVAL unless scale > 0. */
+int pftg_add_poisson_noise_dev(int dtype, void* d, size_t n, double scale, uint64_t seed, void* stream);
+
+/* ---- per-sweep reconstruction metrics (metrics.hpp:11-34) -------------------- */
+/* fill_metrics (solver.cpp:141-160) of a reconstruction x against the truth ref,
+ * both rows x cols complex regions with leading dimensions ld_x / ld_ref
+ * (elements; e.g. the object region inside a frame): out[8] = relative_error,
+ * relative_error_aligned, relative_error(|x|), relative_error(arg x),
+ * ssim(|x|), ssim(arg x), psnr(|x|), psnr(arg x), ranges = dynamic_range of
+ * the truth (metrics.cpp:60-143). FP64 accumulation, deterministic.
+ * Synchronizes the stream. PFTG_EINVAL for regions under 11 x 11 (ssim). */
+int pftg_fill_metrics_dev(int dtype, const void* x, size_t ld_x, const void* ref, size_t ld_ref, size_t rows,
+                          size_t cols, double* out, void* stream);
+
 /* ---- device-resident hybrid_solve (solver.hpp:87-90) ------------------------ */
 typedef struct pftg_solver_config {
   int pft_sweeps, fft_sweeps;      /* SolverConfig (solver.hpp:21-37) */

@@ -82,6 +82,8 @@ def lib():
         L.ref_scope_table_compute.argtypes = [C.c_char_p, dp, C.c_int, C.c_int]
         L.ref_scope_table_single.argtypes = [C.c_char_p, C.c_double, C.c_int, C.c_double]
         L.ref_min_degree.argtypes = [C.c_char_p, C.c_double, C.c_double, C.POINTER(C.c_int)]
+        L.ref_fill_metrics.argtypes = [dp, dp, szt, szt, dp]
+        L.ref_shim_gemm_gflops.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp]
         _libs[path] = L
     return _libs[path]
 
@@ -320,3 +322,30 @@ def min_degree(table_path, eps, target):
     r = C.c_int(0)
     _check(lib().ref_min_degree(str(table_path).encode(), eps, target, C.byref(r)))
     return r.value
+
+
+def fill_metrics(x, truth):
+    """fill_metrics (solver.cpp:141-160) via metrics.cpp:60-143: [rel_err,
+    rel_err_aligned, rel_err_mag, rel_err_phase, ssim_mag, ssim_phase, psnr_mag,
+    psnr_phase]."""
+    x, t = _c128(x), _c128(truth)
+    out = np.zeros(8)
+    _check(lib().ref_fill_metrics(_cptr(x), _cptr(t), x.shape[0], x.shape[1], _cptr(out)))
+    return out
+
+
+def shim_gemm_gflops(m=10, k=32, n=1024, reps=200):
+    """GFLOP/s of the Eigen shim's complex GEMM on the PFT stage-A shape."""
+    g = C.c_double(0)
+    _check(lib().ref_shim_gemm_gflops(m, k, n, reps, C.byref(g)))
+    return g.value
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"

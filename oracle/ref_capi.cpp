@@ -8,8 +8,12 @@
 //   ptycho::{fast_fft2, fast_ifft2, naive_dft2, crop_centered}
 //   ptycho::{band_residual, project_modulus, objective_value, hybrid_solve}
 //   ptycho::minimax::{best_approx, ScopeTable}
+//   ptycho::{relative_error, relative_error_aligned, ssim, psnr, dynamic_range} (fill_metrics set)
 // Complex arrays cross the boundary as interleaved (re, im) float64, row-major,
 // exactly the ComplexField layout (field.hpp:37-65).
+#include <Eigen/Dense>
+
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -19,6 +23,7 @@
 
 #include "ptycho/fft.hpp"
 #include "ptycho/field.hpp"
+#include "ptycho/metrics.hpp"
 #include "ptycho/minimax.hpp"
 #include "ptycho/pft.hpp"
 #include "ptycho/scan.hpp"
@@ -370,5 +375,46 @@ extern "C" int ref_pft_fwd_adj_batch(void* h, const double* z, std::size_t batch
     for (auto& th : pool) th.join();
     for (const auto& e : errs)
       if (!e.empty()) throw std::runtime_error(e);
+  });
+}
+
+// The per-sweep metrics row of hybrid_solve's trace (fill_metrics,
+// solver.cpp:141-160) for reconstruction x vs truth t (both rows x cols):
+// out = rel_err, rel_err_aligned, rel_err_mag, rel_err_phase, ssim_mag,
+// ssim_phase, psnr_mag, psnr_phase.
+extern "C" int ref_fill_metrics(const double* x, const double* t, std::size_t rows, std::size_t cols,
+                                double* out) {
+  return guarded([&] {
+    const ComplexField xf = to_field(x, rows, cols), tf = to_field(t, rows, cols);
+    const RealField xm = magnitude(xf), xp = phase(xf), tm = magnitude(tf), tp = phase(tf);
+    const double rm = dynamic_range(tm), rp = dynamic_range(tp);
+    out[0] = relative_error(xf, tf);
+    out[1] = relative_error_aligned(xf, tf);
+    out[2] = relative_error(xm, tm);
+    out[3] = relative_error(xp, tp);
+    out[4] = ssim(xm, tm, rm);
+    out[5] = ssim(xp, tp, rp);
+    out[6] = psnr(xm, tm, rm);
+    out[7] = psnr(xp, tp, rp);
+  });
+}
+
+// Throughput of the Eigen shim's complex GEMM (oracle/shim/Eigen/Dense) on an
+// m x k x n product -- reported beside the CPU baseline so the reader can
+// judge the shim against a real Eigen build (the reference's stage A is
+// B1^T (r x q) * Z_blk (q x n): m = r, k = q).
+extern "C" int ref_shim_gemm_gflops(int m, int k, int n, int reps, double* gflops) {
+  return guarded([&] {
+    using RowMat = Eigen::Matrix<cdouble, Eigen::Dynamic, Eigen::Dynamic, Eigen::RowMajor>;
+    RowMat A(k, m), B(k, n), T(m, n);
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < m; ++j) A(i, j) = cdouble(0.5 + 0.01 * i, -0.25 + 0.02 * j);
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < n; ++j) B(i, j) = cdouble(0.001 * j, 0.003 * i);
+    T.noalias() = A.transpose() * B;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < reps; ++r) T.noalias() = A.transpose() * B;
+    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *gflops = 8.0 * m * k * n * reps / s / 1e9;
   });
 }

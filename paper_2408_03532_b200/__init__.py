@@ -12,3 +12,5 @@ from .solver import (  # noqa: F401
     ReconResult, Solver, SolverConfig, epie_probe_update, evaluate, hybrid_solve,
     objective_value, pie_object_update, project_modulus, set_window, solve_epie, solve_pie,
     window_slice)
+from .simulate import add_poisson_noise, build_cropped, photon_scale, simulate  # noqa: F401,E402
+from .metrics import Metrics, fill_metrics, relative_error, relative_error_aligned  # noqa: F401,E402

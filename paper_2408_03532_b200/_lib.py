@@ -26,6 +26,7 @@ EXPORTS = (
     "pftg_fft2_dev", "pftg_fft2_host", "pftg_project_modulus_dev", "pftg_crop_centered_dev",
     "pftg_window_slice_dev", "pftg_set_window_dev", "pftg_pie_object_update_dev",
     "pftg_epie_probe_update_dev", "pftg_evaluate_dev",
+    "pftg_simulate_dev", "pftg_add_poisson_noise_dev", "pftg_fill_metrics_dev",
     "pftg_solver_create", "pftg_solver_run", "pftg_solver_trace", "pftg_solver_result",
     "pftg_solver_device_state", "pftg_solver_free",
 )
@@ -89,6 +90,9 @@ def lib():
     L.pftg_epie_probe_update_dev.argtypes = [C.c_int, vp, vp, vp, sz, C.c_double, C.c_int, vp]
     L.pftg_evaluate_dev.argtypes = [C.c_int, vp, sz, sz, vp, sz, sz, i64p, sz, sz, sz, vp, vp, vp,
                                     dp, dp, vp]
+    L.pftg_simulate_dev.argtypes = [C.c_int, vp, sz, sz, vp, sz, sz, i64p, sz, vp, vp]
+    L.pftg_add_poisson_noise_dev.argtypes = [C.c_int, vp, sz, C.c_double, C.c_uint64, vp]
+    L.pftg_fill_metrics_dev.argtypes = [C.c_int, vp, sz, vp, sz, sz, sz, dp, vp]
     L.pftg_solver_create.argtypes = [C.c_int, vp, sz, sz, vp, sz, sz, i64p, sz, vp,
                                      C.POINTER(SolverConfigC), vp, C.POINTER(vp)]
     L.pftg_solver_run.argtypes = [vp, C.c_int]

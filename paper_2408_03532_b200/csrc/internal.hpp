@@ -140,6 +140,7 @@ struct Scratch {
 };
 
 void ensure_device();
+void set_error(const std::string& m);  // thread-local message behind pftg_last_error (capi.cu)
 void check_fft_len(std::size_t n);
 
 // Optional per-kernel timing (pftg_profile_*): CUDA events recorded around

@@ -13,8 +13,9 @@ Decisions (stated in DESIGN.md):
   * data: d = |FFT2(probe * patch)| (simulate.cpp:48-65) with Poisson noise at
     a global scale s = photons / mean_j sum_k d_jk^2 (add_poisson_noise,
     simulate.cpp:67-79): d <- sqrt(Poisson(s d^2) / s).
-Generation runs on the GPU with torch (cuFFT, torch.poisson) -- it builds the
-inputs, it is not the measured path.
+Object and probe are generated with torch on the GPU; the measurements come
+from the package's own GPU simulator (paper_2408_03532_b200.simulate, F1) --
+input generation, outside every timed region.
 """
 from __future__ import annotations
 
@@ -77,17 +78,16 @@ def raster_offsets(n, w, K, jitter, seed):
     return np.array(offs, np.int64)
 
 
-def simulate(obj, probe, offsets, photons, gen, chunk=64):
-    w = probe.shape[0]
-    N = len(offsets)
-    d = torch.empty((N, w, w), dtype=torch.float64, device=obj.device)
-    for c0 in range(0, N, chunk):
-        idx = offsets[c0:c0 + chunk]
-        patches = torch.stack([obj[r:r + w, c:c + w] for r, c in idx]).to(torch.complex128)
-        d[c0:c0 + len(idx)] = torch.fft.fft2(patches * probe.to(torch.complex128)).abs()
+def simulate(obj, probe, offsets, photons, seed):
+    """Measurements through the package's own GPU simulator (F1): d = |FFT2(probe
+    .* window)| in complex128 (simulate.cpp:48-65), then Poisson noise at the
+    global photon scale (add_poisson_noise, simulate.cpp:67-79; counter-based
+    stream, include/pftg.h)."""
+    from .simulate import add_poisson_noise, photon_scale
+    from .simulate import simulate as gpu_simulate
+    d = gpu_simulate(obj.to(torch.complex128).contiguous(), probe.to(torch.complex128).contiguous(), offsets)
     if photons:
-        s = photons / float((d * d).sum(dim=(1, 2)).mean())
-        d = torch.sqrt(torch.poisson(s * d * d, generator=gen) / s)
+        add_poisson_noise(d, photon_scale(d, photons), seed)
     return d
 
 
@@ -99,7 +99,7 @@ def make_problem(name, device="cuda", seed=0, dtype=torch.complex64, npos=None) 
     offs = raster_offsets(n, w, K, 2, seed)
     if npos is not None:
         offs = offs[:npos]
-    d = simulate(obj, probe, offs, photons, gen)
+    d = simulate(obj, probe, offs, photons, 0x5EED + seed)
     return Problem(obj, probe, offs, d.to(torch.float32 if dtype == torch.complex64 else torch.float64), photons)
 
 

@@ -247,6 +247,23 @@ class Solver:
         return ReconResult(frame, probe, obj[:len(wall)][:k], wall[:k], k, bool(fl.value & 2),
                            bool(fl.value & 1))
 
+    def metrics(self, truth):
+        """fill_metrics (solver.cpp:141-160) of the live frame against ``truth``
+        (a frame-shaped CUDA tensor of the solver's dtype), on the device, between
+        sweeps: the per-sweep metric row of the reference's trace. Returns
+        paper_2408_03532_b200.metrics.Metrics."""
+        from .metrics import Metrics
+        fptr, pptr = C.c_void_p(), C.c_void_p()
+        check(lib().pftg_solver_device_state(self._h, C.byref(fptr), C.byref(pptr)))
+        want = torch.complex64 if self.code == PFTG_C64 else torch.complex128
+        if not isinstance(truth, torch.Tensor) or not truth.is_cuda or truth.dtype != want or \
+                tuple(truth.shape) != tuple(self.shapes[0]) or not truth.is_contiguous():
+            raise ValueError(f"metrics: truth must be a contiguous {want} CUDA tensor of shape {self.shapes[0]}")
+        fr, fc = self.shapes[0]
+        out = (C.c_double * 8)()
+        check(lib().pftg_fill_metrics_dev(self.code, fptr, fc, _ptr(truth), fc, fr, fc, out, None))
+        return Metrics(*[float(v) for v in out])
+
     def __del__(self):
         try:
             lib().pftg_solver_free(self._h)
