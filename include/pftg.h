@@ -187,6 +187,24 @@ int pftg_add_poisson_noise_dev(int dtype, void* d, size_t n, double scale, uint6
 int pftg_fill_metrics_dev(int dtype, const void* x, size_t ld_x, const void* ref, size_t ld_ref, size_t rows,
                           size_t cols, double* out, void* stream);
 
+/* ---- 1-D PFT (pft.hpp:25-38, 60-63; pft.cpp:33-101, 266-334) ---------------- */
+typedef struct pftg_plan1d pftg_plan1d; /* pft::PftPlan1D (pft.hpp:25-31) */
+/* pft::pft_plan_1d (pft.hpp:33-34): r = min_degree(eps, mt/p), same tables and errors. */
+int pftg_plan_1d(const pftg_table* t, size_t n, size_t mt, size_t p, double eps, pftg_plan1d** out);
+/* In-memory PftPlan1D (B: q x r, W: (2mt+1) x r, interleaved complex128). */
+int pftg_plan1d_from_tables(size_t n, size_t p, size_t mt, int r, const double* B, const double* W, double eps,
+                            pftg_plan1d** out);
+int pftg_plan1d_load(const char* path, pftg_plan1d** out);        /* load_plan_1d (pft.hpp:62) */
+int pftg_plan1d_save(const pftg_plan1d* plan, const char* path);  /* save_plan (pft.hpp:60) */
+int pftg_plan1d_info(const pftg_plan1d* plan, int64_t* info);     /* n p q mt r */
+int pftg_plan1d_tables(const pftg_plan1d* plan, double* B, double* W);
+void pftg_plan1d_free(pftg_plan1d* plan);
+/* pft::pft_apply_1d (pft.hpp:38): z [batch][n] -> out [batch][2mt+1], DC at index mt
+ * (the +mt edge is kept in 1-D). Device buffers, stream-ordered. */
+int pftg_apply_1d_dev(const pftg_plan1d* plan, int dtype, const void* z, void* out, size_t batch, void* stream);
+/* The same from host buffers (synchronous). */
+int pftg_apply_1d_host(const pftg_plan1d* plan, int dtype, const void* z, void* out, size_t batch);
+
 /* ---- device-resident hybrid_solve (solver.hpp:87-90) ------------------------ */
 typedef struct pftg_solver_config {
   int pft_sweeps, fft_sweeps;      /* SolverConfig (solver.hpp:21-37) */
@@ -196,6 +214,7 @@ typedef struct pftg_solver_config {
   int shuffled;                    /* VisitOrder::shuffled */
   uint64_t seed;
   int objective_every;             /* evaluate objective every k sweeps (1 = reference) */
+  double tv_lambda_mag, tv_lambda_phase; /* per-sweep TV step on |z| / arg z (solver.cpp:264-279) */
 } pftg_solver_config;
 
 /* Copies the HOST inputs to the device: frame [fr][fc], probe [wr][wc],

@@ -113,6 +113,17 @@ def plan_1d(n, mt, p, eps, table) -> Axis:
     return Axis(n, p, q, mt, r, eps, B, W)
 
 
+def pft_apply_1d(a: Axis, z, dtype=np.complex128):
+    """pft_apply_1d (pft.cpp:78-101): C = reshape(z, p x q) B, column FFTs over
+    k (FFTW_FORWARD), out[i] = sum_j C[(i - mt) mod p, j] W[i, j], i in [0, 2mt]."""
+    ct = _ctype(dtype)
+    z = np.asarray(z).astype(ct).reshape(a.p, a.q)
+    Cm = z @ a.B.astype(ct)
+    Cm = np.fft.fft(Cm, axis=0).astype(ct)
+    u = (np.arange(2 * a.mt + 1) - a.mt) % a.p
+    return np.sum(Cm[u, :] * a.W.astype(ct), axis=1)
+
+
 @dataclasses.dataclass
 class Plan2D:
     a1: Axis
@@ -316,10 +327,38 @@ def shuffle_order(order, rng):
         order[i - 1], order[j] = order[j], order[i - 1]
 
 
+def tv_gradient(x):
+    """tv_gradient (solver.cpp:71-87): psi'(t) = t / sqrt(t^2 + 1e-12) over the
+    4-neighbourhood, one-sided at the edges, accumulated in the reference's order."""
+    x = np.asarray(x, np.float64)
+    psi = lambda t: t / np.sqrt(t * t + 1e-6 * 1e-6)  # noqa: E731
+    g = np.zeros_like(x)
+    dv = psi(x[1:, :] - x[:-1, :])  # dv[i] = psi(x[i+1] - x[i])
+    dh = psi(x[:, 1:] - x[:, :-1])
+    g[:-1, :] -= dv
+    g[1:, :] += dv
+    g[:, :-1] -= dh
+    g[:, 1:] += dh
+    return g
+
+
+def tv_step(frame, lam_mag, lam_phase, step):
+    """The per-sweep TV block of hybrid_solve (solver.cpp:264-279): magnitude /
+    phase (phase of 0 is 0, field.cpp:74-87), gradient steps, from_polar."""
+    mag = np.abs(frame).astype(np.float64)
+    ph = np.where(frame == 0, 0.0, np.angle(frame)).astype(np.float64)
+    if lam_mag > 0:
+        mag = mag - lam_mag * step * tv_gradient(mag)
+    if lam_phase > 0:
+        ph = ph - lam_phase * step * tv_gradient(ph)
+    return (mag * np.cos(ph) + 1j * (mag * np.sin(ph))).astype(frame.dtype)
+
+
 def hybrid_solve(frame, probe, offsets, d, *, pft_sweeps, fft_sweeps, table=None, beta=1.0,
                  gamma=1.0, beta_pft=1e-3, gamma_pft=1e-3, eps_pft=1e-3, mt=0, p=0, blind=False,
-                 shuffled=False, seed=0, dtype=np.complex128):
-    """hybrid_solve (solver.cpp:173-302), sequential order, no TV, tol = 0.
+                 shuffled=False, seed=0, dtype=np.complex128, tv_mag=0.0, tv_phase=0.0):
+    """hybrid_solve (solver.cpp:173-302), tol = 0; TV (264-279) when tv_mag /
+    tv_phase > 0.
     ``dtype=np.complex64`` is oracle<float>: frame, probe, measurements and every
     operator in single precision (the reference of the complex64 ePIE tolerance).
 
@@ -359,5 +398,7 @@ def hybrid_solve(frame, probe, offsets, d, *, pft_sweeps, fft_sweeps, table=None
                 if blind:
                     probe = epie_probe_update(probe, zj, project_modulus(probe * zj, d[j], ct), gamma)
             frame[r0:r0 + wr, c0:c0 + wc] = zj
+        if tv_mag > 0 or tv_phase > 0:
+            frame = tv_step(frame, tv_mag, tv_phase, float(beta_pft if band_stage else beta))
         objs.append(objective_value(frame, probe, offsets, d, ct))
     return frame, probe, np.array(objs)

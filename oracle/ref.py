@@ -64,6 +64,15 @@ def lib():
         L.ref_plan_info.argtypes = [vp, i64p]
         L.ref_plan_tables.argtypes = [vp, C.c_int, dp, dp]
         L.ref_pft_apply_2d.argtypes = [vp, dp, szt, szt, dp]
+        L.ref_plan1d_create.restype = vp
+        L.ref_plan1d_create.argtypes = [C.c_char_p, szt, szt, szt, C.c_double]
+        L.ref_plan1d_load.restype = vp
+        L.ref_plan1d_load.argtypes = [C.c_char_p]
+        L.ref_plan1d_save.argtypes = [vp, C.c_char_p]
+        L.ref_plan1d_free.argtypes = [vp]
+        L.ref_plan1d_info.argtypes = [vp, i64p]
+        L.ref_plan1d_tables.argtypes = [vp, dp, dp]
+        L.ref_pft_apply_1d.argtypes = [vp, dp, szt, dp]
         L.ref_pft_adjoint_2d.argtypes = [vp, dp, szt, szt, dp]
         L.ref_pft_fwd_adj_batch.argtypes = [vp, dp, szt, szt, szt, dp, dp, C.c_int]
         for f in ("ref_fast_fft2", "ref_fast_ifft2", "ref_naive_dft2", "ref_naive_idft2"):
@@ -190,6 +199,52 @@ class RefPlan:
         return out
 
 
+class RefPlan1D:
+    """Handle on a reference ``PftPlan1D`` (pft.hpp:25-31)."""
+
+    def __init__(self, handle):
+        if not handle:
+            _check(1)
+        self._L = lib()
+        self.h = C.c_void_p(handle)
+        info = np.zeros(5, np.int64)
+        self._L.ref_plan1d_info(self.h, info.ctypes.data_as(C.POINTER(C.c_int64)))
+        self.n, self.p, self.q, self.mt, self.r = (int(v) for v in info)
+
+    @classmethod
+    def create(cls, table_path, n, mt, p, eps):
+        """pft_plan_1d (pft.cpp:33-76)."""
+        return cls(lib().ref_plan1d_create(str(table_path).encode(), n, mt, p, eps))
+
+    @classmethod
+    def load(cls, plan_path):
+        """load_plan_1d (pft.cpp:310-334)."""
+        return cls(lib().ref_plan1d_load(str(plan_path).encode()))
+
+    def save(self, plan_path):
+        """save_plan(PftPlan1D) (pft.cpp:266-275)."""
+        _check(self._L.ref_plan1d_save(self.h, str(plan_path).encode()))
+
+    def tables(self):
+        B = np.zeros((self.q, self.r), np.complex128)
+        W = np.zeros((2 * self.mt + 1, self.r), np.complex128)
+        self._L.ref_plan1d_tables(self.h, _cptr(B), _cptr(W))
+        return B, W
+
+    def __del__(self):
+        try:
+            self._L.ref_plan1d_free(self.h)
+        except Exception:
+            pass
+
+    def apply(self, z):
+        """pft_apply_1d (pft.cpp:78-101): 2mt+1 band entries, DC at index mt."""
+        z = _c128(z).reshape(-1)
+        out = np.zeros(2 * self.mt + 1, np.complex128)
+        _check(self._L.ref_pft_apply_1d(self.h, _cptr(z), z.shape[0], _cptr(out)))
+        return out
+
+
 def _unary(fname, z):
     z = _c128(z)
     out = np.zeros_like(z)
@@ -278,11 +333,11 @@ def add_poisson_noise(d, scale, seed):
 
 def hybrid_solve(frame, probe, offsets, d, *, pft_sweeps, fft_sweeps, beta=1.0, gamma=1.0,
                  beta_pft=1e-3, gamma_pft=1e-3, eps_pft=1e-3, tol=0.0, mt=0, p=0,
-                 blind=False, shuffled=False, seed=0, table_path=None):
+                 blind=False, shuffled=False, seed=0, table_path=None, tv_mag=0.0, tv_phase=0.0):
     """hybrid_solve (solver.cpp:173-302). Returns (frame, probe, objectives, walls, flags)."""
     f, pr = _c128(frame).copy(), _c128(probe).copy()
     o, d = _i64(offsets), _f64(d)
-    cfg_d = np.array([beta, gamma, beta_pft, gamma_pft, eps_pft, tol, 0.0, 0.0])
+    cfg_d = np.array([beta, gamma, beta_pft, gamma_pft, eps_pft, tol, tv_mag, tv_phase])
     cfg_i = np.array([pft_sweeps, fft_sweeps, mt, mt, p, p, int(blind), int(shuffled), seed],
                      np.int64)
     total = pft_sweeps + fft_sweeps

@@ -213,6 +213,61 @@ int ref_pft_adjoint_2d(void* h, const double* band, std::size_t m1, std::size_t 
 int ref_pft_fwd_adj_batch(void* h, const double* z, std::size_t batch, std::size_t n1,
                           std::size_t n2, double* band_out, double* z_out, int threads);
 
+// ---- 1-D plans and apply (pft.hpp:25-38, 60-63) ----
+struct Plan1DHandle {
+  pft::PftPlan1D plan;
+};
+
+void* ref_plan1d_create(const char* table_path, std::size_t n, std::size_t mt, std::size_t p, double eps) {
+  Plan1DHandle* h = nullptr;
+  const int rc = guarded([&] {
+    const auto t = minimax::ScopeTable::load(table_path);
+    auto hp = std::make_unique<Plan1DHandle>();
+    hp->plan = pft::pft_plan_1d(n, mt, p, eps, t);
+    h = hp.release();
+  });
+  return rc == 0 ? h : nullptr;
+}
+
+void* ref_plan1d_load(const char* plan_path) {
+  Plan1DHandle* h = nullptr;
+  const int rc = guarded([&] {
+    auto hp = std::make_unique<Plan1DHandle>();
+    hp->plan = pft::load_plan_1d(plan_path);
+    h = hp.release();
+  });
+  return rc == 0 ? h : nullptr;
+}
+
+int ref_plan1d_save(void* h, const char* plan_path) {
+  return guarded([&] { pft::save_plan(plan_path, static_cast<Plan1DHandle*>(h)->plan); });
+}
+
+void ref_plan1d_free(void* h) { delete static_cast<Plan1DHandle*>(h); }
+
+// info[5] = n p q mt r
+void ref_plan1d_info(void* h, std::int64_t* info) {
+  const auto& a = static_cast<Plan1DHandle*>(h)->plan;
+  info[0] = static_cast<std::int64_t>(a.n);
+  info[1] = static_cast<std::int64_t>(a.p);
+  info[2] = static_cast<std::int64_t>(a.q);
+  info[3] = static_cast<std::int64_t>(a.mt);
+  info[4] = a.r;
+}
+
+void ref_plan1d_tables(void* h, double* B, double* W) {
+  const auto& a = static_cast<Plan1DHandle*>(h)->plan;
+  from_field(a.B, B);
+  from_field(a.W, W);
+}
+
+int ref_pft_apply_1d(void* h, const double* z, std::size_t n, double* out) {
+  return guarded([&] {
+    const auto band = pft::pft_apply_1d(static_cast<Plan1DHandle*>(h)->plan, to_field(z, n, 1));
+    from_field(band, out);
+  });
+}
+
 // ---- transforms (fft.hpp:9-30) ----
 int ref_fast_fft2(const double* z, std::size_t r, std::size_t c, double* out) {
   return guarded([&] { from_field(fast_fft2(to_field(z, r, c)), out); });

@@ -27,6 +27,8 @@ EXPORTS = (
     "pftg_window_slice_dev", "pftg_set_window_dev", "pftg_pie_object_update_dev",
     "pftg_epie_probe_update_dev", "pftg_evaluate_dev",
     "pftg_simulate_dev", "pftg_add_poisson_noise_dev", "pftg_fill_metrics_dev",
+    "pftg_plan_1d", "pftg_plan1d_from_tables", "pftg_plan1d_load", "pftg_plan1d_save", "pftg_plan1d_info",
+    "pftg_plan1d_tables", "pftg_plan1d_free", "pftg_apply_1d_dev", "pftg_apply_1d_host",
     "pftg_solver_create", "pftg_solver_run", "pftg_solver_trace", "pftg_solver_result",
     "pftg_solver_device_state", "pftg_solver_free",
 )
@@ -44,6 +46,7 @@ class SolverConfigC(C.Structure):
         ("mt1", C.c_int64), ("mt2", C.c_int64), ("p1", C.c_int64), ("p2", C.c_int64),
         ("blind", C.c_int), ("shuffled", C.c_int), ("seed", C.c_uint64),
         ("objective_every", C.c_int),
+        ("tv_lambda_mag", C.c_double), ("tv_lambda_phase", C.c_double),
     ]
 
 
@@ -93,6 +96,16 @@ def lib():
     L.pftg_simulate_dev.argtypes = [C.c_int, vp, sz, sz, vp, sz, sz, i64p, sz, vp, vp]
     L.pftg_add_poisson_noise_dev.argtypes = [C.c_int, vp, sz, C.c_double, C.c_uint64, vp]
     L.pftg_fill_metrics_dev.argtypes = [C.c_int, vp, sz, vp, sz, sz, sz, dp, vp]
+    L.pftg_plan_1d.argtypes = [vp, sz, sz, sz, C.c_double, C.POINTER(vp)]
+    L.pftg_plan1d_from_tables.argtypes = [sz, sz, sz, C.c_int, dp, dp, C.c_double, C.POINTER(vp)]
+    L.pftg_plan1d_load.argtypes = [C.c_char_p, C.POINTER(vp)]
+    L.pftg_plan1d_save.argtypes = [vp, C.c_char_p]
+    L.pftg_plan1d_info.argtypes = [vp, i64p]
+    L.pftg_plan1d_tables.argtypes = [vp, dp, dp]
+    L.pftg_plan1d_free.argtypes = [vp]
+    L.pftg_plan1d_free.restype = None
+    L.pftg_apply_1d_dev.argtypes = [vp, C.c_int, vp, vp, sz, vp]
+    L.pftg_apply_1d_host.argtypes = [vp, C.c_int, vp, vp, sz]
     L.pftg_solver_create.argtypes = [C.c_int, vp, sz, sz, vp, sz, sz, i64p, sz, vp,
                                      C.POINTER(SolverConfigC), vp, C.POINTER(vp)]
     L.pftg_solver_run.argtypes = [vp, C.c_int]

@@ -709,7 +709,7 @@ void check_plan(const pftg_plan* p) {
 
 extern "C" {
 
-int pftg_version(void) { return 1; }
+int pftg_version(void) { return 2; }
 
 int pftg_profile_begin(void) {
   return guarded([&] {

@@ -41,5 +41,7 @@ int table_min_degree(const Table& t, double eps, double target);
 Axis plan_1d(std::size_t n, std::size_t mt, std::size_t p, double eps, const Table& table);
 void plan_save(const Axis& a1, const Axis& a2, const std::string& path);
 void plan_load(Axis& a1, Axis& a2, const std::string& path);
+void plan_save_1d(const Axis& a, const std::string& path);
+void plan_load_1d(Axis& a, const std::string& path);
 
 }  // namespace pftg

@@ -207,4 +207,42 @@ void plan_load(Axis& a1, Axis& a2, const std::string& path) {
   }
 }
 
+// 1-D plan files: "pft-plan-1d v1", one un-suffixed axis line, eps, B then W
+// (pft.cpp:266-275 save_plan(PftPlan1D), 310-334 load_plan_1d).
+void plan_save_1d(const Axis& a, const std::string& path) {
+  std::ofstream os(path, std::ios::binary);
+  if (!os) throw std::runtime_error("cannot open " + path + " for writing");
+  os << "pft-plan-1d v1\n";
+  os << "n " << a.n << " p " << a.p << " q " << a.q << " mt " << a.mt << " r " << a.r << "\n";
+  os << "eps " << fmt_eps(a.eps) << "\n---\n";
+  write_block(os, a.B, a.q, a.r);
+  write_block(os, a.W, 2 * a.mt + 1, a.r);
+  if (!os) throw std::runtime_error("write failure on " + path);
+}
+
+void plan_load_1d(Axis& a, const std::string& path) {
+  std::ifstream is(path, std::ios::binary);
+  if (!is) throw std::runtime_error("cannot open " + path);
+  std::string line;
+  if (!std::getline(is, line) || line != "pft-plan-1d v1")
+    throw std::runtime_error(path + " is not a pft-plan-1d v1 file");
+  if (!std::getline(is, line)) throw std::runtime_error("truncated plan " + path);
+  {
+    std::istringstream iss(line);
+    std::string key;
+    if (!(iss >> key >> a.n >> key >> a.p >> key >> a.q >> key >> a.mt >> key >> a.r))
+      throw std::runtime_error("malformed plan axis line in " + path);
+  }
+  if (!std::getline(is, line) || line.rfind("eps ", 0) != 0)
+    throw std::runtime_error("missing eps line in " + path);
+  a.eps = std::stod(line.substr(4));
+  if (!std::getline(is, line) || line != "---") throw std::runtime_error("missing block separator in " + path);
+  std::uint32_t rb, cb, rw, cw;
+  a.B = read_block(is, rb, cb);
+  a.W = read_block(is, rw, cw);
+  if (a.p * a.q != a.n || rb != a.q || cb != static_cast<std::uint32_t>(a.r) || rw != 2 * a.mt + 1 ||
+      cw != static_cast<std::uint32_t>(a.r))
+    throw std::runtime_error("inconsistent plan blocks in " + path);
+}
+
 }  // namespace pftg

@@ -12,7 +12,9 @@
 //    projection of the updated exit wave (253-259);
 //  - per sweep: objective over all positions (287), divergence guards
 //    (291-295) and the relative-change stop (296-299).
-// TV smoothing (264-279) is not on the BASELINE path and is rejected if asked.
+//  - per sweep, when tv_lambda_mag / tv_lambda_phase > 0: one TV gradient
+//    step on |z| and arg z of the whole frame, step lambda * (beta_pft in the
+//    band stage, beta in the FFT stage), recomposed by polar (264-279); k_tv.
 //
 // Each position is 3 (non-blind) or 5 (blind) kernel launches that keep the
 // patch, spectrum and PFT intermediates in L2; a whole sweep is captured once
@@ -105,6 +107,66 @@ __global__ void k_crop_real(const R* __restrict__ d, R* __restrict__ out, int w1
 
 constexpr int kRedBlocks = 296;
 
+// TV step (solver.cpp:71-87 tv_gradient, 264-279): psi'(t) = t / sqrt(t^2 + 1e-6^2)
+// over the 4-neighbourhood with one-sided edges, on mag = |z| and ph = arg z
+// (phase of 0 is 0, field.cpp:80-87), then z = polar(mag - lm g(mag), ph - lp g(ph)).
+// A 32 x 8 tile stages mag / ph with a one-pixel halo in shared memory, so each
+// pixel's atan2 / hypot runs ~1.3 times instead of 5. Out-of-place (out != z).
+template <class R>
+__device__ __forceinline__ R tv_psi(R t) {
+  const R delta = R(1e-6);
+  return t / sqrt(t * t + delta * delta);
+}
+
+template <class R>
+__global__ void __launch_bounds__(256) k_tv(const typename CT<R>::C* __restrict__ z, typename CT<R>::C* __restrict__ out,
+                                            int rows, int cols, R lm, R lp) {
+  __shared__ R sm[10][34], sp[10][34];
+  const int i0 = blockIdx.y * 8, j0 = blockIdx.x * 32;
+  for (int t = threadIdx.y * 32 + threadIdx.x; t < 10 * 34; t += 256) {
+    const int ti = t / 34, tj = t % 34;
+    const int i = i0 + ti - 1, j = j0 + tj - 1;
+    R m = 0, ph = 0;
+    if (i >= 0 && i < rows && j >= 0 && j < cols) {
+      const auto v = z[(long long)i * cols + j];
+      m = hypot(v.x, v.y);
+      ph = (v.x == R(0) && v.y == R(0)) ? R(0) : atan2(v.y, v.x);
+    }
+    sm[ti][tj] = m;
+    sp[ti][tj] = ph;
+  }
+  __syncthreads();
+  const int i = i0 + threadIdx.y, j = j0 + threadIdx.x;
+  if (i >= rows || j >= cols) return;
+  const int a = threadIdx.y + 1, b = threadIdx.x + 1;
+  R gm = 0, gp = 0;
+  if (i + 1 < rows) {
+    gm -= tv_psi(sm[a + 1][b] - sm[a][b]);
+    gp -= tv_psi(sp[a + 1][b] - sp[a][b]);
+  }
+  if (i > 0) {
+    gm += tv_psi(sm[a][b] - sm[a - 1][b]);
+    gp += tv_psi(sp[a][b] - sp[a - 1][b]);
+  }
+  if (j + 1 < cols) {
+    gm -= tv_psi(sm[a][b + 1] - sm[a][b]);
+    gp -= tv_psi(sp[a][b + 1] - sp[a][b]);
+  }
+  if (j > 0) {
+    gm += tv_psi(sm[a][b] - sm[a][b - 1]);
+    gp += tv_psi(sp[a][b] - sp[a][b - 1]);
+  }
+  R m = sm[a][b], ph = sp[a][b];
+  if (lm > R(0)) m -= lm * gm;
+  if (lp > R(0)) ph -= lp * gp;
+  R sn, cs;
+  sincos(ph, &sn, &cs);
+  typename CT<R>::C o;
+  o.x = m * cs;  // std::polar (libstdc++): (rho cos theta, rho sin theta)
+  o.y = m * sn;
+  out[(long long)i * cols + j] = o;
+}
+
 }  // namespace
 
 struct pftg_solver {
@@ -119,6 +181,7 @@ struct pftg_solver {
   void* frame = nullptr;
   void* probe = nullptr;
   void* prev = nullptr;
+  void* tv = nullptr;  // TV step output (frame-sized)
   void* d = nullptr;
   void* dperm = nullptr;
   void* dcrop = nullptr;
@@ -142,7 +205,7 @@ struct pftg_solver {
   ~pftg_solver() {
     for (auto& g : graph)
       if (g) cudaGraphExecDestroy(g);
-    void* bufs[] = {frame, probe, prev, d, dperm, dcrop, doffs, G, Gt, X, X2, Xe, part, red};
+    void* bufs[] = {frame, probe, prev, tv, d, dperm, dcrop, doffs, G, Gt, X, X2, Xe, part, red};
     for (void* b : bufs)
       if (b) cudaFree(b);
     if (st) cudaStreamDestroy(st);
@@ -297,6 +360,16 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
 template <class R>
 void enqueue_sweep(pftg_solver& s, bool band) {
   for (std::size_t t = 0; t < s.npos; ++t) enqueue_position<R>(s, s.order[t], band);
+  if (s.cfg.tv_lambda_mag > 0.0 || s.cfg.tv_lambda_phase > 0.0) {
+    // solver.cpp:264-279: step lambda * step_scale, step_scale = beta_pft (band) or beta (FFT)
+    const double step = band ? s.cfg.beta_pft : s.cfg.beta;
+    const dim3 grid((unsigned)((s.fc + 31) / 32), (unsigned)((s.fr + 7) / 8));
+    k_tv<R><<<grid, dim3(32, 8), 0, s.st>>>(static_cast<const Cx<R>*>(s.frame), static_cast<Cx<R>*>(s.tv),
+                                             (int)s.fr, (int)s.fc, (R)(s.cfg.tv_lambda_mag * step),
+                                             (R)(s.cfg.tv_lambda_phase * step));
+    PFTG_LAUNCH_CHECK();
+    PFTG_CUDA(cudaMemcpyAsync(s.frame, s.tv, sizeof(Cx<R>) * s.fr * s.fc, cudaMemcpyDeviceToDevice, s.st));
+  }
 }
 
 template <class R>
@@ -469,6 +542,7 @@ void create(pftg_solver& s, const void* frame, const void* probe, const int64_t*
   PFTG_CUDA(cudaMemcpyAsync(s.frame, frame, sizeof(Cx<R>) * fn, cudaMemcpyHostToDevice, s.st));
   PFTG_CUDA(cudaMemcpyAsync(s.probe, probe, sizeof(Cx<R>) * pn, cudaMemcpyHostToDevice, s.st));
   if (s.cfg.tol > 0.0) PFTG_CUDA(cudaMalloc(&s.prev, sizeof(Cx<R>) * fn));
+  if (s.cfg.tv_lambda_mag > 0.0 || s.cfg.tv_lambda_phase > 0.0) PFTG_CUDA(cudaMalloc(&s.tv, sizeof(Cx<R>) * fn));
   PFTG_CUDA(cudaMalloc(&s.d, sizeof(R) * pn * s.npos));
   // uploads are ordered on s.st ahead of the kernels that read them
   PFTG_CUDA(cudaMemcpyAsync(s.d, d, sizeof(R) * pn * s.npos, cudaMemcpyHostToDevice, s.st));

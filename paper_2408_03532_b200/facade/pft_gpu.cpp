@@ -6,6 +6,7 @@
 //
 //   ptycho::pft::pft_apply_2d   (pft.hpp:53, pft.cpp:119-172)
 //   ptycho::pft::pft_adjoint_2d (pft.hpp:57, pft.cpp:174-226)
+//   ptycho::pft::pft_apply_1d   (pft.hpp:38, pft.cpp:78-101)
 //   ptycho::fast_fft2           (fft.hpp:18, fft.cpp:175-178)
 //   ptycho::fast_ifft2          (fft.hpp:19, fft.cpp:180-183)
 //
@@ -26,7 +27,8 @@
 // verbatim reference sources): compile with -I<proj/core>/include
 // -I<repo>/include, and compile the reference's pft.cpp / fft.cpp with
 // -Dpft_apply_2d=cpu_pft_apply_2d -Dpft_adjoint_2d=cpu_pft_adjoint_2d
-// -Dfast_fft2=cpu_fast_fft2 -Dfast_ifft2=cpu_fast_ifft2 (or delete those four
+// -Dpft_apply_1d=cpu_pft_apply_1d
+// -Dfast_fft2=cpu_fast_fft2 -Dfast_ifft2=cpu_fast_ifft2 (or delete those five
 // definitions) so this file's definitions are the ones linked.
 #include <map>
 #include <memory>
@@ -111,6 +113,19 @@ ComplexField pft_adjoint_2d(const PftPlan2D& plan, const ComplexField& band) {
   ComplexField out(plan.axis1.n, plan.axis2.n);
   const GpuPlan g = gpu_plan(plan);
   check(pftg_adjoint_2d_host(g.get(), PFTG_C128, band.data(), out.data(), 1));
+  return out;
+}
+
+ComplexField pft_apply_1d(const PftPlan1D& plan, const ComplexField& z) {
+  if (!z.is_vector() || z.rows() != plan.n)
+    throw std::invalid_argument("pft_apply_1d: z must be an n-vector matching the plan");  // pft.cpp:79-80
+  // PftPlan1D has no shared identity to cache on: the GPU plan lives for this call
+  pftg_plan1d* h = nullptr;
+  check(pftg_plan1d_from_tables(plan.n, plan.p, plan.mt, plan.r, reinterpret_cast<const double*>(plan.B.data()),
+                                reinterpret_cast<const double*>(plan.W.data()), plan.eps, &h));
+  std::unique_ptr<pftg_plan1d, void (*)(pftg_plan1d*)> g(h, pftg_plan1d_free);
+  ComplexField out(2 * plan.mt + 1, 1);
+  check(pftg_apply_1d_host(g.get(), PFTG_C128, z.data(), out.data(), 1));
   return out;
 }
 

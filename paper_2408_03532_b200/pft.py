@@ -13,6 +13,9 @@ pft::pft_plan_2d           ``pft_plan_2d(n1, n2, mt1, mt2, p1, p2, eps, table)``
 pft::load_plan_2d/save     ``PftPlan2D.load(path)`` / ``plan.save(path)`` (pft.hpp:60-63)
 pft::pft_apply_2d          ``pft_apply_2d(plan, z)``            (pft.hpp:53)
 pft::pft_adjoint_2d        ``pft_adjoint_2d(plan, band)``       (pft.hpp:57)
+pft::pft_plan_1d           ``pft_plan_1d(n, mt, p, eps, table)`` (pft.hpp:33)
+pft::pft_apply_1d          ``pft_apply_1d(plan, z)``            (pft.hpp:38)
+pft::load_plan_1d/save     ``PftPlan1D.load(path)`` / ``plan.save(path)`` (pft.hpp:60-62)
 fast_fft2 / fast_ifft2     ``fast_fft2(z)`` / ``fast_ifft2(z)`` (fft.hpp:18-19)
 crop_centered              ``crop_centered(d, mt1, mt2)``       (fft.hpp:30)
 =========================  ====================================================
@@ -146,6 +149,85 @@ class PftPlan2D:
             lib().pftg_plan_free(self._h)
         except Exception:
             pass
+
+
+class PftPlan1D:
+    """pft::PftPlan1D (pft.hpp:25-31): immutable 1-D plan."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle)
+        info = np.zeros(5, np.int64)
+        check(lib().pftg_plan1d_info(self._h, info.ctypes.data_as(C.POINTER(C.c_int64))))
+        self.n, self.p, self.q, self.mt, self.r = (int(v) for v in info)
+
+    @property
+    def band_len(self):
+        return 2 * self.mt + 1
+
+    @classmethod
+    def load(cls, path) -> "PftPlan1D":
+        h = C.c_void_p()
+        check(lib().pftg_plan1d_load(str(path).encode(), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_tables(cls, n, p, mt, B, W, eps=0.0) -> "PftPlan1D":
+        B = np.ascontiguousarray(B, np.complex128)
+        W = np.ascontiguousarray(W, np.complex128)
+        r = B.shape[1]
+        if B.shape != (n // p, r) or W.shape != (2 * mt + 1, r):
+            raise ValueError("pftg_plan1d_from_tables: table shapes do not match the plan")
+        dp = C.POINTER(C.c_double)
+        h = C.c_void_p()
+        check(lib().pftg_plan1d_from_tables(n, p, mt, r, B.ctypes.data_as(dp), W.ctypes.data_as(dp), eps,
+                                            C.byref(h)))
+        return cls(h.value)
+
+    def save(self, path) -> None:
+        check(lib().pftg_plan1d_save(self._h, str(path).encode()))
+
+    def tables(self):
+        B = np.zeros((self.q, self.r), np.complex128)
+        W = np.zeros((2 * self.mt + 1, self.r), np.complex128)
+        check(lib().pftg_plan1d_tables(self._h, B.ctypes.data_as(C.POINTER(C.c_double)),
+                                       W.ctypes.data_as(C.POINTER(C.c_double))))
+        return B, W
+
+    def __del__(self):
+        try:
+            lib().pftg_plan1d_free(self._h)
+        except Exception:
+            pass
+
+
+def pft_plan_1d(n, mt, p, eps, table: ScopeTable | None = None) -> PftPlan1D:
+    """pft::pft_plan_1d (pft.hpp:33-34; pft.cpp:33-76)."""
+    table = table or ScopeTable.load()
+    h = C.c_void_p()
+    check(lib().pftg_plan_1d(table._h, n, mt, p, eps, C.byref(h)))
+    return PftPlan1D(h.value)
+
+
+def pft_apply_1d(plan: PftPlan1D, z):
+    """pft::pft_apply_1d: the 2mt+1 centered band entries of the DFT of each
+    n-vector (last axis), DC at index mt (pft.hpp:36-38)."""
+    if isinstance(z, np.ndarray):
+        if z.shape[-1] != plan.n:
+            raise ValueError("pft_apply_1d: z must be an n-vector matching the plan")
+        z = np.ascontiguousarray(z)
+        b = int(np.prod(z.shape[:-1], dtype=np.int64))
+        out = np.empty(z.shape[:-1] + (plan.band_len,), z.dtype)
+        check(lib().pftg_apply_1d_host(plan._h, _dtype_code(z), z.ctypes.data, out.ctypes.data, b))
+        return out
+    z = _dev(z)
+    if z.shape[-1] != plan.n:
+        raise ValueError("pft_apply_1d: z must be an n-vector matching the plan")
+    b = 1
+    for s_ in z.shape[:-1]:
+        b *= int(s_)
+    out = torch.empty(z.shape[:-1] + (plan.band_len,), dtype=z.dtype, device=z.device)
+    check(lib().pftg_apply_1d_dev(plan._h, _dtype_code(z), _ptr(z), _ptr(out), b, _stream()))
+    return out
 
 
 def pft_plan_2d(n1, n2, mt1, mt2, p1, p2, eps, table: ScopeTable | None = None) -> PftPlan2D:

@@ -160,7 +160,7 @@ def objective_value(frame, probe, offsets, d) -> float:
 
 @dataclasses.dataclass
 class SolverConfig:
-    """ptycho::SolverConfig (solver.hpp:21-37); TV is not on the GPU path."""
+    """ptycho::SolverConfig (solver.hpp:21-37)."""
     pft_sweeps: int = 0
     fft_sweeps: int = 50
     beta: float = 1.0
@@ -198,8 +198,6 @@ class Solver:
 
     def __init__(self, d, offsets, probe_init, object_init, cfg: SolverConfig,
                  table: ScopeTable | None = None, dtype=np.complex64):
-        if cfg.tv_lambda_mag > 0 or cfg.tv_lambda_phase > 0:
-            raise ValueError("hybrid_solve: TV smoothing is not part of the GPU path")
         cdt = np.dtype(dtype)
         rdt = np.float32 if cdt == np.complex64 else np.float64
         self.code = PFTG_C64 if cdt == np.complex64 else PFTG_C128
@@ -218,7 +216,8 @@ class Solver:
         self.shapes = (obj.shape, pr.shape)
         c = SolverConfigC(cfg.pft_sweeps, cfg.fft_sweeps, cfg.beta, cfg.gamma, cfg.beta_pft,
                           cfg.gamma_pft, cfg.eps_pft, cfg.tol, cfg.mt1, cfg.mt2, cfg.p1, cfg.p2,
-                          int(cfg.blind), int(cfg.shuffled), cfg.seed, cfg.objective_every)
+                          int(cfg.blind), int(cfg.shuffled), cfg.seed, cfg.objective_every,
+                          cfg.tv_lambda_mag, cfg.tv_lambda_phase)
         h = C.c_void_p()
         check(lib().pftg_solver_create(self.code, obj.ctypes.data, obj.shape[0], obj.shape[1],
                                        pr.ctypes.data, pr.shape[0], pr.shape[1],

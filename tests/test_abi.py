@@ -106,10 +106,12 @@ def test_solver_config_defaults_mirror_reference():
     assert (c.mt1, c.p1, c.tol, c.blind, c.shuffled, c.seed) == (0, 0, 0.0, False, False, 0)
 
 
-def test_tv_is_rejected_not_ignored():
-    with pytest.raises(ValueError, match="TV"):
-        P.Solver(np.zeros((1, 32, 32)), [[0, 0]], np.ones((32, 32)), np.ones((32, 32)),
-                 P.SolverConfig(tv_lambda_mag=1e-3))
+def test_solver_config_struct_carries_tv():
+    """pftg_solver_config ends with the two TV step sizes (solver.hpp:32-33)."""
+    from paper_2408_03532_b200._lib import SolverConfigC
+    names = [f[0] for f in SolverConfigC._fields_]
+    assert names[-2:] == ["tv_lambda_mag", "tv_lambda_phase"]
+    assert P.SolverConfig().tv_lambda_mag == 0.0 and P.SolverConfig().tv_lambda_phase == 0.0
 
 
 def test_plan_from_tables_equals_file_plan(tmp_path, ref):
@@ -144,3 +146,44 @@ def test_facade_library_links_gpu_operators():
         assert f" U {f}" in syms, f
     deps = subprocess.run(["ldd", str(ref.FACADE_PATH)], capture_output=True, text=True).stdout
     assert "libpftg.so" in deps
+
+
+PLANS_1D = [(1024, 64, 64, 1e-7), (4096, 128, 128, 1e-3), (1000, 40, 40, 1e-3), (960, 30, 30, 1e-7),
+            (65536, 64, 64, 1e-3), (512, 64, 16, 1e-1)]
+
+
+@pytest.mark.parametrize("shape", PLANS_1D)
+def test_plan_1d_tables_and_file_match_reference(tmp_path, ref, shape):
+    """pft_plan_1d (pft.cpp:33-76) tables bit-identical; 1-D plan files
+    (pft.cpp:266-275, 310-334) byte-identical both ways."""
+    n, mt, p, eps = shape
+    if (n, mt, p) == (512, 64, 16):
+        pytest.skip("xi = 4 is outside the default table")
+    pl = P.pft_plan_1d(n, mt, p, eps)
+    rp = ref.RefPlan1D.create(DATA / "scope_table_v1.txt", n, mt, p, eps)
+    assert (pl.n, pl.p, pl.q, pl.mt, pl.r) == (rp.n, rp.p, rp.q, rp.mt, rp.r)
+    B, W = pl.tables()
+    Br, Wr = rp.tables()
+    assert np.array_equal(B, Br) and np.array_equal(W, Wr)
+    pl.save(tmp_path / "ours.plan")
+    rp.save(tmp_path / "ref.plan")
+    assert (tmp_path / "ours.plan").read_bytes() == (tmp_path / "ref.plan").read_bytes()
+    back = P.PftPlan1D.load(tmp_path / "ref.plan")
+    assert np.array_equal(back.tables()[1], Wr)
+    assert ref.RefPlan1D.load(tmp_path / "ours.plan").r == pl.r
+    fr = P.PftPlan1D.from_tables(n, p, mt, B, W, eps)
+    assert np.array_equal(fr.tables()[0], Br)
+
+
+def test_plan_1d_errors_mirror_reference(tmp_path):
+    t = P.ScopeTable.load()
+    with pytest.raises(ValueError, match="p must divide n"):
+        P.pft_plan_1d(16, 1, 5, 1e-1, t)
+    with pytest.raises(ValueError, match="q = n/p >= 2"):
+        P.pft_plan_1d(16, 4, 16, 1e-1, t)
+    with pytest.raises(ValueError, match="infeasible"):
+        P.pft_plan_1d(1024, 256, 64, 1e-7, t)
+    bad = tmp_path / "bad.plan"
+    bad.write_text("pft-plan-2d v1\n")
+    with pytest.raises(OSError, match="pft-plan-1d"):
+        P.PftPlan1D.load(bad)

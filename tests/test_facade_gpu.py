@@ -61,3 +61,14 @@ def test_verbatim_hybrid_solve_on_gpu_transforms(fac, blind):
     assert rel_l2(f_gpu, f_cpu) <= 1e-9
     assert rel_l2(p_gpu, p_cpu) <= 1e-9
     assert np.allclose(o_gpu, o_cpu, rtol=1e-9)
+
+
+def test_facade_pft_apply_1d_matches_reference(fac):
+    rng = np.random.default_rng(61)
+    z = rng.standard_normal(4096) + 1j * rng.standard_normal(4096)
+    cpu = fac.RefPlan1D.create(DATA / "scope_table_v1.txt", 4096, 128, 128, 1e-3)
+    want = cpu.apply(z)
+    with fac.facade():
+        gpu = fac.RefPlan1D.create(DATA / "scope_table_v1.txt", 4096, 128, 128, 1e-3)
+        got = gpu.apply(z)
+    assert rel_l2(got, want) <= 1e-10

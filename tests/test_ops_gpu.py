@@ -135,6 +135,32 @@ def test_hybrid_solve_c128_matches_reference(ref, blind):
     assert np.allclose(res.objective, obj_ref, rtol=1e-8)
 
 
+@pytest.mark.parametrize("tv", [(0.05, 0.0), (0.03, 0.02)])
+def test_hybrid_solve_tv_c128_matches_reference(ref, tv):
+    """TV step per sweep (solver.cpp:264-279) on the GPU (k_tv) against the
+    verbatim reference solver: band + FFT sweeps, blind."""
+    rng = np.random.default_rng(28)
+    obj, probe, offs = _small_problem(rng)
+    d = ref.simulate(obj, probe, offs)
+    init = np.exp(1j * 0.1 * rng.standard_normal(obj.shape)) * 0.8
+    pinit = probe * 0.9
+    kw = dict(pft_sweeps=2, fft_sweeps=2, beta=1.0, gamma=1.0, beta_pft=1.0 / 64 ** 2,
+              gamma_pft=1.0 / 64 ** 2, eps_pft=1e-3, blind=True)
+    f_ref, p_ref, obj_ref, _, _ = ref.hybrid_solve(init, pinit, offs, d, table_path=DATA / "scope_table_v1.txt",
+                                                   tv_mag=tv[0], tv_phase=tv[1], **kw)
+    cfg = P.SolverConfig(tv_lambda_mag=tv[0], tv_lambda_phase=tv[1], **kw)
+    res = P.hybrid_solve(d, offs, pinit, init, cfg, dtype=np.complex128)
+    assert rel_l2(res.frame, f_ref) <= 1e-9
+    assert rel_l2(res.probe, p_ref) <= 1e-9
+    assert np.allclose(res.objective, obj_ref, rtol=1e-8)
+    res32 = P.hybrid_solve(d, offs, pinit, init, cfg, dtype=np.complex64)
+    from oracle import pft_oracle as O
+    tab = O.load_scope_table(DATA / "scope_table_v1.txt")
+    ff, _, _ = O.hybrid_solve(init, pinit, offs, d, table=tab, dtype=np.complex64, tv_mag=tv[0],
+                              tv_phase=tv[1], **kw)
+    assert rel_l2(res32.frame, f_ref) <= 4.0 * rel_l2(ff, f_ref) + 1e-6
+
+
 # complex64 ePIE gate (SURVEY §8(c) C5): the GPU complex64 solve may deviate from
 # the reference (double) by at most EPIE_FLOOR_FACTOR x the deviation of
 # oracle<float> -- the reference's algorithm run entirely in complex64

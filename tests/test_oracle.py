@@ -158,6 +158,25 @@ def test_hybrid_solve_matches_reference_golden():
     assert np.allclose(objs, g["hybrid_objective"], rtol=1e-9)
 
 
+@pytest.mark.parametrize("tv", [(0.05, 0.0), (0.0, 0.05), (0.03, 0.02)])
+def test_tv_port_matches_reference_library(ref, tv):
+    """TV smoothing inside hybrid_solve (solver.cpp:71-87, 264-279): the numpy
+    restatement against the verbatim reference solver, band and FFT sweeps."""
+    g = np.load(GOLDEN / "solver_tiny.npz")
+    cfg = g["hybrid_cfg"]
+    kw = dict(pft_sweeps=int(cfg[0]), fft_sweeps=int(cfg[1]), beta=cfg[2], gamma=cfg[3],
+              beta_pft=cfg[4], gamma_pft=cfg[5], eps_pft=cfg[6], blind=True, tv_mag=tv[0],
+              tv_phase=tv[1])
+    f, p, objs = O.hybrid_solve(g["init"], g["probe"] * 0.9, g["offs"], g["d"], table=TABLE, **kw)
+    fr, pr, objr, _, _ = ref.hybrid_solve(g["init"], g["probe"] * 0.9, g["offs"], g["d"],
+                                          table_path=DATA / "scope_table_v1.txt", **kw)
+    f0, _, _ = O.hybrid_solve(g["init"], g["probe"] * 0.9, g["offs"], g["d"], table=TABLE,
+                              **{**kw, "tv_mag": 0.0, "tv_phase": 0.0})
+    assert rel_l2(f, f0) > 1e-6  # TV changed the trajectory
+    assert rel_l2(f, fr) <= 1e-10 and rel_l2(p, pr) <= 1e-10
+    assert np.allclose(objs, objr, rtol=1e-9)
+
+
 def test_acc8_fixed_point_at_truth():
     """SPEC ACC-8: noiseless data at the truth: one PIE sweep moves z by <= 1e-8."""
     g = np.load(GOLDEN / "solver_tiny.npz")
@@ -253,3 +272,20 @@ def test_oracle_float_floor_literal_cfg2(ref):
         assert rel_l2(O.pft_adjoint_2d(po, y), want_a) <= 1e-11
         adj = rel_l2(O.pft_adjoint_2d(po, y, np.complex64), want_a)
         assert lo <= fwd <= hi and lo <= adj <= hi, (tab, fwd, adj)
+
+
+@pytest.mark.parametrize("shape", [(1024, 64, 64, 1e-7), (1000, 40, 40, 1e-3), (960, 30, 30, 1e-7),
+                                   (4096, 16, 128, 1e-3)])
+def test_port_pft_apply_1d_matches_reference_library(ref, shape):
+    """pft_apply_1d (pft.cpp:78-101): restatement vs the verbatim reference,
+    and the band against the FFT (ACC-2 style bound)."""
+    n, mt, p, eps = shape
+    a = O.plan_1d(n, mt, p, eps, TABLE)
+    rp = ref.RefPlan1D.create(DATA / "scope_table_v1.txt", n, mt, p, eps)
+    rng = np.random.default_rng(41)
+    z = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    got, want = O.pft_apply_1d(a, z), rp.apply(z)
+    assert rel_l2(got, want) <= 1e-12
+    full = np.fft.fft(z)
+    crop = full[(np.arange(2 * mt + 1) - mt) % n]
+    assert np.max(np.abs(want - crop)) <= 2 * eps * np.sum(np.abs(z))

@@ -277,3 +277,41 @@ def test_e1_shard_union_bit_identical():
             backs.append(y)
         assert torch.equal(torch.cat(bands), band), ws
         assert torch.equal(torch.cat(backs), back), ws
+
+
+# ---- 1-D PFT (pft.hpp:33-38) ----
+CASES_1D = [(1024, 64, 64, 1e-7), (4096, 128, 128, 1e-3), (1000, 40, 40, 1e-3), (960, 30, 30, 1e-7),
+            (65536, 64, 64, 1e-3), (4096, 16, 128, 1e-3), (64, 4, 8, 1e-3)]
+
+
+@pytest.mark.parametrize("shape", CASES_1D)
+def test_pft_apply_1d_matches_reference(ref, shape):
+    n, mt, p, eps = shape
+    g = P.pft_plan_1d(n, mt, p, eps)
+    r = ref.RefPlan1D.create(DATA / "scope_table_v1.txt", n, mt, p, eps)
+    rng = np.random.default_rng(n + mt)
+    z = cnormal(rng, (5, n))
+    got = P.pft_apply_1d(g, torch.from_numpy(z).cuda()).cpu().numpy()
+    for b in range(5):
+        assert rel_l2(got[b], r.apply(z[b])) <= TOL128
+    z32 = z.astype(np.complex64)
+    got32 = P.pft_apply_1d(g, torch.from_numpy(z32).cuda()).cpu().numpy()
+    for b in (0, 4):
+        assert rel_l2(got32[b], r.apply(z32[b].astype(np.complex128))) <= TOL64
+    host = P.pft_apply_1d(g, z[1:3])  # host-buffer entry point
+    assert np.array_equal(host, got[1:3])
+
+
+def test_pft_apply_1d_edge_cases(ref):
+    g = P.pft_plan_1d(1024, 64, 64, 1e-7)
+    empty = P.pft_apply_1d(g, torch.zeros((0, 1024), dtype=torch.complex128, device="cuda"))
+    assert tuple(empty.shape) == (0, 129)
+    zero = P.pft_apply_1d(g, torch.zeros((2, 1024), dtype=torch.complex128, device="cuda"))
+    assert torch.count_nonzero(zero).item() == 0
+    with pytest.raises(ValueError, match="n-vector"):
+        P.pft_apply_1d(g, torch.zeros((2, 512), dtype=torch.complex128, device="cuda"))
+    # delta at 0 -> all-ones band up to the polynomial error (SPEC known answer)
+    d = torch.zeros(1024, dtype=torch.complex128, device="cuda")
+    d[0] = 1
+    out = P.pft_apply_1d(g, d).cpu().numpy()
+    assert np.max(np.abs(out - 1)) <= 2e-7

@@ -4,6 +4,7 @@
 out=gpurun_out; mkdir -p $out; tag=${1:-r8}
 python -m pytest tests -m gpu -q --timeout 600 -rf > $out/${tag}_tests.log 2>&1
 tail -3 $out/${tag}_tests.log
+python bench.py --steps 20 --warmup 5 > $out/${tag}_bench_cfg2.log 2>&1
 for w in cfg1 cfg3 cfg5; do python bench.py --workload $w --steps 10 --warmup 3 > $out/${tag}_bench_$w.log 2>&1; done
 python bench.py --workload cfg4 --steps 10 --warmup 3 --no-cpu-baseline > $out/${tag}_bench_cfg4.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/${tag}_eval_launches.csv \
