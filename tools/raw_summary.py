@@ -26,7 +26,7 @@ def main(path):
     hdr, units = rows[0], rows[1]
     idx = {k: (hdr.index(v) if v in hdr else None) for k, v in M.items()}
     ki = hdr.index("Kernel Name")
-    print("kernel," + ",".join(M))
+    print("kernel\t" + "\t".join(M))
     for r in rows[2:]:
         name = r[ki].split("(")[0].replace("void ", "")
         vals = []
@@ -42,7 +42,7 @@ def main(path):
                 scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1e-6)
                 v = v * scale
             vals.append(f"{v:.4g}")
-        print(name + "," + ",".join(vals))
+        print(name.replace(" ", "") + "\t" + "\t".join(vals))
 
 
 if __name__ == "__main__":
