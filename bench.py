@@ -54,7 +54,37 @@ WORKLOADS = {
 }
 
 
-FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 nominal
+
+
+FLOPS_PER_TRANSFORM = {"cfg1": 22.7e6, "cfg2": 72.0e6}
+# (PFT band transform, full w x w FFT) MFLOP per operator application
+EPIE_FLOPS = {"cfg3": (10.8e6, 5 * 256 * 256 * 16), "cfg4": (46.4e6, 23.6e6)}
+
+
+def fp64_peak():
+    p = ROOT / "profiles" / "fma_peak.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["fp64_dfma_tflops"]), \
+            "measured: tools/fma_peak.cu DFMA (profiles/fma_peak.json)"
+    return 37.0, "datasheet"
+
+
+def flop_line(flops_per_step, ms_per_step, kind="fp32"):
+    peak, how = fp32_peak() if kind == "fp32" else fp64_peak()
+    ach = flops_per_step / (ms_per_step / 1e3) / 1e12
+    return {"bound": kind, "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+            "flops_per_step": flops_per_step, "peak_kind": how}
+
+
+def fp32_peak():
+    """Measured packed-FFMA2 FP32 peak (tools/fma_peak.cu on a B200, committed as
+    profiles/fma_peak.json), else the nominal 148 x 128 x 2 x 1965 MHz."""
+    p = ROOT / "profiles" / "fma_peak.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return float(j["fp32_ffma2_tflops"]), "measured: tools/fma_peak.cu FFMA2 (profiles/fma_peak.json)"
+    return FP32_PEAK_TFLOPS, "nominal: 148 SMs x 128 FP32 lanes x 2 FLOP x 1965 MHz"
 FLOPS_PER_POSITION_CFG5 = 46.4e6 + 23.6e6  # SURVEY §8 D4: factored PFT band (r = 9) + 5 n log2 n FFT
 
 
@@ -89,6 +119,20 @@ def captured_traffic_per_field(kname):
             return None
         tot += float(rows[2][h[m]]) * scale.get(rows[1][h[m]], 1)
     return tot / ent[1]
+
+
+def eval_traffic_per_step(npos, path="profiles/r8_eval_raw.csv", per=32):
+    import csv
+    if not (ROOT / path).exists():
+        return None
+    rows = list(csv.reader(open(ROOT / path)))
+    h = {x: j for j, x in enumerate(rows[0])}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = 0.0
+    for r in rows[2:]:
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(r[h[m]].replace(",", "")) * scale.get(rows[1][h[m]], 1)
+    return tot * npos / per
 
 
 class ClockSampler:
@@ -392,6 +436,10 @@ def run_ours(args):
                          "kernel_ms": prof.ms, "kernel_launches": prof.count,
                          "kernel_timing": "CUDA events around every launch on its stream, in a replay of "
                                           "the K timed steps right after the timed region"},
+            # algorithmic FLOPs per transform of the factored PFT
+            # (cfg1 22.7 MFLOP in FP64, cfg2 72.0 MFLOP in FP32); both directions count
+            "flop_roofline": flop_line(FLOPS_PER_TRANSFORM[args.workload] * 2 * batch, ms_per_step,
+                                       "fp32" if dt == "c64" else "fp64"),
             "e2e": {"value": e2e_value, "unit": "transforms/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": gpu_launches,
@@ -533,6 +581,12 @@ def run_epie(args):
         "fft_updates_per_s": npos * fft_sweeps / t_fft,
         "final_objective": float(res.objective[-1]), "final_rel_err_aligned": err,
         "time_to_fixed_error": x1,
+        # SURVEY §8 D4 per blind position: band stage 2 forward + 2 adjoint PFTs,
+        # FFT stage 2 forward + 2 inverse FFTs, plus one forward FFT per position
+        # for the per-sweep objective (solver.cpp:287)
+        "flop_roofline": flop_line(npos * (pft_sweeps * (4 * EPIE_FLOPS[args.workload][0] + EPIE_FLOPS[args.workload][1])
+                                           + fft_sweeps * 5 * EPIE_FLOPS[args.workload][1]),
+                                   1e3 * walls[-1]),
         "objective_trace": [float(v) for v in res.objective],
         "kernel_ms": prof.ms, "gpu_launches": sum(prof.launches.values()),
         "cpu_baseline": cpu,
@@ -608,15 +662,18 @@ def run_evaluator(args):
             "phi_fft": phi[0], "phi_band": phi[1],
             "roofline": {"bound": "hbm", "kernel": "whole step (per-rank algorithmic bytes)",
                          "achieved": achieved_step, "peak": hbm, "unit": "GB/s", "frac": achieved_step / hbm,
-                         "traffic": None, "peak_kind": peak_kind, "dominant_kernel": kname,
+                         "traffic": eval_traffic_per_step(pe - pb),
+                         "traffic_source": "ncu --set full DRAM read+write of the four evaluator kernels of one "
+                                           "32-position chunk (profiles/r8_eval_raw.csv), x positions / 32",
+                         "peak_kind": peak_kind, "dominant_kernel": kname,
                          "kernel_ms": prof.ms},
             # this workload is compute-bound on the CUDA cores
             # (PFT band r = 9 at 46.4 MFLOP + 512^2 FFT at 23.6 MFLOP per position)
             "flop_roofline": {"bound": "fp32", "achieved": flops_step / (ms / args.steps / 1e3) / 1e12,
-                              "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                              "frac": flops_step / (ms / args.steps / 1e3) / 1e12 / FP32_PEAK_TFLOPS,
+                              "peak": fp32_peak()[0], "unit": "TFLOP/s",
+                              "frac": flops_step / (ms / args.steps / 1e3) / 1e12 / fp32_peak()[0],
                               "flops_per_position": FLOPS_PER_POSITION_CFG5,
-                              "peak_kind": "nominal: 148 SMs x 128 FP32 lanes x 2 FLOP x 1965 MHz"},
+                              "peak_kind": fp32_peak()[1]},
             "gpu_launches": sum(prof.launches.values()), "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -42,6 +42,8 @@ const Knobs& knobs() {
     o.epie_lanefft = on("PFTG_EPIE_LANEFFT");
     o.tma_ns = num("PFTG_TMA_NS");
     o.cols_grid = num("PFTG_COLS_GRID");
+    o.eval_chunk = num("PFTG_EVAL_CHUNK");
+    o.eval_one_stream = on("PFTG_EVAL_ONE_STREAM");
 #ifdef PFTG_PROFILING
     o.debug_tma = num("PFTG_DEBUG_TMA");
     o.debug_ws = num("PFTG_DEBUG_WS");
@@ -86,6 +88,22 @@ void ensure_device() {
   std::uint64_t keep = ~std::uint64_t(0);
   PFTG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   if (dev < 64) checked[dev] = true;
+}
+
+// One non-blocking side stream per device (fork / join with events; shared by
+// concurrent callers, which only serializes their side work).
+cudaStream_t side_stream() {
+  int dev = 0;
+  PFTG_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> streams;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = streams.find(dev);
+  if (it != streams.end()) return it->second;
+  cudaStream_t s;
+  PFTG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  streams.emplace(dev, s);
+  return s;
 }
 
 void check_fft_len(std::size_t n) {
@@ -573,7 +591,8 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
   const PftDev<R>* pd = plan ? &plan_dev<R>(*plan) : nullptr;
   if (pd && (pd->n1 != n1 || pd->n2 != n2))
     throw std::invalid_argument("band_residual: plan does not match the window shape");
-  const std::size_t chunk = std::max<std::size_t>(1, std::min<std::size_t>(count, (64u << 20) / (sizeof(Cx<R>) * n)));
+  std::size_t chunk = std::max<std::size_t>(1, std::min<std::size_t>(count, (64u << 20) / (sizeof(Cx<R>) * n)));
+  if (knobs().eval_chunk > 0) chunk = std::max<std::size_t>(1, std::min<std::size_t>(count, knobs().eval_chunk));
   Scratch doffs(sizeof(long long) * std::max<std::size_t>(count, 1), st);
   if (count) PFTG_CUDA(cudaMemcpyAsync(doffs.p, offs.data(), sizeof(long long) * count, cudaMemcpyHostToDevice, st));
   Scratch X(sizeof(Cx<R>) * n * chunk, st);
@@ -587,6 +606,18 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
     G.reset(new Scratch(sizeof(Cx<R>) * (std::size_t)pd->p1 * pd->r1 * pd->M2 * chunk, st));
     bstrips = cols_strips<R>(*pd);
     bpart.reset(new Scratch(sizeof(double) * bstrips * std::max<std::size_t>(count, 1), st));
+  }
+  // The full-FFT residual and the PFT band residual are independent: the band
+  // chain runs on a side stream (forked / joined with events) so its kernels
+  // fill the SMs the FFT kernels leave idle at chunk boundaries.
+  cudaStream_t sb = st;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (pd && count && !knobs().eval_one_stream && !capturing(st)) {
+    sb = side_stream();
+    PFTG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    PFTG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    PFTG_CUDA(cudaEventRecord(ev_fork, st));
+    PFTG_CUDA(cudaStreamWaitEvent(sb, ev_fork, 0));
   }
   for (std::size_t c0 = 0; c0 < count; c0 += chunk) {
     const int nb = (int)std::min(chunk, count - c0);
@@ -623,11 +654,17 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
       bool evec = vec_ok(frame, (long long)fc, 0) && vec_ok(probe, n2, 0);
       for (std::size_t j = c0; j < c0 + nb; ++j) evec = evec && (offs[j] % 2 == 0);
       Src<R> s2{static_cast<const Cx<R>*>(frame), (long long)fc, 0, o, static_cast<const Cx<R>*>(probe), evec};
-      launch_fwd_rows<R>(*pd, s2, G->as<Cx<R>>(), nb, st);
+      launch_fwd_rows<R>(*pd, s2, G->as<Cx<R>>(), nb, sb);
       const long long mb = (long long)pd->M1 * pd->M2;
       launch_fwd_cols<R>(*pd, 2, G->as<Cx<R>>(), nullptr, static_cast<const R*>(dcrop) + (pb + c0) * mb, mb,
-                         nullptr, bpart->as<double>() + c0 * bstrips, nb, st);
+                         nullptr, bpart->as<double>() + c0 * bstrips, nb, sb);
     }
+  }
+  if (ev_fork) {
+    PFTG_CUDA(cudaEventRecord(ev_join, sb));
+    PFTG_CUDA(cudaStreamWaitEvent(st, ev_join, 0));  // scratch frees and the D2H below are ordered after the band chain
+    cudaEventDestroy(ev_fork);
+    cudaEventDestroy(ev_join);
   }
   std::vector<double> h(nstrips * count), hb(bstrips * count);
   if (count) PFTG_CUDA(cudaMemcpyAsync(h.data(), part.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));

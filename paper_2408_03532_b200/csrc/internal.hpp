@@ -39,6 +39,8 @@ void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
 struct Knobs {
   bool no_pdl, no_tma, no_ws, no_wide, no_split, no_local_cols, eval_lanefft, epie_lanefft;
   int tma_ns, cols_grid;  // 0 = unset
+  int eval_chunk;         // evaluator positions per chunk (0 = 64 MB of spectra)
+  bool eval_one_stream;   // evaluator: FFT and PFT chains on one stream
   int debug_tma, debug_ws, debug_adj, debug_cols, debug_adjcols;
   bool debug_wide_adj;
 };
