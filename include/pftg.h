@@ -75,6 +75,28 @@ int pftg_table_min_degree(const pftg_table* t, double eps, double target_scope, 
 
 /* pft_plan_2d (pft.hpp:49-51): r = min_degree(eps, mt/p) per axis;
  * B[l,j] = w_j (1-2l/q)^j, W[t,j] = (t/p)^j e^{-i pi t/p}  (pft.cpp:33-76). */
+/* ---- offline scope-table pipeline (minimax.hpp:28-70) ----
+ * Own near-minimax solver (csrc/minimax.cpp), certified like the reference
+ * (4097-point a-posteriori error); coefficients are near- (not bit-) identical. */
+/* best_approx (minimax.hpp:28): coeff = r interleaved complex, achieved = certified error */
+int pftg_best_approx(int r, double xi, double* coeff, double* achieved);
+/* ScopeTable::compute (minimax.hpp:48-49); eps list (default 1e-1 .. 1e-7), r = 1..max_r */
+int pftg_table_compute(const double* eps, int neps, int max_r, pftg_table** out);
+int pftg_table_save(const pftg_table* t, const char* path); /* ScopeTable::save (minimax.hpp:51) */
+int pftg_table_info(const pftg_table* t, int* nrec, int* max_r);
+/* record i (eps-major, r ascending): coeff = r interleaved complex */
+int pftg_table_record(const pftg_table* t, int i, double* eps, int* r, double* xi, double* achieved,
+                      double* coeff);
+
+/* ---- measurement-set directory (simulate.hpp:40-43, raw_io.hpp:10-27) ----
+ * d [count][rows][cols], dcrop [count][2mt1][2mt2] (NULL: none, mt = 0). */
+int pftg_measurements_save(const char* dir, size_t count, size_t rows, size_t cols, const double* d, size_t mt1,
+                           size_t mt2, const double* dcrop, double noise_scale, uint64_t noise_seed);
+/* verifies the manifest; info = count rows cols mt1 mt2 */
+int pftg_measurements_info(const char* dir, int64_t* info, double* noise_scale, uint64_t* noise_seed);
+/* host buffers in the GPU path's precision: float (PFTG_C64) or double (PFTG_C128); dcrop may be NULL */
+int pftg_measurements_read(const char* dir, int dtype, void* d, void* dcrop);
+
 int pftg_plan_2d(const pftg_table* t, size_t n1, size_t n2, size_t mt1, size_t mt2, size_t p1,
                  size_t p2, double eps, pftg_plan** out);
 /* PftPlan2D from in-memory tables (pft.hpp:25-47): per axis n, p, mt, r and

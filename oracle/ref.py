@@ -84,6 +84,8 @@ def lib():
         L.ref_epie_probe_update.argtypes = [dp, dp, dp, szt, szt, C.c_double, C.c_int]
         L.ref_objective_value.argtypes = [dp, szt, szt, dp, szt, szt, i64p, szt, dp, dp]
         L.ref_simulate.argtypes = [dp, szt, szt, dp, szt, szt, i64p, szt, dp]
+        L.ref_save_measurements.argtypes = [C.c_char_p, dp, szt, szt, szt, szt, szt, C.c_double, C.c_uint64]
+        L.ref_load_measurements.argtypes = [C.c_char_p, i64p, dp, dp, dp]
         L.ref_add_poisson_noise.argtypes = [dp, szt, szt, szt, C.c_double, C.c_uint64]
         L.ref_hybrid_solve.argtypes = [dp, szt, szt, dp, szt, szt, i64p, szt, dp, dp, i64p,
                                        C.c_char_p, dp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
@@ -321,6 +323,27 @@ def simulate(frame, probe, offsets):
     _check(lib().ref_simulate(_cptr(f), f.shape[0], f.shape[1], _cptr(p), p.shape[0], p.shape[1],
                               o.ctypes.data_as(C.POINTER(C.c_int64)), len(o), _cptr(d)))
     return d
+
+
+def save_measurements(path, d, mt=0, noise_scale=0.0, noise_seed=0):
+    """save_measurements (simulate.cpp:91-127); build_cropped(mt) first when mt > 0."""
+    d = _f64(d)
+    _check(lib().ref_save_measurements(str(path).encode(), _cptr(d), d.shape[0], d.shape[1], d.shape[2],
+                                       mt, mt, noise_scale, noise_seed))
+
+
+def load_measurements(path):
+    """load_measurements (simulate.cpp:129-164) -> (d, dcrop or None, (scale, seed))."""
+    info = np.zeros(5, np.int64)
+    noise = np.zeros(2)
+    _check(lib().ref_load_measurements(str(path).encode(), info.ctypes.data_as(C.POINTER(C.c_int64)),
+                                       _cptr(noise), None, None))
+    cnt, r, c, m1, m2 = (int(v) for v in info)
+    d = np.zeros((cnt, r, c))
+    dc = np.zeros((cnt, 2 * m1, 2 * m2)) if m1 else None
+    _check(lib().ref_load_measurements(str(path).encode(), info.ctypes.data_as(C.POINTER(C.c_int64)),
+                                       _cptr(noise), _cptr(d), _cptr(dc) if dc is not None else None))
+    return d, dc, (float(noise[0]), int(noise[1]))
 
 
 def add_poisson_noise(d, scale, seed):

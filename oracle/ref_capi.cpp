@@ -343,6 +343,46 @@ int ref_simulate(const double* frame, std::size_t fr, std::size_t fc, const doub
   });
 }
 
+// save_measurements (simulate.cpp:91-127) of d [npos][wr][wc]; build_cropped
+// first when mt1 > 0; the noise fields are recorded as given.
+int ref_save_measurements(const char* dir, const double* d, std::size_t npos, std::size_t wr, std::size_t wc,
+                          std::size_t mt1, std::size_t mt2, double noise_scale, std::uint64_t noise_seed) {
+  return guarded([&] {
+    MeasurementSet ms;
+    ms.window_rows = wr;
+    ms.window_cols = wc;
+    for (std::size_t j = 0; j < npos; ++j) {
+      RealField x(wr, wc);
+      std::memcpy(x.data(), d + j * wr * wc, wr * wc * sizeof(double));
+      ms.d.push_back(std::move(x));
+    }
+    if (mt1 > 0) build_cropped(ms, mt1, mt2);
+    ms.noise_scale = noise_scale;
+    ms.noise_seed = noise_seed;
+    save_measurements(dir, ms);
+  });
+}
+
+// load_measurements (simulate.cpp:129-164): info[5] = count rows cols mt1 mt2;
+// d / dcrop filled when non-null.
+int ref_load_measurements(const char* dir, std::int64_t* info, double* noise, double* d, double* dcrop) {
+  return guarded([&] {
+    const MeasurementSet ms = load_measurements(dir);
+    info[0] = static_cast<std::int64_t>(ms.count());
+    info[1] = static_cast<std::int64_t>(ms.window_rows);
+    info[2] = static_cast<std::int64_t>(ms.window_cols);
+    info[3] = static_cast<std::int64_t>(ms.mt1);
+    info[4] = static_cast<std::int64_t>(ms.mt2);
+    noise[0] = ms.noise_scale;
+    noise[1] = static_cast<double>(ms.noise_seed);
+    const std::size_t wn = ms.window_rows * ms.window_cols, cn = 4 * ms.mt1 * ms.mt2;
+    for (std::size_t j = 0; j < ms.count(); ++j) {
+      if (d) std::memcpy(d + j * wn, ms.d[j].data(), wn * sizeof(double));
+      if (dcrop && j < ms.d_crop.size()) std::memcpy(dcrop + j * cn, ms.d_crop[j].data(), cn * sizeof(double));
+    }
+  });
+}
+
 int ref_add_poisson_noise(double* d, std::size_t wr, std::size_t wc, std::size_t npos,
                           double scale, std::uint64_t seed) {
   return guarded([&] {

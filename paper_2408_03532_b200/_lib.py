@@ -19,6 +19,8 @@ PFTG_C64, PFTG_C128 = 0, 1
 EXPORTS = (
     "pftg_version", "pftg_last_error", "pftg_device_ok", "pftg_profile_begin", "pftg_profile_end",
     "pftg_table_load", "pftg_table_free", "pftg_table_min_degree",
+    "pftg_best_approx", "pftg_table_compute", "pftg_table_save", "pftg_table_info", "pftg_table_record",
+    "pftg_measurements_save", "pftg_measurements_info", "pftg_measurements_read",
     "pftg_plan_2d", "pftg_plan_from_tables", "pftg_plan_load", "pftg_plan_save", "pftg_plan_free", "pftg_plan_info",
     "pftg_plan_tables",
     "pftg_apply_2d_dev", "pftg_adjoint_2d_dev", "pftg_apply_2d_host", "pftg_adjoint_2d_host",
@@ -96,6 +98,14 @@ def lib():
     L.pftg_simulate_dev.argtypes = [C.c_int, vp, sz, sz, vp, sz, sz, i64p, sz, vp, vp]
     L.pftg_add_poisson_noise_dev.argtypes = [C.c_int, vp, sz, C.c_double, C.c_uint64, vp]
     L.pftg_fill_metrics_dev.argtypes = [C.c_int, vp, sz, vp, sz, sz, sz, dp, vp]
+    L.pftg_best_approx.argtypes = [C.c_int, C.c_double, dp, dp]
+    L.pftg_table_compute.argtypes = [dp, C.c_int, C.c_int, C.POINTER(vp)]
+    L.pftg_table_save.argtypes = [vp, C.c_char_p]
+    L.pftg_table_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.pftg_table_record.argtypes = [vp, C.c_int, dp, C.POINTER(C.c_int), dp, dp, dp]
+    L.pftg_measurements_save.argtypes = [C.c_char_p, sz, sz, sz, dp, sz, sz, dp, C.c_double, C.c_uint64]
+    L.pftg_measurements_info.argtypes = [C.c_char_p, i64p, dp, C.POINTER(C.c_uint64)]
+    L.pftg_measurements_read.argtypes = [C.c_char_p, C.c_int, vp, vp]
     L.pftg_plan_1d.argtypes = [vp, sz, sz, sz, C.c_double, C.POINTER(vp)]
     L.pftg_plan1d_from_tables.argtypes = [sz, sz, sz, C.c_int, dp, dp, C.c_double, C.POINTER(vp)]
     L.pftg_plan1d_load.argtypes = [C.c_char_p, C.POINTER(vp)]

@@ -809,6 +809,94 @@ int pftg_table_min_degree(const pftg_table* t, double eps, double target, int* r
   return guarded([&] { *r_out = table_min_degree(t->t, eps, target); });
 }
 
+int pftg_best_approx(int r, double xi, double* coeff, double* achieved) {
+  return guarded([&] {
+    if (!coeff) throw std::invalid_argument("pftg_best_approx: null output");
+    double e = 0.0;
+    const std::vector<cd> w = best_approx_own(r, xi, &e);
+    std::memcpy(coeff, w.data(), w.size() * sizeof(cd));
+    if (achieved) *achieved = e;
+  });
+}
+
+int pftg_table_compute(const double* eps, int neps, int max_r, pftg_table** out) {
+  return guarded([&] {
+    if (!out || (neps > 0 && !eps)) throw std::invalid_argument("pftg_table_compute: null argument");
+    auto t = std::make_unique<pftg_table>();
+    t->t = table_compute(std::vector<double>(eps, eps + std::max(neps, 0)), max_r);
+    *out = t.release();
+  });
+}
+
+int pftg_table_save(const pftg_table* t, const char* path) {
+  return guarded([&] {
+    if (!t || !path) throw std::invalid_argument("pftg_table_save: null argument");
+    table_save(t->t, path);
+  });
+}
+
+int pftg_table_info(const pftg_table* t, int* nrec, int* max_r) {
+  return guarded([&] {
+    if (!t) throw std::invalid_argument("pftg_table_info: null table");
+    if (nrec) *nrec = (int)t->t.records.size();
+    if (max_r) *max_r = t->t.max_r;
+  });
+}
+
+int pftg_table_record(const pftg_table* t, int i, double* eps, int* r, double* xi, double* achieved,
+                      double* coeff) {
+  return guarded([&] {
+    if (!t) throw std::invalid_argument("pftg_table_record: null table");
+    if (i < 0 || i >= (int)t->t.records.size()) throw std::out_of_range("pftg_table_record: index out of range");
+    const Record& rec = t->t.records[i];
+    if (eps) *eps = rec.eps;
+    if (r) *r = rec.r;
+    if (xi) *xi = rec.xi;
+    if (achieved) *achieved = rec.achieved_error;
+    if (coeff) std::memcpy(coeff, rec.coeff.data(), rec.coeff.size() * sizeof(cd));
+  });
+}
+
+int pftg_measurements_save(const char* dir, size_t count, size_t rows, size_t cols, const double* d, size_t mt1,
+                           size_t mt2, const double* dcrop, double noise_scale, uint64_t noise_seed) {
+  return guarded([&] {
+    if (!dir || (count && !d)) throw std::invalid_argument("pftg_measurements_save: null argument");
+    MeasMeta m;
+    m.count = count;
+    m.rows = rows;
+    m.cols = cols;
+    m.mt1 = dcrop ? mt1 : 0;
+    m.mt2 = dcrop ? mt2 : 0;
+    m.noise_scale = noise_scale;
+    m.noise_seed = noise_seed;
+    meas_save(dir, m, d, dcrop);
+  });
+}
+
+int pftg_measurements_info(const char* dir, int64_t* info, double* noise_scale, uint64_t* noise_seed) {
+  return guarded([&] {
+    if (!dir || !info) throw std::invalid_argument("pftg_measurements_info: null argument");
+    const MeasMeta m = meas_info(dir);
+    info[0] = (int64_t)m.count;
+    info[1] = (int64_t)m.rows;
+    info[2] = (int64_t)m.cols;
+    info[3] = (int64_t)m.mt1;
+    info[4] = (int64_t)m.mt2;
+    if (noise_scale) *noise_scale = m.noise_scale;
+    if (noise_seed) *noise_seed = m.noise_seed;
+  });
+}
+
+int pftg_measurements_read(const char* dir, int dtype, void* d, void* dcrop) {
+  return guarded([&] {
+    check_dtype(dtype);
+    if (!dir || !d) throw std::invalid_argument("pftg_measurements_read: null argument");
+    const MeasMeta m = meas_info(dir);
+    if (dtype == PFTG_C64) meas_read<float>(dir, m, static_cast<float*>(d), static_cast<float*>(dcrop));
+    else meas_read<double>(dir, m, static_cast<double*>(d), static_cast<double*>(dcrop));
+  });
+}
+
 int pftg_plan_2d(const pftg_table* t, size_t n1, size_t n2, size_t mt1, size_t mt2, size_t p1, size_t p2,
                  double eps, pftg_plan** out) {
   return guarded([&] {

@@ -36,11 +36,25 @@ struct Axis {
 };
 
 Table table_load(const std::string& path);
+// minimax.cpp: own near-minimax solver and the scope-table computation
+std::vector<cd> best_approx_own(int r, double xi, double* achieved);
+Table table_compute(const std::vector<double>& eps_list, int max_r);
+void table_save(const Table& t, const std::string& path);
 const Record* table_find(const Table& t, double eps, int r);
 int table_min_degree(const Table& t, double eps, double target);
 Axis plan_1d(std::size_t n, std::size_t mt, std::size_t p, double eps, const Table& table);
 void plan_save(const Axis& a1, const Axis& a2, const std::string& path);
 void plan_load(Axis& a1, Axis& a2, const std::string& path);
+// meas_io.cpp: the measurement-set directory (simulate.cpp:91-164)
+struct MeasMeta {
+  std::size_t count = 0, rows = 0, cols = 0, mt1 = 0, mt2 = 0;
+  double noise_scale = 0.0;
+  unsigned long long noise_seed = 0;
+};
+void meas_save(const std::string& dir, const MeasMeta& m, const double* d, const double* dcrop);
+MeasMeta meas_info(const std::string& dir);  // verifies the manifest
+template <class T>
+void meas_read(const std::string& dir, const MeasMeta& m, T* d, T* dcrop);
 void plan_save_1d(const Axis& a, const std::string& path);
 void plan_load_1d(Axis& a, const std::string& path);
 

@@ -79,6 +79,33 @@ class ScopeTable:
         check(lib().pftg_table_load(str(path).encode(), C.byref(h)))
         return cls(h.value)
 
+    @classmethod
+    def compute(cls, eps_list=(1e-1, 1e-2, 1e-3, 1e-4, 1e-5, 1e-6, 1e-7), max_r: int = 25) -> "ScopeTable":
+        """ScopeTable::compute (minimax.hpp:48-49): the own near-minimax solver
+        (csrc/minimax.cpp) over eps x r = 1..max_r."""
+        e = np.ascontiguousarray(eps_list, np.float64)
+        h = C.c_void_p()
+        check(lib().pftg_table_compute(e.ctypes.data_as(C.POINTER(C.c_double)), len(e), max_r, C.byref(h)))
+        return cls(h.value)
+
+    def save(self, path) -> None:
+        """ScopeTable::save: the pft-scope-table v1 text format."""
+        check(lib().pftg_table_save(self._h, str(path).encode()))
+
+    def records(self):
+        """[(eps, r, xi, achieved_error, coeff complex128[r]), ...], eps-major, r ascending."""
+        n, mr = C.c_int(), C.c_int()
+        check(lib().pftg_table_info(self._h, C.byref(n), C.byref(mr)))
+        out = []
+        for i in range(n.value):
+            eps, xi, ach, r = C.c_double(), C.c_double(), C.c_double(), C.c_int()
+            check(lib().pftg_table_record(self._h, i, C.byref(eps), C.byref(r), C.byref(xi), C.byref(ach), None))
+            w = np.zeros(r.value, np.complex128)
+            check(lib().pftg_table_record(self._h, i, None, None, None, None,
+                                          w.ctypes.data_as(C.POINTER(C.c_double))))
+            out.append((eps.value, r.value, xi.value, ach.value, w))
+        return out
+
     def min_degree(self, eps: float, target_scope: float) -> int:
         r = C.c_int()
         check(lib().pftg_table_min_degree(self._h, eps, target_scope, C.byref(r)))
@@ -198,6 +225,14 @@ class PftPlan1D:
             lib().pftg_plan1d_free(self._h)
         except Exception:
             pass
+
+
+def best_approx(r: int, xi: float):
+    """minimax::best_approx (minimax.hpp:28): (coeff complex128[r], achieved_error)."""
+    w = np.zeros(r, np.complex128)
+    e = C.c_double()
+    check(lib().pftg_best_approx(r, xi, w.ctypes.data_as(C.POINTER(C.c_double)), C.byref(e)))
+    return w, e.value
 
 
 def pft_plan_1d(n, mt, p, eps, table: ScopeTable | None = None) -> PftPlan1D:

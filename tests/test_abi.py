@@ -187,3 +187,87 @@ def test_plan_1d_errors_mirror_reference(tmp_path):
     bad.write_text("pft-plan-2d v1\n")
     with pytest.raises(OSError, match="pft-plan-1d"):
         P.PftPlan1D.load(bad)
+
+
+# ---- offline scope-table pipeline ----
+
+@pytest.mark.parametrize("r,xi", [(1, 0.1), (9, 1.0), (13, 1.0), (12, 4.0), (10, 4.0), (25, 10.0)])
+def test_best_approx_matches_reference(ref, r, xi):
+    """Own near-minimax solver vs the reference's Remez (minimax.cpp:276-342):
+    certified error within 1e-4 relative (never worse by more), parity
+    structure (even real / odd imaginary) exact; coefficients within 1e-6 where
+    the approximation is resolved (the xi = 4, 10 cases sit at errors ~1 where
+    the exchange solutions differ in the 5th digit, ours slightly lower)."""
+    w, e = P.best_approx(r, xi)
+    wr, er = ref.best_approx(r, xi)[:2]
+    assert e <= er * (1 + 1e-4)
+    assert abs(e - er) <= 1e-4 * er
+    assert np.all(w[0::2].imag == 0) and np.all(w[1::2].real == 0)
+    if er < 1e-2:  # resolved cases: the two minimax solutions coincide closely
+        assert np.max(np.abs(w - wr)) <= 1e-6 * max(1.0, np.max(np.abs(wr)))
+
+
+def test_scope_table_compute_matches_reference_table(tmp_path, ref):
+    """ScopeTable::compute (minimax.cpp:388-433): every (eps, r) record's scope
+    xi equals the reference-built table's, achieved <= eps, min_degree agrees on
+    a grid of targets; the saved file loads in the reference and here."""
+    from oracle import pft_oracle as O
+    t = P.ScopeTable.compute()
+    R = O.load_scope_table(DATA / "scope_table_v1.txt")
+    recs = t.records()
+    assert len(recs) == len(R) == 7 * 25
+    for (eps, r, xi, ach, w), rec in zip(recs, R):
+        assert abs(rec.eps - eps) <= 1e-12 * eps and rec.r == r
+        assert abs(xi - rec.xi) <= 2e-3 * rec.xi
+        assert ach <= eps or xi == 0.0
+    for eps in (1e-1, 1e-3, 1e-5, 1e-7):
+        for tgt in (0.1, 0.5, 1.0, 2.0, 4.0):
+            try:
+                a = t.min_degree(eps, tgt)
+            except ValueError:
+                a = None
+            try:
+                b = O.min_degree(R, eps, tgt)
+            except ValueError:
+                b = None
+            assert a == b, (eps, tgt)
+    t.save(tmp_path / "t.txt")
+    assert ref.min_degree(tmp_path / "t.txt", 1e-7, 1.0) == 13
+    assert P.ScopeTable.load(tmp_path / "t.txt").min_degree(1e-3, 1.0) == 9
+    small = P.ScopeTable.compute([1e-3], 10)
+    assert len(small.records()) == 10
+    with pytest.raises(ValueError):
+        P.ScopeTable.compute([], 5)
+
+
+# ---- measurement-set directory (simulate.cpp:91-164; SURVEY §8(f) F3) ----
+
+def test_measurement_directory_interop(tmp_path, ref):
+    rng = np.random.default_rng(5)
+    d = np.abs(rng.standard_normal((3, 32, 32))) * 10
+    ref.save_measurements(tmp_path / "r", d, mt=4, noise_scale=123.5, noise_seed=77)
+    dd, dc, sc, sd = P.load_measurements(tmp_path / "r", np.float64)
+    assert np.array_equal(dd, d) and (sc, sd) == (123.5, 77)
+    from oracle import pft_oracle as O
+    assert np.array_equal(dc, np.stack([O.crop_centered(x, 4, 4) for x in d]))
+    d32, dc32, _, _ = P.load_measurements(tmp_path / "r")
+    assert d32.dtype == np.float32 and np.array_equal(d32, d.astype(np.float32))
+    # ours -> byte-identical directory, loadable by the reference
+    P.save_measurements(tmp_path / "o", d, dc, 123.5, 77)
+    for f in sorted((tmp_path / "r").iterdir()):
+        assert (tmp_path / "o" / f.name).read_bytes() == f.read_bytes(), f.name
+    rd, rdc, (rs, rseed) = ref.load_measurements(tmp_path / "o")
+    assert np.array_equal(rd, d) and np.array_equal(rdc, dc) and (rs, rseed) == (123.5, 77)
+    # no crop
+    P.save_measurements(tmp_path / "n", d)
+    nd, ndc, _, _ = P.load_measurements(tmp_path / "n", np.float64)
+    assert ndc is None and np.array_equal(nd, d)
+    # the manifest pins every file
+    f = tmp_path / "o" / "d_0001.ptyr"
+    b = bytearray(f.read_bytes())
+    b[-1] ^= 1
+    f.write_bytes(bytes(b))
+    with pytest.raises(OSError, match="manifest hash mismatch"):
+        P.load_measurements(tmp_path / "o")
+    with pytest.raises(OSError, match="manifest"):
+        P.load_measurements(tmp_path / "missing")
