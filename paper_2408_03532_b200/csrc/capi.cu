@@ -44,6 +44,8 @@ const Knobs& knobs() {
     o.cols_grid = num("PFTG_COLS_GRID");
     o.eval_chunk = num("PFTG_EVAL_CHUNK");
     o.eval_one_stream = on("PFTG_EVAL_ONE_STREAM");
+    o.no_tile = on("PFTG_NO_TILE");
+    o.force_tile = on("PFTG_TILE");
 #ifdef PFTG_PROFILING
     o.debug_tma = num("PFTG_DEBUG_TMA");
     o.debug_ws = num("PFTG_DEBUG_WS");
@@ -147,6 +149,17 @@ void prof_add_launches(const int* delta) {
   for (int k = 0; k < K_NUM; ++k) p.launches[k] += delta[k];
 }
 
+// Profiling only: keeps the stream busy for ~ns so the start event and the
+// timed launch are both enqueued before the GPU reaches them -- the event
+// interval then measures the kernel, not host-side submission gaps.
+__global__ void k_prof_spin(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 ProfScope::ProfScope(cudaStream_t s, int k) : kid(k), st(s) {
   ProfState& p = prof();
   {
@@ -156,6 +169,7 @@ ProfScope::ProfScope(cudaStream_t s, int k) : kid(k), st(s) {
   }
   if (capturing(st)) return;
   e0 = new_event();
+  k_prof_spin<<<1, 32, 0, st>>>(30000ull);
   PFTG_CUDA(cudaEventRecord(e0, st));
 }
 
@@ -364,8 +378,15 @@ std::size_t chunk_fields(const PftDev<R>& pd, std::size_t batch = 0) {
 }
 
 template <class R>
-void apply_dev(const pftg_plan* plan, const void* z, void* band, std::size_t batch, cudaStream_t st) {
+void apply_dev(const pftg_plan* plan, const void* z, void* band, std::size_t batch, cudaStream_t st,
+               std::size_t call_batch = 0) {
   const PftDev<R>& pd = plan_dev<R>(*plan);
+  // the path is chosen on the caller's whole batch (host-buffer chunks included),
+  // so a call gives bit-identical results through either entry point
+  if (tile_path_ok(pd, call_batch ? call_batch : batch)) {  // small batches: >= p1 p2 CTAs per stage (pft_tile.cu)
+    tile_apply<R>(pd, z, (long long)pd.n1 * pd.n2, band, (int)batch, st);
+    return;
+  }
   const std::size_t chunk = std::min(batch, chunk_fields(pd, batch));
   const std::size_t gsz = (std::size_t)g_field_elems<R>(pd);
   Scratch G(sizeof(Cx<R>) * gsz * chunk, st);
@@ -381,8 +402,13 @@ void apply_dev(const pftg_plan* plan, const void* z, void* band, std::size_t bat
 }
 
 template <class R>
-void adjoint_dev(const pftg_plan* plan, const void* band, void* z, std::size_t batch, cudaStream_t st) {
+void adjoint_dev(const pftg_plan* plan, const void* band, void* z, std::size_t batch, cudaStream_t st,
+                 std::size_t call_batch = 0) {
   const PftDev<R>& pd = plan_dev<R>(*plan);
+  if (tile_path_ok(pd, call_batch ? call_batch : batch)) {
+    tile_adjoint<R>(pd, band, z, (long long)pd.n1 * pd.n2, (int)batch, st);
+    return;
+  }
   const std::size_t chunk = std::min(batch, chunk_fields(pd, batch));
   const std::size_t gsz = (std::size_t)pd.p1 * pd.r1 * pd.M2;
   Scratch G(sizeof(Cx<R>) * gsz * chunk, st);
@@ -1012,7 +1038,7 @@ int pftg_apply_2d_host(const pftg_plan* plan, int dtype, const void* z, void* ba
       using R = decltype(tag);
       const std::size_t chunk = host_chunk(batch, sizeof(Cx<R>) * nz);
       host_pipeline<R>(batch, nz, nb, z, band, chunk, [&](Cx<R>* din, Cx<R>* dout, std::size_t nbat, cudaStream_t s) {
-        apply_dev<R>(plan, din, dout, nbat, s);
+        apply_dev<R>(plan, din, dout, nbat, s, batch);
       });
     };
     if (dtype == PFTG_C64) run(float{});
@@ -1031,7 +1057,7 @@ int pftg_adjoint_2d_host(const pftg_plan* plan, int dtype, const void* band, voi
       using R = decltype(tag);
       const std::size_t chunk = host_chunk(batch, sizeof(Cx<R>) * nz);
       host_pipeline<R>(batch, nb, nz, band, z, chunk, [&](Cx<R>* din, Cx<R>* dout, std::size_t nbat, cudaStream_t s) {
-        adjoint_dev<R>(plan, din, dout, nbat, s);
+        adjoint_dev<R>(plan, din, dout, nbat, s, batch);
       });
     };
     if (dtype == PFTG_C64) run(float{});

@@ -41,6 +41,7 @@ struct Knobs {
   int tma_ns, cols_grid;  // 0 = unset
   int eval_chunk;         // evaluator positions per chunk (0 = 64 MB of spectra)
   bool eval_one_stream;   // evaluator: FFT and PFT chains on one stream
+  bool no_tile, force_tile;  // small-batch tile path (pft_tile.cu): off / forced
   int debug_tma, debug_ws, debug_adj, debug_cols, debug_adjcols;
   bool debug_wide_adj;
 };
@@ -113,6 +114,14 @@ void launch_adj_cols(const PftDev<R>& pd, const typename CT<R>::C* band, typenam
 template <class R>
 void launch_adj_rows(const PftDev<R>& pd, int epi, const typename CT<R>::C* Gt, const EpiArgs& ep,
                      int batch, cudaStream_t st);
+
+// ---- small-batch tile path (pft_tile.cu) ----
+template <class R>
+bool tile_path_ok(const PftDev<R>& pd, std::size_t batch);
+template <class R>
+void tile_apply(const PftDev<R>& pd, const void* z, long long bstride, void* band, int batch, cudaStream_t st);
+template <class R>
+void tile_adjoint(const PftDev<R>& pd, const void* band, void* z, long long bstride, int batch, cudaStream_t st);
 
 // ---- full FFT building blocks (fft_launch_*.cu) ----
 template <class R>
