@@ -359,7 +359,7 @@ def run_ours(args):
     # Per-kernel CUDA-event times for the roofline: the same K steps replayed
     # with events around every launch (events between kernels would break the
     # programmatic-dependent-launch overlap inside the timed region itself).
-    with KernelProfile() as prof:
+    with KernelProfile(isolate=True) as prof:
         for _ in range(args.steps):
             step_eager()  # eager launches: graph replays carry no per-kernel events
         torch.cuda.synchronize()
@@ -670,11 +670,16 @@ def run_evaluator(args):
         dist.barrier(device_ids=[local])
     clk = ClockSampler(local).__enter__()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with KernelProfile() as prof:
-        e0.record()
+    e0.record()
+    for _ in range(args.steps):
+        phi = step()
+    e1.record()
+    torch.cuda.synchronize()
+    # per-kernel times and launch counts: the same K steps replayed with events
+    # (isolated launches), outside the timed region
+    with KernelProfile(isolate=True) as prof:
         for _ in range(args.steps):
-            phi = step()
-        e1.record()
+            step()
         torch.cuda.synchronize()
     t_end = time.perf_counter() + 1.0
     while time.perf_counter() < t_end:

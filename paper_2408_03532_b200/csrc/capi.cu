@@ -119,6 +119,7 @@ namespace {
 struct ProfState {
   std::mutex mu;
   bool on = false;
+  bool isolate = false;  // spin before each timed launch (pftg_profile_isolate)
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
   int launches[K_NUM] = {};
 };
@@ -169,7 +170,7 @@ ProfScope::ProfScope(cudaStream_t s, int k) : kid(k), st(s) {
   }
   if (capturing(st)) return;
   e0 = new_event();
-  k_prof_spin<<<1, 32, 0, st>>>(30000ull);
+  if (prof().isolate) k_prof_spin<<<1, 32, 0, st>>>(30000ull);
   PFTG_CUDA(cudaEventRecord(e0, st));
 }
 
@@ -785,6 +786,14 @@ int pftg_profile_begin(void) {
     p.ev.clear();
     std::fill(p.launches, p.launches + K_NUM, 0);
     p.on = true;
+  });
+}
+
+int pftg_profile_isolate(int on) {
+  return guarded([&] {
+    ProfState& p = prof();
+    std::lock_guard<std::mutex> lock(p.mu);
+    p.isolate = on != 0;
   });
 }
 

@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(32 * NCOL) ke_cols256_proj(float2* X, const fl
 // DFT_512 of the row, natural order. grid (512 / (4 * RPG), positions), block
 // 256 = four 64-thread groups, each transforming RPG rows.
 template <int RPG>
-__global__ void __launch_bounds__(256, 3) ke_rows512(const float2* __restrict__ frame, long long ld,
+__global__ void __launch_bounds__(256, 2) ke_rows512(const float2* __restrict__ frame, long long ld,
                                                   const long long* __restrict__ offs,
                                                   const float2* __restrict__ probe, const float2* __restrict__ tw,
                                                   float2* __restrict__ X) {
