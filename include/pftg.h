@@ -65,10 +65,12 @@ int pftg_device_ok(void);
  * included (arrays of 6). */
 int pftg_profile_begin(void);
 int pftg_profile_end(double* ms, int* count, int* launches);
-/* on != 0: every profiled launch is preceded by a ~30 us device spin, so its
+/* Profiling mode for the next begin/end window: 0 = CUDA events around every
+ * launch; 1 = the same, each launch preceded by a ~30 us device spin so its
  * events time the kernel rather than host-side submission gaps (replays only:
- * the spins lengthen the stream). */
-int pftg_profile_isolate(int on);
+ * the spins lengthen the stream); 2 = launch counts only (no events: for
+ * counting the launches of a timed region). */
+int pftg_profile_mode(int mode);
 
 /* ---- offline phase: scope table + plans (host) ---------------------------- */
 /* ScopeTable::load (minimax.hpp:50, format minimax.cpp:470-522). */

@@ -17,7 +17,7 @@ PFTG_C64, PFTG_C128 = 0, 1
 
 # Every symbol include/pftg.h declares (checked by tests/test_abi.py).
 EXPORTS = (
-    "pftg_version", "pftg_last_error", "pftg_device_ok", "pftg_profile_begin", "pftg_profile_end", "pftg_profile_isolate",
+    "pftg_version", "pftg_last_error", "pftg_device_ok", "pftg_profile_begin", "pftg_profile_end", "pftg_profile_mode",
     "pftg_table_load", "pftg_table_free", "pftg_table_min_degree",
     "pftg_best_approx", "pftg_table_compute", "pftg_table_save", "pftg_table_info", "pftg_table_record",
     "pftg_measurements_save", "pftg_measurements_info", "pftg_measurements_read",
@@ -134,14 +134,15 @@ KERNEL_NAMES = ("pft_rows_fwd", "pft_cols_fwd", "pft_cols_adj", "pft_rows_adj", 
 
 class KernelProfile:
     """Context manager over pftg_profile_begin/end: per-kernel CUDA-event time.
-    isolate=True spins the stream before each launch (pftg_profile_isolate) so
-    the events time the kernel alone -- for replays outside a timed region."""
+    isolate=True spins the stream before each launch so the events time the
+    kernel alone (replays outside a timed region); count_only=True records no
+    events, only launch counts (safe inside a timed region)."""
 
-    def __init__(self, isolate=False):
-        self.isolate = isolate
+    def __init__(self, isolate=False, count_only=False):
+        self.mode = 2 if count_only else (1 if isolate else 0)
 
     def __enter__(self):
-        check(lib().pftg_profile_isolate(int(self.isolate)))
+        check(lib().pftg_profile_mode(self.mode))
         check(lib().pftg_profile_begin())
         return self
 
@@ -150,7 +151,7 @@ class KernelProfile:
         cnt = (C.c_int * len(KERNEL_NAMES))()
         launches = (C.c_int * len(KERNEL_NAMES))()
         check(lib().pftg_profile_end(ms, cnt, launches))
-        check(lib().pftg_profile_isolate(0))
+        check(lib().pftg_profile_mode(0))
         self.ms = {KERNEL_NAMES[k]: ms[k] for k in range(len(KERNEL_NAMES))}
         self.count = {KERNEL_NAMES[k]: cnt[k] for k in range(len(KERNEL_NAMES))}
         self.launches = {KERNEL_NAMES[k]: launches[k] for k in range(len(KERNEL_NAMES))}

@@ -119,7 +119,7 @@ namespace {
 struct ProfState {
   std::mutex mu;
   bool on = false;
-  bool isolate = false;  // spin before each timed launch (pftg_profile_isolate)
+  int mode = 0;  // pftg_profile_mode: 0 events, 1 events + spin, 2 launch counts only
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
   int launches[K_NUM] = {};
 };
@@ -166,11 +166,11 @@ ProfScope::ProfScope(cudaStream_t s, int k) : kid(k), st(s) {
   {
     std::lock_guard<std::mutex> lock(p.mu);
     ++p.launches[k];
-    if (!p.on) return;
+    if (!p.on || p.mode == 2) return;
   }
   if (capturing(st)) return;
   e0 = new_event();
-  if (prof().isolate) k_prof_spin<<<1, 32, 0, st>>>(30000ull);
+  if (prof().mode == 1) k_prof_spin<<<1, 32, 0, st>>>(30000ull);
   PFTG_CUDA(cudaEventRecord(e0, st));
 }
 
@@ -789,11 +789,12 @@ int pftg_profile_begin(void) {
   });
 }
 
-int pftg_profile_isolate(int on) {
+int pftg_profile_mode(int mode) {
   return guarded([&] {
+    if (mode < 0 || mode > 2) throw std::invalid_argument("pftg_profile_mode: mode must be 0, 1 or 2");
     ProfState& p = prof();
     std::lock_guard<std::mutex> lock(p.mu);
-    p.isolate = on != 0;
+    p.mode = mode;
   });
 }
 
