@@ -116,7 +116,8 @@ enum { E512_FWD = 0, E512_OBJ = 1, E512_PROBE = 2 };
 template <int MODE>
 __global__ void __launch_bounds__(256) ke_rows512_epie(const float2* __restrict__ tw, float2* frame, long long ld,
                                                        const long long* __restrict__ off, float2* probe,
-                                                       float2* X, float2* X2, float scale, float step, int fuse) {
+                                                       float2* X, float2* X2, float scale, float step, int fuse,
+                                                       const long long* __restrict__ off_next) {
   __shared__ float2 tws[256];
   __shared__ __align__(16) float2 sbuf[4][kE512Buf];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) tws[i] = tw[i];
@@ -178,6 +179,19 @@ __global__ void __launch_bounds__(256) ke_rows512_epie(const float2* __restrict_
     pv.x -= step * gr.x;
     pv.y -= step * gr.y;
     prow[c] = pv;
+    a[k] = pv;
+  }
+  if (fuse) {
+    // the next scan position's forward row transform (E512_FWD of position
+    // j+1) from the probe row just updated here: its object rows were final
+    // after the object-update kernel, and this group owns probe row r
+    const float2* nrow = frame + *off_next + (long long)r * ld;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = cmul(a[k], nrow[l + 64 * k]);
+    gsync();  // S free
+    fft512<-1>(a, S, tws, l, gsync);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) X[(size_t)r * 512 + l + 64 * k] = a[k];
   }
 }
 
@@ -291,7 +305,8 @@ __device__ __forceinline__ void fft256(float2 (&a)[8], float2* S, const float2* 
 template <int MODE>
 __global__ void __launch_bounds__(128) ke_rows256_epie(const float2* __restrict__ tw, float2* frame, long long ld,
                                                        const long long* __restrict__ off, float2* probe,
-                                                       float2* X, float2* X2, float scale, float step, int fuse) {
+                                                       float2* X, float2* X2, float scale, float step, int fuse,
+                                                       const long long* __restrict__ off_next) {
   __shared__ float2 tws[128];
   __shared__ __align__(16) float2 sbuf[4][kE256Buf];
   for (int i = threadIdx.x; i < 128; i += blockDim.x) tws[i] = tw[i];
@@ -352,6 +367,16 @@ __global__ void __launch_bounds__(128) ke_rows256_epie(const float2* __restrict_
     pv.x -= step * gr.x;
     pv.y -= step * gr.y;
     prow[c] = pv;
+    a[k] = pv;
+  }
+  if (fuse) {  // next position's forward row transform (see ke_rows512_epie)
+    const float2* nrow = frame + *off_next + (long long)r * ld;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = cmul(a[k], nrow[l + 32 * k]);
+    __syncwarp();
+    fft256<-1>(a, S, tws, l, wsync);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) X[(size_t)r * 256 + l + 32 * k] = a[k];
   }
 }
 

@@ -199,6 +199,7 @@ struct pftg_solver {
   std::vector<double> objective, wall;
   int sweeps_run = 0;
   int flags = 0;
+  bool fwd_ready = false;  // enqueue state: the next position's forward rows are already fused in
   double frame_guard = 0, probe_guard = 0;
   double t_accum = 0;
 
@@ -229,8 +230,11 @@ inline bool use_fft256(const pftg_solver& s) {
   return !off && s.wr == 256 && s.wc == 256;
 }
 
+// jn: the next position in this sweep's visit order (-1 for the last): blind
+// FFT-stage positions fuse the next position's forward row transform into
+// their probe-update kernel (cross-position fusion, 5 -> 4 launches each).
 template <class R>
-void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
+void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
   const cudaStream_t st = s.st;
   const int n1 = (int)s.wr, n2 = (int)s.wc;
   const long long n = (long long)n1 * n2;
@@ -275,9 +279,10 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
       float2* X2 = static_cast<float2*>(s.X2);
       const float* dn = static_cast<const float*>(s.d) + (long long)j * n;
       const float scale = 1.0f / static_cast<float>(n);
-      {
+      if (!s.fwd_ready) {
         ProfScope prof(st, K_FFT_ROWS);
-        ke_rows512_epie<E512_FWD><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, 1.f, 0.f, 0);
+        ke_rows512_epie<E512_FWD><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, 1.f, 0.f, 0,
+                                                         nullptr);
       }
       {
         ProfScope prof(st, K_FFT_COLS);
@@ -286,7 +291,7 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
       {
         ProfScope prof(st, K_FFT_ROWS);
         ke_rows512_epie<E512_OBJ><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, scale,
-                                                       (float)s.cfg.beta, blind ? 1 : 0);
+                                                       (float)s.cfg.beta, blind ? 1 : 0, nullptr);
       }
       if (blind) {
         {
@@ -295,8 +300,10 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
         }
         ProfScope prof(st, K_FFT_ROWS);
         ke_rows512_epie<E512_PROBE><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, scale,
-                                                         (float)s.cfg.gamma, 0);
+                                                         (float)s.cfg.gamma, jn >= 0 ? 1 : 0,
+                                                         jn >= 0 ? s.doffs + jn : nullptr);
       }
+      s.fwd_ready = blind && jn >= 0;
       PFTG_LAUNCH_CHECK();
       return;
     }
@@ -308,9 +315,10 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
       float2* X2 = static_cast<float2*>(s.X2);
       const float* dn = static_cast<const float*>(s.d) + (long long)j * n;
       const float scale = 1.0f / static_cast<float>(n);
-      {
+      if (!s.fwd_ready) {
         ProfScope prof(st, K_FFT_ROWS);
-        ke_rows256_epie<E512_FWD><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, 1.f, 0.f, 0);
+        ke_rows256_epie<E512_FWD><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, 1.f, 0.f, 0,
+                                                        nullptr);
       }
       {
         ProfScope prof(st, K_FFT_COLS);
@@ -319,7 +327,7 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
       {
         ProfScope prof(st, K_FFT_ROWS);
         ke_rows256_epie<E512_OBJ><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, scale,
-                                                      (float)s.cfg.beta, blind ? 1 : 0);
+                                                      (float)s.cfg.beta, blind ? 1 : 0, nullptr);
       }
       if (blind) {
         {
@@ -328,8 +336,10 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
         }
         ProfScope prof(st, K_FFT_ROWS);
         ke_rows256_epie<E512_PROBE><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, scale,
-                                                        (float)s.cfg.gamma, 0);
+                                                        (float)s.cfg.gamma, jn >= 0 ? 1 : 0,
+                                                        jn >= 0 ? s.doffs + jn : nullptr);
       }
+      s.fwd_ready = blind && jn >= 0;
       PFTG_LAUNCH_CHECK();
       return;
     }
@@ -359,7 +369,10 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band) {
 
 template <class R>
 void enqueue_sweep(pftg_solver& s, bool band) {
-  for (std::size_t t = 0; t < s.npos; ++t) enqueue_position<R>(s, s.order[t], band);
+  s.fwd_ready = false;
+  for (std::size_t t = 0; t < s.npos; ++t)
+    enqueue_position<R>(s, s.order[t], band, t + 1 < s.npos ? (long long)s.order[t + 1] : -1);
+  s.fwd_ready = false;
   if (s.cfg.tv_lambda_mag > 0.0 || s.cfg.tv_lambda_phase > 0.0) {
     // solver.cpp:264-279: step lambda * step_scale, step_scale = beta_pft (band) or beta (FFT)
     const double step = band ? s.cfg.beta_pft : s.cfg.beta;
