@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
   }
   __syncthreads();
 
-  const bool fuse_fwd = (EPI == 1) && ep.G2 != nullptr;
+  const bool fuse_fwd = (EPI >= 1) && ep.G2 != nullptr;
   const int n2 = pl.n2;
   const long long row0 = (long long)k1 * Q;
   for (int c = threadIdx.x * V; c < n2; c += blockDim.x * V) {
@@ -487,8 +487,10 @@ __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
         e[v] = cmul(pv, o);
       }
     };
-    // probe update P -= gamma conj(z_j) resid2 (solver.cpp:249-250)
-    auto upd_probe = [&](int l, const C (&z)[V]) {
+    // probe update P -= gamma conj(z_j) resid2 (solver.cpp:249-250); with G2 set
+    // (cross-position fusion) e = the next position's exit wave P' z_next
+    const C* objn = reinterpret_cast<const C*>(ep.obj) + ep.obj_off2 + row0 * ep.obj_ld + c;
+    auto upd_probe = [&](int l, const C (&z)[V], C (&e)[V]) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const C o = obj[(long long)l * ep.obj_ld + v];
@@ -497,14 +499,16 @@ __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
         pv.x -= st * g.x;
         pv.y -= st * g.y;
         pr[(long long)l * n2 + v] = pv;
+        if (fuse_fwd) e[v] = cmul(pv, objn[(long long)l * ep.obj_ld + v]);
       }
     };
-    if (EPI == 1) {
+    if (EPI >= 1) {
       expand_pairs_v<R, Q, RR, V>(
           bp.b1, tv,
           [&](int l, const C (&z)[V]) {
             C e[V];
-            upd_obj(l, z, e);
+            if (EPI == 1) upd_obj(l, z, e);
+            else upd_probe(l, z, e);
             if (fuse_fwd) {
 #pragma unroll
               for (int v = 0; v < V; ++v) {
@@ -519,8 +523,13 @@ __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
           },
           [&](int l, const C (&zl)[V], const C (&zm)[V]) {
             C el[V], em[V];
-            upd_obj(l, zl, el);
-            upd_obj(Q - l, zm, em);
+            if (EPI == 1) {
+              upd_obj(l, zl, el);
+              upd_obj(Q - l, zm, em);
+            } else {
+              upd_probe(l, zl, el);
+              upd_probe(Q - l, zm, em);
+            }
             if (fuse_fwd) {
 #pragma unroll
               for (int v = 0; v < V; ++v) {
@@ -538,12 +547,6 @@ __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
           for (int j = 0; j < RR; ++j) T[(size_t)j * ldT + tc] = acc2[v][j];
         }
       }
-    } else {
-      expand_pairs_v<R, Q, RR, V>(bp.b1, tv, [&](int l, const C (&z)[V]) { upd_probe(l, z); },
-                                  [&](int l, const C (&zl)[V], const C (&zm)[V]) {
-                                    upd_probe(l, zl);
-                                    upd_probe(Q - l, zm);
-                                  });
     }
   }
   if (fuse_fwd) {

@@ -631,7 +631,10 @@ struct EpiArgs {
   long long obj_off;       // element offset of the window's (0,0)
   void* probe;             // [n1][n2]
   double step;             // beta_pft or gamma_pft
-  void* G2;                // EPI 1: fused forward output (may be null)
+  void* G2;                // EPI 1: fused forward output of the new exit wave P z' (may be null);
+                           // EPI 2: fused forward output of the NEXT position's exit wave
+                           //        P' z[obj_off2] (cross-position fusion; may be null)
+  long long obj_off2;      // EPI 2 with G2: element offset of the next position's window
   int vec_ok;              // host-verified 16-byte alignment of out / obj window / probe rows
 };
 
@@ -691,7 +694,7 @@ __global__ void __launch_bounds__(sizeof(R) == 4 ? 512 : 256) k_adj_rows(PftDev<
 
   // A^dagger + epilogue, one column per thread.
   const int q1 = pl.q1, r1 = pl.r1, n2 = pl.n2;
-  const bool fuse_fwd = (EPI == 1) && ep.G2 != nullptr;
+  const bool fuse_fwd = (EPI >= 1) && ep.G2 != nullptr;
   for (int c = threadIdx.x; c < n2; c += blockDim.x) {
     const int tc = c + c / q2;
     C tv[RB];
@@ -734,6 +737,13 @@ __global__ void __launch_bounds__(sizeof(R) == 4 ? 512 : 256) k_adj_rows(PftDev<
         pv.x -= (R)ep.step * g.x;
         pv.y -= (R)ep.step * g.y;
         pr[row * n2 + c] = pv;
+        if (fuse_fwd) {  // next position's exit wave from this thread's own new probe element
+          const C on = reinterpret_cast<const C*>(ep.obj)[ep.obj_off2 + row * ep.obj_ld + c];
+          const C e = cmul(pv, on);
+#pragma unroll
+          for (int j = 0; j < RB; ++j)
+            if (j < r1) bmac(acc2[j], bv[j], e, (j & 1) != 0);
+        }
       }
     }
     if (fuse_fwd) {

@@ -249,7 +249,7 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
     // 16-byte column pairs when the window starts on an even column of an even-width frame
     const int vec = (s.offs[j] % 2 == 0) && (s.fc % 2 == 0) && (s.wc % 2 == 0);
     Src<R> src{frame, (long long)s.fc, 0, doff, probe, vec};
-    launch_fwd_rows<R>(pd, src, static_cast<Cx<R>*>(s.G), 1, st);
+    if (!s.fwd_ready) launch_fwd_rows<R>(pd, src, static_cast<Cx<R>*>(s.G), 1, st);
     launch_fwd_cols<R>(pd, 1, static_cast<Cx<R>*>(s.G), nullptr, dc, mb, static_cast<Cx<R>*>(s.Gt), nullptr, 1, st);
     EpiArgs ep{};
     ep.obj = frame;
@@ -264,9 +264,13 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
       launch_fwd_cols<R>(pd, 1, static_cast<Cx<R>*>(s.G), nullptr, dc, mb, static_cast<Cx<R>*>(s.Gt), nullptr, 1,
                          st);
       ep.step = s.cfg.gamma_pft;
-      ep.G2 = nullptr;
+      // cross-position fusion: the probe-update rows kernel also runs the next
+      // position's forward rows pass (its exit wave P' z_next) into G
+      ep.G2 = jn >= 0 ? s.G : nullptr;
+      ep.obj_off2 = jn >= 0 ? s.offs[jn] : 0;
       launch_adj_rows<R>(pd, 2, static_cast<Cx<R>*>(s.Gt), ep, 1, st);
     }
+    s.fwd_ready = blind && jn >= 0;
     return;
   }
   if constexpr (sizeof(R) == 4) {
