@@ -7,10 +7,12 @@ missing or no sm_100 GPU is present, every compute call raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
-LIB_PATH = HERE / "libpftg.so"
+# PFTG_LIB_PATH: an alternative build (e.g. the -DPFTG_PROFILING library of tools/)
+LIB_PATH = Path(os.environ["PFTG_LIB_PATH"]) if os.environ.get("PFTG_LIB_PATH") else HERE / "libpftg.so"
 
 PFTG_OK, PFTG_EINVAL, PFTG_ELOGIC, PFTG_ERANGE, PFTG_ERUNTIME, PFTG_ECUDA = range(6)
 PFTG_C64, PFTG_C128 = 0, 1

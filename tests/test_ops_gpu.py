@@ -370,3 +370,37 @@ def test_window_bounds_and_operand_checks():
         P.evaluate(frame, patch, np.array([[0, 0], [80, 0]]), d)
     with pytest.raises(ValueError):
         P.evaluate(frame, patch, np.array([[0, 0], [10, 0], [20, 0]]), d)
+
+
+def test_evaluator_cfg5_full_size_chunk_invariance_and_sample(ref):
+    """BASELINE configs[4] at full size (1600 positions of 512^2 complex64 on the
+    4096^2 cfg4 object, band M = 128): the one-call evaluation equals the sum of
+    four position ranges (summation order only), and a sample of positions
+    matches the reference (objective_value / pft_apply_2d in double on the
+    complex64 inputs) within complex64 rounding."""
+    from paper_2408_03532_b200 import problems as PR
+    prob = PR.make_problem("cfg4", seed=0)
+    obj = prob.obj * (1 + 0.05 * torch.randn(prob.obj.shape, dtype=torch.complex64, device="cuda",
+                                            generator=torch.Generator(device="cuda").manual_seed(3)))
+    w, npos = prob.probe.shape[0], len(prob.offsets)
+    assert npos == 1600 and w == 512
+    plan = P.pft_plan_2d(w, w, 64, 64, 64, 64, 1e-3)
+    dcrop = P.crop_centered(prob.d, 64, 64)
+    fs, bs = P.evaluate(obj, prob.probe, prob.offsets, prob.d, (0, npos), plan, dcrop)
+    parts = [P.evaluate(obj, prob.probe, prob.offsets, prob.d, (b, e), plan, dcrop)
+             for b, e in ((0, 400), (400, 800), (800, 1200), (1200, 1600))]
+    assert abs(fs - sum(p[0] for p in parts)) <= 1e-12 * fs
+    assert abs(bs - sum(p[1] for p in parts)) <= 1e-12 * bs
+    o64 = obj.cpu().numpy().astype(np.complex128)
+    p64 = prob.probe.cpu().numpy().astype(np.complex128)
+    d64 = prob.d.cpu().numpy().astype(np.float64)
+    dc = dcrop.cpu().numpy().astype(np.float64)
+    r = ref.RefPlan.create(DATA / "scope_table_v1.txt", w, w, 64, 64, 64, 64, 1e-3)
+    for j in (0, 777, 1599):
+        gf, gb = P.evaluate(obj, prob.probe, prob.offsets, prob.d, (j, j + 1), plan, dcrop)
+        o = prob.offsets[j]
+        want_f = ref.objective_value(o64, p64, [o], d64[j:j + 1])
+        ex = p64 * o64[o[0]:o[0] + w, o[1]:o[1] + w]
+        want_b = np.sum((np.abs(r.apply(ex)) - dc[j]) ** 2)
+        assert abs(gf - want_f) <= 1e-4 * want_f, (j, gf, want_f)
+        assert abs(gb - want_b) <= 1e-4 * want_b, (j, gb, want_b)

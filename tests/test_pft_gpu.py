@@ -315,3 +315,24 @@ def test_pft_apply_1d_edge_cases(ref):
     d[0] = 1
     out = P.pft_apply_1d(g, d).cpu().numpy()
     assert np.max(np.abs(out - 1)) <= 2e-7
+
+
+def test_full_cfg2_size_linearity_and_dot_test():
+    """Size-independent properties at the full BASELINE configs[1] size (64 x
+    1024^2 complex64, M = 256) on the well-conditioned companion plan (p = 128,
+    q = 8, r = 13): linearity A(x + 2y) = A x + 2 A y and the adjoint identity
+    <A x, y> = <x, A* y>, both within complex64 rounding."""
+    g = P.pft_plan_2d(1024, 1024, 128, 128, 128, 128, 1e-7)
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.randn((64, 1024, 1024), dtype=torch.complex64, device="cuda", generator=gen)
+    y = torch.randn((64, 1024, 1024), dtype=torch.complex64, device="cuda", generator=gen)
+    ax, ay = P.pft_apply_2d(g, x), P.pft_apply_2d(g, y)
+    axy = P.pft_apply_2d(g, x + 2 * y)
+    lin = (torch.linalg.vector_norm(axy - (ax + 2 * ay)) / torch.linalg.vector_norm(axy)).item()
+    assert lin <= 1e-5, lin
+    v = torch.randn((64, 256, 256), dtype=torch.complex64, device="cuda", generator=gen)
+    atv = P.pft_adjoint_2d(g, v)
+    lhs = torch.sum(ax.to(torch.complex128) * v.conj().to(torch.complex128), dim=(1, 2))
+    rhs = torch.sum(x.to(torch.complex128) * atv.conj().to(torch.complex128), dim=(1, 2))
+    rel = (torch.abs(lhs - rhs) / torch.abs(lhs)).max().item()
+    assert rel <= 1e-4, rel
