@@ -136,6 +136,11 @@ int pftg_adjoint_2d_dev(const pftg_plan* plan, int dtype, const void* band, void
  * batch (pinned host memory recommended). */
 int pftg_apply_2d_host(const pftg_plan* plan, int dtype, const void* z, void* band, size_t batch);
 int pftg_adjoint_2d_host(const pftg_plan* plan, int dtype, const void* band, void* z, size_t batch);
+/* BASELINE configs[1] in one streamed call: band = pft_apply_2d(z) and
+ * back = pft_adjoint_2d(band) per field, host buffers, chunks pipelined on two
+ * streams so H2D and D2H copies overlap (full-duplex PCIe). Results are
+ * bit-identical to the two separate calls. */
+int pftg_fwd_adj_2d_host(const pftg_plan* plan, int dtype, const void* z, void* band, void* back, size_t batch);
 
 /* band_residual (solver.hpp:63): A*(A x - dcrop .* exp(i arg(A x))), batched;
  * dcrop is real [batch][2mt1][2mt2]. */

@@ -7,7 +7,7 @@ the reference's operator API. There is no CPU fallback.
 from ._lib import CudaError, LIB_PATH  # noqa: F401
 from .pft import (  # noqa: F401
     DEFAULT_TABLE, PftPlan1D, PftPlan2D, ScopeTable, band_residual, crop_centered, fast_fft2,
-    fast_ifft2, best_approx, pft_adjoint_2d, pft_apply_1d, pft_apply_2d, pft_plan_1d, pft_plan_2d)
+    fast_ifft2, best_approx, pft_adjoint_2d, pft_fwd_adj_2d, pft_apply_1d, pft_apply_2d, pft_plan_1d, pft_plan_2d)
 from .solver import (  # noqa: F401
     ReconResult, Solver, SolverConfig, epie_probe_update, evaluate, hybrid_solve,
     objective_value, pie_object_update, project_modulus, set_window, solve_epie, solve_pie,

@@ -25,7 +25,7 @@ EXPORTS = (
     "pftg_measurements_save", "pftg_measurements_info", "pftg_measurements_read",
     "pftg_plan_2d", "pftg_plan_from_tables", "pftg_plan_load", "pftg_plan_save", "pftg_plan_free", "pftg_plan_info",
     "pftg_plan_tables",
-    "pftg_apply_2d_dev", "pftg_adjoint_2d_dev", "pftg_apply_2d_host", "pftg_adjoint_2d_host",
+    "pftg_apply_2d_dev", "pftg_adjoint_2d_dev", "pftg_apply_2d_host", "pftg_adjoint_2d_host", "pftg_fwd_adj_2d_host",
     "pftg_band_residual_dev",
     "pftg_fft2_dev", "pftg_fft2_host", "pftg_project_modulus_dev", "pftg_crop_centered_dev",
     "pftg_window_slice_dev", "pftg_set_window_dev", "pftg_pie_object_update_dev",
@@ -86,6 +86,7 @@ def lib():
     L.pftg_adjoint_2d_dev.argtypes = [vp, C.c_int, vp, vp, sz, vp]
     L.pftg_apply_2d_host.argtypes = [vp, C.c_int, vp, vp, sz]
     L.pftg_adjoint_2d_host.argtypes = [vp, C.c_int, vp, vp, sz]
+    L.pftg_fwd_adj_2d_host.argtypes = [vp, C.c_int, vp, vp, vp, sz]
     L.pftg_band_residual_dev.argtypes = [vp, C.c_int, vp, vp, vp, sz, vp]
     L.pftg_fft2_dev.argtypes = [C.c_int, vp, vp, sz, sz, sz, C.c_int, vp]
     L.pftg_fft2_host.argtypes = [C.c_int, vp, vp, sz, sz, sz, C.c_int]

@@ -265,6 +265,25 @@ def pft_apply_1d(plan: PftPlan1D, z):
     return out
 
 
+def pft_fwd_adj_2d(plan: "PftPlan2D", z):
+    """BASELINE configs[1] in one call: (band, back) = (pft_apply_2d(z),
+    pft_adjoint_2d(band)). Host numpy input: one streamed C-ABI call
+    (pftg_fwd_adj_2d_host, H2D and D2H overlapped); CUDA tensors: the two
+    device calls. Bit-identical to calling the two operators in turn."""
+    if isinstance(z, np.ndarray):
+        if tuple(z.shape[-2:]) != plan.field_shape:
+            raise ValueError("pft_apply_2d: z shape must match the plan")
+        z = np.ascontiguousarray(z)
+        b = _batch(z, plan.field_shape)
+        band = np.empty(z.shape[:-2] + plan.band_shape, z.dtype)
+        back = np.empty(z.shape, z.dtype)
+        check(lib().pftg_fwd_adj_2d_host(plan._h, _dtype_code(z), z.ctypes.data, band.ctypes.data,
+                                         back.ctypes.data, b))
+        return band, back
+    band = pft_apply_2d(plan, z)
+    return band, pft_adjoint_2d(plan, band)
+
+
 def pft_plan_2d(n1, n2, mt1, mt2, p1, p2, eps, table: ScopeTable | None = None) -> PftPlan2D:
     """pft::pft_plan_2d (pft.hpp:49-51; pft.cpp:33-76,103-112)."""
     table = table or ScopeTable.load()

@@ -174,6 +174,9 @@ def test_host_buffer_path_matches_device(ref):
     hz = P.pft_adjoint_2d(g, hb)
     dz = P.pft_adjoint_2d(g, torch.from_numpy(hb).cuda()).cpu().numpy()
     assert np.array_equal(hz, dz)
+    # the streamed forward + adjoint call (BASELINE configs[1] as one call)
+    fb, fz = P.pft_fwd_adj_2d(g, z)
+    assert np.array_equal(fb, hb) and np.array_equal(fz, hz)
 
 
 def test_dot_test_c128():
