@@ -390,8 +390,33 @@ __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
   fast_stage_b_to_g<R, Q, RR, P>(pl, bp, T, W2s, tw2s, Gblk);
 }
 
+// One-element asynchronous global -> shared copy (LDGSTS: 8 bytes for
+// complex64, 16 for complex128) and its group fences
+template <class C>
+__device__ __forceinline__ void pf_cp(C* smem, const C* gmem) {
+  if constexpr (sizeof(C) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void pf_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void pf_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Shared-memory bytes of the ePIE epilogue prefetch (PF = 1): probe, object
+// window and (EPI 2) next object window rows of one row block.
+template <class R>
+__host__ inline size_t adj_prefetch_smem(int n2, int q) {
+  return 3 * sizeof(typename CT<R>::C) * (size_t)q * n2 + 16;
+}
+
 // Adjoint rows pass (+ ePIE epilogues), mirror of k_adj_rows with pairing.
-template <class R, int Q, int RR, int P, int V, int EPI>
+// PF = 1 (ePIE epilogues): the row block's probe / object window rows (and
+// the next position's window rows for the EPI 2 fused forward) are copied
+// into shared memory with cp.async at kernel entry, overlapping the D-dagger /
+// FFT phase -- the epilogue then runs on shared memory instead of one L2
+// round trip per expanded row (it was 5.7 us of a cfg4 position's 12 us
+// kernel, tools/band_dbg.sh).
+template <class R, int Q, int RR, int P, int V, int EPI, int PF = 0>
 __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
     kf_adj_rows(PftDev<R> pl, BPar<R, Q, RR> bp, const typename CT<R>::C* __restrict__ Gt, EpiArgs ep) {
   using C = typename CT<R>::C;
@@ -400,8 +425,26 @@ __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
   const int ldT = ldT_of(pl.n2, Q);
   C* W2s = T + (size_t)RR * ldT;
   C* tw2s = W2s + (size_t)RR * pl.M2;
-  fast_load_tables(pl, W2s, tw2s);
   const int k1 = blockIdx.x, f = blockIdx.y;
+  C* pfP = smem_after<C>(smem_raw, tw2s + P / 2 + 1, 16);  // [Q][n2] probe rows (PF)
+  C* pfO = pfP + (size_t)Q * pl.n2;                         // object window rows
+  C* pfN = pfO + (size_t)Q * pl.n2;                         // next window rows (EPI 2 + G2)
+  if constexpr (PF && EPI >= 1) {
+    const int n2 = pl.n2;
+    const long long r0 = (long long)k1 * Q;
+    const C* pg = reinterpret_cast<const C*>(ep.probe) + r0 * n2;
+    const C* og = reinterpret_cast<const C*>(ep.obj) + ep.obj_off + r0 * ep.obj_ld;
+    const C* ng = reinterpret_cast<const C*>(ep.obj) + ep.obj_off2 + r0 * ep.obj_ld;
+    const bool nxt = EPI == 2 && ep.G2 != nullptr;
+    for (int i = threadIdx.x; i < Q * n2; i += blockDim.x) {
+      const int l = i / n2, c = i - l * n2;
+      pf_cp(pfP + i, pg + (long long)l * n2 + c);
+      pf_cp(pfO + i, og + (long long)l * ep.obj_ld + c);
+      if (nxt) pf_cp(pfN + i, ng + (long long)l * ep.obj_ld + c);
+    }
+    pf_commit();
+  }
+  fast_load_tables(pl, W2s, tw2s);
   const C* Gblk = Gt + ((size_t)f * pl.p1 + k1) * RR * pl.M2;
   __syncthreads();
 
@@ -412,7 +455,7 @@ __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int lig = lane & (PL - 1), giw = lane / PL;
   const int M2 = pl.M2, mt2 = pl.mt2;
-  for (int base = warp * GPW; base < RR; base += nwarps * GPW) {
+  for (int base = warp * GPW; base < RR && !PFTG_DBG(ep.dbg, 1); base += nwarps * GPW) {
     const int j1 = base + giw;
     const bool valid = j1 < RR;
     C x[S][RR];
@@ -443,7 +486,11 @@ __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
   const bool fuse_fwd = (EPI >= 1) && ep.G2 != nullptr;
   const int n2 = pl.n2;
   const long long row0 = (long long)k1 * Q;
-  for (int c = threadIdx.x * V; c < n2; c += blockDim.x * V) {
+  if constexpr (PF && EPI >= 1) {
+    pf_wait_all();
+    __syncthreads();
+  }
+  for (int c = threadIdx.x * V; c < n2 && !PFTG_DBG(ep.dbg, 4); c += blockDim.x * V) {
     C tv[V][RR];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -468,6 +515,9 @@ __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
     }
     C* obj = reinterpret_cast<C*>(ep.obj) + ep.obj_off + row0 * ep.obj_ld + c;
     C* pr = reinterpret_cast<C*>(ep.probe) + row0 * n2 + c;
+    // reads of the row block's probe / object / next-window elements (l = row in block)
+    auto ld_p = [&](int l, int v) { return PF ? pfP[(size_t)l * n2 + c + v] : pr[(long long)l * n2 + v]; };
+    auto ld_o = [&](int l, int v) { return PF ? pfO[(size_t)l * n2 + c + v] : obj[(long long)l * ep.obj_ld + v]; };
     const R st = (R)ep.step;
     C acc2[V][RR];
 #pragma unroll
@@ -478,8 +528,8 @@ __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
     auto upd_obj = [&](int l, const C (&z)[V], C (&e)[V]) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        const C pv = pr[(long long)l * n2 + v];
-        C o = obj[(long long)l * ep.obj_ld + v];
+        const C pv = ld_p(l, v);
+        C o = ld_o(l, v);
         const C g = cmulc(pv, z[v]);
         o.x -= st * g.x;
         o.y -= st * g.y;
@@ -493,13 +543,13 @@ __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
     auto upd_probe = [&](int l, const C (&z)[V], C (&e)[V]) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        const C o = obj[(long long)l * ep.obj_ld + v];
-        C pv = pr[(long long)l * n2 + v];
+        const C o = ld_o(l, v);
+        C pv = ld_p(l, v);
         const C g = cmulc(o, z[v]);
         pv.x -= st * g.x;
         pv.y -= st * g.y;
         pr[(long long)l * n2 + v] = pv;
-        if (fuse_fwd) e[v] = cmul(pv, objn[(long long)l * ep.obj_ld + v]);
+        if (fuse_fwd) e[v] = cmul(pv, PF ? pfN[(size_t)l * n2 + c + v] : objn[(long long)l * ep.obj_ld + v]);
       }
     };
     if (EPI >= 1) {
@@ -549,7 +599,7 @@ __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
       }
     }
   }
-  if (fuse_fwd) {
+  if (fuse_fwd && !PFTG_DBG(ep.dbg, 2)) {
     __syncthreads();
     C* G2blk = reinterpret_cast<C*>(ep.G2) + ((size_t)f * pl.p1 + k1) * RR * pl.M2;
     fast_stage_b_to_g<R, Q, RR, P>(pl, bp, T, W2s, tw2s, G2blk);

@@ -636,6 +636,7 @@ struct EpiArgs {
                            //        P' z[obj_off2] (cross-position fusion; may be null)
   long long obj_off2;      // EPI 2 with G2: element offset of the next position's window
   int vec_ok;              // host-verified 16-byte alignment of out / obj window / probe rows
+  int dbg;                 // profiling build only (PFTG_DEBUG_ADJ): skip P1 (1) / fused stage B (2) / epilogue (4)
 };
 
 template <class R, int S2, int RB, int EPI>

@@ -353,19 +353,32 @@ bool fast_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, 
     const auto bp = make_bpar<R_, Q, RR>(pd);
     const bool vec = sizeof(R_) == 4 && ep.vec_ok && (pd.n2 % 2 == 0);
     const dim3 grid(pd.p1, batch);
-    auto go = [&](auto kern) {
+    // ePIE epilogues: prefetch the row block's probe / window rows when they fit
+    const size_t smem_pf = smem + 16 + adj_prefetch_smem<R_>(pd.n2, Q);
+    const bool pf = epi >= 1 && smem_pf <= 227 * 1024 && !knobs().no_prefetch;
+    auto go = [&](auto kern, size_t sm) {
       allow_smem(kern);
-      kern<<<grid, fast_nt<RR, P>(), smem, st>>>(pd, bp, Gt, ep);
+      kern<<<grid, fast_nt<RR, P>(), sm, st>>>(pd, bp, Gt, ep);
     };
     if (epi == 0) {
-      if (vec) go(kf_adj_rows<R_, Q, RR, P, VV, 0>);
-      else go(kf_adj_rows<R_, Q, RR, P, 1, 0>);
+      if (vec) go(kf_adj_rows<R_, Q, RR, P, VV, 0>, smem);
+      else go(kf_adj_rows<R_, Q, RR, P, 1, 0>, smem);
     } else if (epi == 1) {
-      if (vec) go(kf_adj_rows<R_, Q, RR, P, VV, 1>);
-      else go(kf_adj_rows<R_, Q, RR, P, 1, 1>);
+      if (pf) {
+        if (vec) go(kf_adj_rows<R_, Q, RR, P, VV, 1, 1>, smem_pf);
+        else go(kf_adj_rows<R_, Q, RR, P, 1, 1, 1>, smem_pf);
+      } else {
+        if (vec) go(kf_adj_rows<R_, Q, RR, P, VV, 1>, smem);
+        else go(kf_adj_rows<R_, Q, RR, P, 1, 1>, smem);
+      }
     } else {
-      if (vec) go(kf_adj_rows<R_, Q, RR, P, VV, 2>);
-      else go(kf_adj_rows<R_, Q, RR, P, 1, 2>);
+      if (pf) {
+        if (vec) go(kf_adj_rows<R_, Q, RR, P, VV, 2, 1>, smem_pf);
+        else go(kf_adj_rows<R_, Q, RR, P, 1, 2, 1>, smem_pf);
+      } else {
+        if (vec) go(kf_adj_rows<R_, Q, RR, P, VV, 2>, smem);
+        else go(kf_adj_rows<R_, Q, RR, P, 1, 2>, smem);
+      }
     }
   });
 }

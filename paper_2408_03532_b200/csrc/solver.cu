@@ -259,6 +259,7 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
     ep.step = s.cfg.beta_pft;
     ep.G2 = blind ? s.G : nullptr;
     ep.vec_ok = vec;
+    ep.dbg = knobs().debug_adj;
     launch_adj_rows<R>(pd, 1, static_cast<Cx<R>*>(s.Gt), ep, 1, st);
     if (blind) {
       launch_fwd_cols<R>(pd, 1, static_cast<Cx<R>*>(s.G), nullptr, dc, mb, static_cast<Cx<R>*>(s.Gt), nullptr, 1,
