@@ -550,8 +550,10 @@ __device__ __forceinline__ void block_sum_store(double v, double* scratch, doubl
 // MODE 1: forward cols -> band residual vs dcrop -> adjoint cols -> Gout.
 // MODE 2: forward cols -> sum (|band| - dcrop)^2 per CTA into partial.
 // grid = (ceil(M2/nb), batch).
-template <class R, int S1, int RB, int MODE>
-__global__ void __launch_bounds__(256, 3) k_fwd_cols(PftDev<R> pl, const typename CT<R>::C* __restrict__ G,
+// NT = 320: single-column strips (one ePIE position) run one warp per j1 for
+// r1 <= 10, so each lane-group FFT phase is one round instead of two.
+template <class R, int S1, int RB, int MODE, int NT = 256>
+__global__ void __launch_bounds__(NT, NT == 256 ? 3 : 2) k_fwd_cols(PftDev<R> pl, const typename CT<R>::C* __restrict__ G,
                                                   typename CT<R>::C* __restrict__ band,
                                                   const R* __restrict__ dcrop, long long dstride,
                                                   typename CT<R>::C* __restrict__ Gout,

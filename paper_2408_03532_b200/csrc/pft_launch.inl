@@ -480,9 +480,15 @@ void launch_fwd_cols<R_>(const PftDev<R_>& pd, int mode, const typename CT<R_>::
       allow_smem(k);
       k<<<grid, 256, smem, st>>>(pl, G, band, dc, dstride, Gout, partial);
     } else if (mode == 1) {
-      auto k = k_fwd_cols<R_, S, RB, 1>;
-      allow_smem(k);
-      k<<<grid, 256, smem, st>>>(pl, G, band, dc, dstride, Gout, partial);
+      if (pl.nb == 1 && pd.r1 > 8 && pd.r1 <= 10) {  // one warp per j1 (single-column strips)
+        auto k = k_fwd_cols<R_, S, RB, 1, 320>;
+        allow_smem(k);
+        k<<<grid, 32 * pd.r1, smem, st>>>(pl, G, band, dc, dstride, Gout, partial);
+      } else {
+        auto k = k_fwd_cols<R_, S, RB, 1>;
+        allow_smem(k);
+        k<<<grid, 256, smem, st>>>(pl, G, band, dc, dstride, Gout, partial);
+      }
     } else {
       auto k = k_fwd_cols<R_, S, RB, 2>;
       allow_smem(k);
