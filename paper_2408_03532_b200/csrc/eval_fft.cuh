@@ -115,31 +115,36 @@ enum { E512_FWD = 0, E512_OBJ = 1, E512_PROBE = 2 };
 // frame + *off: the window (row stride ld); X: rows in, X2: fused forward out (E512_OBJ).
 template <int MODE>
 __global__ void __launch_bounds__(256) ke_rows512_epie(const float2* __restrict__ tw, float2* frame, long long ld,
-                                                       const long long* __restrict__ off, float2* probe,
+                                                       long long off, float2* probe,
                                                        float2* X, float2* X2, float scale, float step, int fuse,
-                                                       const long long* __restrict__ off_next) {
+                                                       long long off_next) {
+  // window offsets by value (graph node parameters) and the row loads issued
+  // before the twiddle-table barrier: one L2 round trip before the first pass
   __shared__ float2 tws[256];
   __shared__ __align__(16) float2 sbuf[4][kE512Buf];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) tws[i] = tw[i];
-  __syncthreads();
   const int g = threadIdx.x >> 6, l = threadIdx.x & 63;
   const int r = blockIdx.x * 4 + g;
   float2* S = sbuf[g];
   auto gsync = [&]() { named_sync(1 + g, 64); };
-  float2* orow = frame + *off + (long long)r * ld;
+  float2* orow = frame + off + (long long)r * ld;
   float2* prow = probe + (size_t)r * 512;
   float2 a[8];
   if (MODE == E512_FWD) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) a[k] = cmul(prow[l + 64 * k], orow[l + 64 * k]);
+  } else {
+    const float2* xin = (MODE == E512_OBJ ? X : X2) + (size_t)r * 512;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = xin[l + 64 * k];
+  }
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tws[i] = tw[i];
+  __syncthreads();
+  if (MODE == E512_FWD) {
     fft512<-1>(a, S, tws, l, gsync);
 #pragma unroll
     for (int k = 0; k < 8; ++k) X[(size_t)r * 512 + l + 64 * k] = a[k];
     return;
   }
-  const float2* xin = (MODE == E512_OBJ ? X : X2) + (size_t)r * 512;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) a[k] = xin[l + 64 * k];
   fft512<+1>(a, S, tws, l, gsync);
   if (MODE == E512_OBJ) {
 #pragma unroll
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(256) ke_rows512_epie(const float2* __restrict_
     // the next scan position's forward row transform (E512_FWD of position
     // j+1) from the probe row just updated here: its object rows were final
     // after the object-update kernel, and this group owns probe row r
-    const float2* nrow = frame + *off_next + (long long)r * ld;
+    const float2* nrow = frame + off_next + (long long)r * ld;
 #pragma unroll
     for (int k = 0; k < 8; ++k) a[k] = cmul(a[k], nrow[l + 64 * k]);
     gsync();  // S free
@@ -304,31 +309,34 @@ __device__ __forceinline__ void fft256(float2 (&a)[8], float2* S, const float2* 
 // warps, one window row each; the group barrier is a warp barrier).
 template <int MODE>
 __global__ void __launch_bounds__(128) ke_rows256_epie(const float2* __restrict__ tw, float2* frame, long long ld,
-                                                       const long long* __restrict__ off, float2* probe,
+                                                       long long off, float2* probe,
                                                        float2* X, float2* X2, float scale, float step, int fuse,
-                                                       const long long* __restrict__ off_next) {
+                                                       long long off_next) {
   __shared__ float2 tws[128];
   __shared__ __align__(16) float2 sbuf[4][kE256Buf];
-  for (int i = threadIdx.x; i < 128; i += blockDim.x) tws[i] = tw[i];
-  __syncthreads();
   const int g = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int r = blockIdx.x * 4 + g;
   float2* S = sbuf[g];
   auto wsync = []() { __syncwarp(); };
-  float2* orow = frame + *off + (long long)r * ld;
+  float2* orow = frame + off + (long long)r * ld;
   float2* prow = probe + (size_t)r * 256;
   float2 a[8];
   if (MODE == E512_FWD) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) a[k] = cmul(prow[l + 32 * k], orow[l + 32 * k]);
+  } else {
+    const float2* xin = (MODE == E512_OBJ ? X : X2) + (size_t)r * 256;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = xin[l + 32 * k];
+  }
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) tws[i] = tw[i];
+  __syncthreads();
+  if (MODE == E512_FWD) {
     fft256<-1>(a, S, tws, l, wsync);
 #pragma unroll
     for (int k = 0; k < 8; ++k) X[(size_t)r * 256 + l + 32 * k] = a[k];
     return;
   }
-  const float2* xin = (MODE == E512_OBJ ? X : X2) + (size_t)r * 256;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) a[k] = xin[l + 32 * k];
   fft256<+1>(a, S, tws, l, wsync);
   if (MODE == E512_OBJ) {
 #pragma unroll
@@ -370,7 +378,7 @@ __global__ void __launch_bounds__(128) ke_rows256_epie(const float2* __restrict_
     a[k] = pv;
   }
   if (fuse) {  // next position's forward row transform (see ke_rows512_epie)
-    const float2* nrow = frame + *off_next + (long long)r * ld;
+    const float2* nrow = frame + off_next + (long long)r * ld;
 #pragma unroll
     for (int k = 0; k < 8; ++k) a[k] = cmul(a[k], nrow[l + 32 * k]);
     __syncwarp();

@@ -286,8 +286,8 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
       const float scale = 1.0f / static_cast<float>(n);
       if (!s.fwd_ready) {
         ProfScope prof(st, K_FFT_ROWS);
-        ke_rows512_epie<E512_FWD><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, 1.f, 0.f, 0,
-                                                         nullptr);
+        ke_rows512_epie<E512_FWD><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, 1.f, 0.f, 0,
+                                                         0);
       }
       {
         ProfScope prof(st, K_FFT_COLS);
@@ -295,8 +295,8 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
       }
       {
         ProfScope prof(st, K_FFT_ROWS);
-        ke_rows512_epie<E512_OBJ><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, scale,
-                                                       (float)s.cfg.beta, blind ? 1 : 0, nullptr);
+        ke_rows512_epie<E512_OBJ><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
+                                                       (float)s.cfg.beta, blind ? 1 : 0, 0);
       }
       if (blind) {
         {
@@ -304,9 +304,9 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
           ke_cols512_proj<4><<<128, 256, 0, st>>>(X2, dn, tw);
         }
         ProfScope prof(st, K_FFT_ROWS);
-        ke_rows512_epie<E512_PROBE><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, scale,
+        ke_rows512_epie<E512_PROBE><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
                                                          (float)s.cfg.gamma, jn >= 0 ? 1 : 0,
-                                                         jn >= 0 ? s.doffs + jn : nullptr);
+                                                         jn >= 0 ? s.offs[jn] : 0);
       }
       s.fwd_ready = blind && jn >= 0;
       PFTG_LAUNCH_CHECK();
@@ -322,8 +322,8 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
       const float scale = 1.0f / static_cast<float>(n);
       if (!s.fwd_ready) {
         ProfScope prof(st, K_FFT_ROWS);
-        ke_rows256_epie<E512_FWD><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, 1.f, 0.f, 0,
-                                                        nullptr);
+        ke_rows256_epie<E512_FWD><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, 1.f, 0.f, 0,
+                                                        0);
       }
       {
         ProfScope prof(st, K_FFT_COLS);
@@ -331,8 +331,8 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
       }
       {
         ProfScope prof(st, K_FFT_ROWS);
-        ke_rows256_epie<E512_OBJ><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, scale,
-                                                      (float)s.cfg.beta, blind ? 1 : 0, nullptr);
+        ke_rows256_epie<E512_OBJ><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
+                                                      (float)s.cfg.beta, blind ? 1 : 0, 0);
       }
       if (blind) {
         {
@@ -340,9 +340,9 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
           ke_cols256_proj<4><<<64, 128, 0, st>>>(X2, dn, tw);
         }
         ProfScope prof(st, K_FFT_ROWS);
-        ke_rows256_epie<E512_PROBE><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, doff, pr, X, X2, scale,
+        ke_rows256_epie<E512_PROBE><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
                                                         (float)s.cfg.gamma, jn >= 0 ? 1 : 0,
-                                                        jn >= 0 ? s.doffs + jn : nullptr);
+                                                        jn >= 0 ? s.offs[jn] : 0);
       }
       s.fwd_ready = blind && jn >= 0;
       PFTG_LAUNCH_CHECK();
