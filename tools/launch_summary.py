@@ -16,7 +16,8 @@ def main(path, only_ours=True):
         if only_ours and ("at::" in name or "native" in name):
             continue
         v = float(r[vi].replace(",", ""))
-        v = v / 1e3 if r[ui] == "nsecond" else (v * 1e3 if r[ui] == "msecond" else v)
+        u = r[ui]
+        v = v / 1e3 if u in ("nsecond", "ns") else (v * 1e3 if u in ("msecond", "ms") else v)
         n, t = agg.get(name, (0, 0.0))
         agg[name] = (n + 1, t + v)
     tot = sum(t for _, t in agg.values())

@@ -37,7 +37,7 @@ def main(path):
             v = float(r[i].replace(",", ""))
             u = units[i]
             if k == "time_us":
-                v = v / 1000.0 if u == "nsecond" else v * (1000.0 if u == "msecond" else 1.0)
+                v = v / 1000.0 if u in ("nsecond", "ns") else v * (1000.0 if u in ("msecond", "ms") else 1.0)
             if k.endswith("_MB"):
                 scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1e-6)
                 v = v * scale
