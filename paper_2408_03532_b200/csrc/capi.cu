@@ -47,6 +47,7 @@ const Knobs& knobs() {
     o.no_tile = on("PFTG_NO_TILE");
     o.force_tile = on("PFTG_TILE");
     o.host_chunk_mb = num("PFTG_HOST_CHUNK_MB");
+    o.no_persist = on("PFTG_NO_PERSIST");
     o.no_prefetch = on("PFTG_NO_PREFETCH");
 #ifdef PFTG_PROFILING
     o.debug_tma = num("PFTG_DEBUG_TMA");

@@ -43,6 +43,7 @@ struct Knobs {
   bool eval_one_stream;   // evaluator: FFT and PFT chains on one stream
   bool no_tile, force_tile;  // small-batch tile path (pft_tile.cu): off / forced
   int host_chunk_mb;         // host-buffer pipelines: MB per copy (0 = 32)
+  bool no_persist;           // ePIE full-FFT stage: per-position kernel graph instead of the persistent sweep
   bool no_prefetch;          // ePIE adjoint-rows epilogue without the shared-memory prefetch
   int debug_tma, debug_ws, debug_adj, debug_cols, debug_adjcols;
   bool debug_wide_adj;

@@ -31,6 +31,7 @@
 #include <stdexcept>
 #include <vector>
 
+#include "epie_sweep.cuh"
 #include "eval_fft.cuh"
 #include "../../include/pftg.h"
 #include "internal.hpp"
@@ -182,6 +183,7 @@ struct pftg_solver {
   void* probe = nullptr;
   void* prev = nullptr;
   void* tv = nullptr;  // TV step output (frame-sized)
+  unsigned* bar = nullptr;  // grid-barrier counter of the persistent FFT-stage sweep
   void* d = nullptr;
   void* dperm = nullptr;
   void* dcrop = nullptr;
@@ -206,7 +208,7 @@ struct pftg_solver {
   ~pftg_solver() {
     for (auto& g : graph)
       if (g) cudaGraphExecDestroy(g);
-    void* bufs[] = {frame, probe, prev, tv, d, dperm, dcrop, doffs, G, Gt, X, X2, Xe, part, red};
+    void* bufs[] = {frame, probe, prev, tv, bar, d, dperm, dcrop, doffs, G, Gt, X, X2, Xe, part, red};
     for (void* b : bufs)
       if (b) cudaFree(b);
     if (st) cudaStreamDestroy(st);
@@ -373,11 +375,66 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
 }
 
 template <class R>
+void enqueue_positions(pftg_solver& s, bool band);
+template <class R>
+void enqueue_tv(pftg_solver& s, bool band);
+
+// Full-FFT stage, complex64 256^2 / 512^2 windows, list order: the whole sweep
+// as one cooperative persistent kernel (epie_sweep.cuh). PFTG_NO_PERSIST=1 keeps
+// the per-position graph of four kernels.
+template <class R>
+bool persistent_fft(const pftg_solver& s, bool band) {
+  return sizeof(R) == 4 && !band && !s.cfg.shuffled && !knobs().no_persist && (use_fft512(s) || use_fft256(s));
+}
+
+template <class R>
+void launch_persistent_fft(pftg_solver& s) {
+  int dev = 0, nsm = 0, coop = 0;
+  PFTG_CUDA(cudaGetDevice(&dev));
+  PFTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  PFTG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  if (!coop) throw cuda_error("pftg: cooperative launch unsupported");
+  const int W = (int)s.wr;
+  const float2* tw = fft_twiddles<float>(W);
+  float2* fr = static_cast<float2*>(s.frame);
+  float2* pr = static_cast<float2*>(s.probe);
+  float2* X = static_cast<float2*>(s.X);
+  float2* X2 = static_cast<float2*>(s.X2);
+  const float* d = static_cast<const float*>(s.d);
+  long long ld = (long long)s.fc;
+  const long long* offs = s.doffs;
+  int npos = (int)s.npos;
+  float scale = 1.0f / static_cast<float>((long long)W * W), beta = (float)s.cfg.beta, gamma = (float)s.cfg.gamma;
+  unsigned* bar = s.bar;
+  void* args[] = {&tw, &fr, &ld, &offs, &npos, &pr, &X, &X2, &d, &scale, &beta, &gamma, &bar};
+  const bool blind = s.cfg.blind != 0;
+  void* k = W == 512 ? (blind ? (void*)ke_epie_sweep<512, 1> : (void*)ke_epie_sweep<512, 0>)
+                     : (blind ? (void*)ke_epie_sweep<256, 1> : (void*)ke_epie_sweep<256, 0>);
+  PFTG_CUDA(cudaMemsetAsync(s.bar, 0, sizeof(unsigned), s.st));
+  ProfScope prof(s.st, K_FFT_ROWS);
+  PFTG_CUDA(cudaLaunchCooperativeKernel(k, dim3(nsm), dim3(256), args, 0, s.st));
+}
+
+template <class R>
 void enqueue_sweep(pftg_solver& s, bool band) {
+  if (persistent_fft<R>(s, band)) {
+    if constexpr (sizeof(R) == 4) launch_persistent_fft<R>(s);
+  } else {
+    enqueue_positions<R>(s, band);
+  }
+  enqueue_tv<R>(s, band);
+}
+
+template <class R>
+void enqueue_positions(pftg_solver& s, bool band) {
   s.fwd_ready = false;
   for (std::size_t t = 0; t < s.npos; ++t)
     enqueue_position<R>(s, s.order[t], band, t + 1 < s.npos ? (long long)s.order[t + 1] : -1);
   s.fwd_ready = false;
+}
+
+template <class R>
+void enqueue_tv(pftg_solver& s, bool band) {
   if (s.cfg.tv_lambda_mag > 0.0 || s.cfg.tv_lambda_phase > 0.0) {
     // solver.cpp:264-279: step lambda * step_scale, step_scale = beta_pft (band) or beta (FFT)
     const double step = band ? s.cfg.beta_pft : s.cfg.beta;
@@ -469,6 +526,8 @@ void run(pftg_solver& s, int max_sweeps) {
         std::swap(s.order[i - 1], s.order[j]);
       }
       enqueue_sweep<R>(s, band);
+    } else if (persistent_fft<R>(s, band)) {
+      enqueue_sweep<R>(s, band);  // one cooperative launch (+ TV): nothing to capture
     } else {
       cudaGraphExec_t& g = s.graph[band ? 0 : 1];
       int* delta = s.graph_launches[band ? 0 : 1];
@@ -578,6 +637,7 @@ void create(pftg_solver& s, const void* frame, const void* probe, const int64_t*
   PFTG_CUDA(cudaMalloc(&s.part, sizeof(double) * std::max(64, fft_cols_strips<R>((int)s.wc)) *
                                     std::max<std::size_t>(s.npos, 1)));
   PFTG_CUDA(cudaMalloc(&s.red, sizeof(double) * 2 * kRedBlocks));
+  PFTG_CUDA(cudaMalloc(&s.bar, sizeof(unsigned)));
   (void)fft_twiddles<R>((int)s.wr);
   (void)fft_twiddles<R>((int)s.wc);
   if (s.cfg.pft_sweeps > 0) {

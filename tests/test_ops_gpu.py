@@ -404,3 +404,43 @@ def test_evaluator_cfg5_full_size_chunk_invariance_and_sample(ref):
         want_b = np.sum((np.abs(r.apply(ex)) - dc[j]) ** 2)
         assert abs(gf - want_f) <= 1e-4 * want_f, (j, gf, want_f)
         assert abs(gb - want_b) <= 1e-4 * want_b, (j, gb, want_b)
+
+
+_PERSIST_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2408_03532_b200 as P
+rng = np.random.default_rng(31)
+out = {}
+for w, n, blind in ((256, 400, True), (256, 400, False), (512, 700, True)):
+    obj = (rng.random((n, n)) * np.exp(1j * rng.random((n, n)))).astype(np.complex64)
+    probe = np.exp(-((np.arange(w) - w / 2) ** 2)[:, None] / (w * w / 8.0)
+                   - ((np.arange(w) - w / 2) ** 2)[None, :] / (w * w / 8.0)).astype(np.complex64)
+    offs = np.array([[r, c] for r in (0, 37, n - w) for c in (0, 51, n - w)], np.int64)
+    d = (np.abs(rng.standard_normal((len(offs), w, w))) * 30).astype(np.float32)
+    cfg = P.SolverConfig(pft_sweeps=0, fft_sweeps=2, beta=0.5, gamma=0.05, blind=blind)
+    r = P.hybrid_solve(d, offs, probe, obj, cfg)
+    out[f"f{w}{int(blind)}"] = r.frame
+    out[f"p{w}{int(blind)}"] = r.probe
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_persistent_fft_sweep_bit_identical(tmp_path):
+    """The persistent cooperative full-FFT sweep (epie_sweep.cuh) runs the same
+    arithmetic as the per-position kernel graph: frames and probes after two
+    sweeps are bit-identical (256^2 blind / non-blind, 512^2 blind)."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    script = tmp_path / "persist.py"
+    script.write_text(_PERSIST_SCRIPT)
+    res = {}
+    for tag, extra in (("persist", {}), ("graph", {"PFTG_NO_PERSIST": "1"})):
+        env = {**os.environ, **extra}
+        out = tmp_path / f"{tag}.npz"
+        subprocess.run([sys.executable, str(script), str(ROOT), str(out)], env=env, check=True, timeout=600)
+        res[tag] = np.load(out)
+    for k in res["persist"].files:
+        assert np.array_equal(res["persist"][k], res["graph"][k]), k
