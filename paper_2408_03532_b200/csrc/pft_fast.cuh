@@ -416,16 +416,17 @@ __host__ inline size_t adj_prefetch_smem(int n2, int q) {
 // FFT phase -- the epilogue then runs on shared memory instead of one L2
 // round trip per expanded row (it was 5.7 us of a cfg4 position's 12 us
 // kernel, tools/band_dbg.sh).
+// Body of one (row block k1, field f) work item (also the adjoint-rows phase of
+// the persistent band sweep, band_sweep.cuh); any block size >= fast_nt.
 template <class R, int Q, int RR, int P, int V, int EPI, int PF = 0>
-__global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
-    kf_adj_rows(PftDev<R> pl, BPar<R, Q, RR> bp, const typename CT<R>::C* __restrict__ Gt, EpiArgs ep) {
+__device__ __forceinline__ void kf_adj_rows_body(const PftDev<R>& pl, const BPar<R, Q, RR>& bp,
+                                                 const typename CT<R>::C* __restrict__ Gt, const EpiArgs& ep, int k1,
+                                                 int f, unsigned char* smem_raw) {
   using C = typename CT<R>::C;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   C* T = reinterpret_cast<C*>(smem_raw);
   const int ldT = ldT_of(pl.n2, Q);
   C* W2s = T + (size_t)RR * ldT;
   C* tw2s = W2s + (size_t)RR * pl.M2;
-  const int k1 = blockIdx.x, f = blockIdx.y;
   C* pfP = smem_after<C>(smem_raw, tw2s + P / 2 + 1, 16);  // [Q][n2] probe rows (PF)
   C* pfO = pfP + (size_t)Q * pl.n2;                         // object window rows
   C* pfN = pfO + (size_t)Q * pl.n2;                         // next window rows (EPI 2 + G2)
@@ -604,6 +605,14 @@ __global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
     C* G2blk = reinterpret_cast<C*>(ep.G2) + ((size_t)f * pl.p1 + k1) * RR * pl.M2;
     fast_stage_b_to_g<R, Q, RR, P>(pl, bp, T, W2s, tw2s, G2blk);
   }
+  __syncthreads();  // shared memory free for the caller's next work item
+}
+
+template <class R, int Q, int RR, int P, int V, int EPI, int PF = 0>
+__global__ void __launch_bounds__(fast_nt<RR, P>(), fast_min_blocks<R, RR, P>())
+    kf_adj_rows(PftDev<R> pl, BPar<R, Q, RR> bp, const typename CT<R>::C* __restrict__ Gt, EpiArgs ep) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  kf_adj_rows_body<R, Q, RR, P, V, EPI, PF>(pl, bp, Gt, ep, blockIdx.x, blockIdx.y, smem_raw);
 }
 
 }  // namespace pftg

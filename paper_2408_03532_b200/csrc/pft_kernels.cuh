@@ -552,17 +552,19 @@ __device__ __forceinline__ void block_sum_store(double v, double* scratch, doubl
 // grid = (ceil(M2/nb), batch).
 // NT = 320: single-column strips (one ePIE position) run one warp per j1 for
 // r1 <= 10, so each lane-group FFT phase is one round instead of two.
-template <class R, int S1, int RB, int MODE, int NT = 256>
-__global__ void __launch_bounds__(NT, NT == 256 ? 3 : 2) k_fwd_cols(PftDev<R> pl, const typename CT<R>::C* __restrict__ G,
-                                                  typename CT<R>::C* __restrict__ band,
-                                                  const R* __restrict__ dcrop, long long dstride,
-                                                  typename CT<R>::C* __restrict__ Gout,
-                                                  double* __restrict__ partial) {
+// Body of one (strip bx, field f) work item of a grid with gx strips per field
+// (also the cols phase of the persistent band sweep, band_sweep.cuh).
+template <class R, int S1, int RB, int MODE>
+__device__ __forceinline__ void k_fwd_cols_body(const PftDev<R>& pl, const typename CT<R>::C* __restrict__ G,
+                                                typename CT<R>::C* __restrict__ band,
+                                                const R* __restrict__ dcrop, long long dstride,
+                                                typename CT<R>::C* __restrict__ Gout,
+                                                double* __restrict__ partial, int bx, int f, int gx,
+                                                unsigned char* smem_raw) {
   using C = typename CT<R>::C;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nb = pl.nb;
   ColsSmem<R> sm(smem_raw, pl, nb);
-  const int f = blockIdx.y, b0 = blockIdx.x * nb;
+  const int b0 = bx * nb;
   const int nbv = min(nb, pl.M2 - b0);
   cols_load_tables(pl, sm);
   const C* Gf = G + (size_t)f * pl.p1 * pl.r1 * pl.M2;
@@ -582,7 +584,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 2) k_fwd_cols(PftDev<R> pl
   if (MODE == 2) {
     double acc = 0.0;
     project_strip(pl, sm, nb, nbv, dc, b0, false, &acc);
-    block_sum_store(acc, sm.red, partial + (size_t)f * gridDim.x + blockIdx.x);
+    block_sum_store(acc, sm.red, partial + (size_t)f * gx + bx);
     return;
   }
   project_strip(pl, sm, nb, nbv, dc, b0, true, nullptr);
@@ -591,6 +593,18 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 2) k_fwd_cols(PftDev<R> pl
   else cols_adjoint<R, S1, RB>(pl, sm, nb);
   __syncthreads();
   cols_store_g(pl, sm, Gout + (size_t)f * pl.p1 * pl.r1 * pl.M2, b0, nb, nbv);
+  __syncthreads();  // shared memory free for the caller's next work item
+}
+
+template <class R, int S1, int RB, int MODE, int NT = 256>
+__global__ void __launch_bounds__(NT, NT == 256 ? 3 : 2) k_fwd_cols(PftDev<R> pl, const typename CT<R>::C* __restrict__ G,
+                                                  typename CT<R>::C* __restrict__ band,
+                                                  const R* __restrict__ dcrop, long long dstride,
+                                                  typename CT<R>::C* __restrict__ Gout,
+                                                  double* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  k_fwd_cols_body<R, S1, RB, MODE>(pl, G, band, dcrop, dstride, Gout, partial, blockIdx.x, blockIdx.y, gridDim.x,
+                                   smem_raw);
 }
 
 // Adjoint cols: band -> Gt. grid = (ceil(M2/nb), batch).

@@ -31,6 +31,7 @@
 #include <stdexcept>
 #include <vector>
 
+#include "band_sweep.cuh"
 #include "epie_sweep.cuh"
 #include "eval_fft.cuh"
 #include "../../include/pftg.h"
@@ -415,10 +416,69 @@ void launch_persistent_fft(pftg_solver& s) {
   PFTG_CUDA(cudaLaunchCooperativeKernel(k, dim3(nsm), dim3(256), args, 0, s.st));
 }
 
+// PFT-band stage, blind, list order, complex64 q = 8 plans with r = 9 and
+// p = 32 / 64 (BASELINE configs[2] / [3]): the sweep as one cooperative
+// persistent kernel (band_sweep.cuh) after the first position's forward rows
+// pass. PFTG_NO_PERSIST=1 keeps the per-position graph.
+template <class R>
+bool persistent_band(const pftg_solver& s, bool band) {
+  if (sizeof(R) != 4 || !band || !s.cfg.blind || s.cfg.shuffled || knobs().no_persist || !s.plan) return false;
+  const pftg::Axis& a1 = s.plan->a1;
+  const pftg::Axis& a2 = s.plan->a2;
+  return a1.q == 8 && a2.q == 8 && a1.r == 9 && a2.r == 9 && a1.p == a2.p && (a1.p == 32 || a1.p == 64) &&
+         a1.n == a2.n && a1.mt == a2.mt;
+}
+
+template <class R, int Q, int RR, int P>
+void launch_persistent_band(pftg_solver& s) {
+  const PftDev<R>& pd = plan_dev<R>(*s.plan);
+  PftDev<R> pc = pd;  // single-position cols strips (launch_fwd_cols' narrowing)
+  while (pc.nb > 1 && (long long)((pc.M2 + pc.nb - 1) / pc.nb) < 148) pc.nb /= 2;
+  BPar<R, Q, RR> bp;
+  for (int l = 0; l <= Q / 2; ++l)
+    for (int j = 0; j < RR; ++j) {
+      bp.b1[l][j] = static_cast<R>(pd.hBv1[l * RR + j]);
+      bp.b2[l][j] = static_cast<R>(pd.hBv2[l * RR + j]);
+    }
+  const size_t rows_sm = fast_rows_smem<R>(pd.n2, Q, RR, pd.M2, P) + 16 + adj_prefetch_smem<R>(pd.n2, Q);
+  const size_t smem = std::max(rows_sm, cols_smem_bytes(pc));
+  if (smem > 227 * 1024) throw std::invalid_argument("pftg: persistent band sweep does not fit shared memory");
+  constexpr int S1 = P / 32 > 0 ? P / 32 : 1, RB = 10;
+  auto k = kb_band_sweep<R, Q, RR, P, S1, RB>;
+  PFTG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, nsm = 0;
+  PFTG_CUDA(cudaGetDevice(&dev));
+  PFTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  // the first position's forward rows pass (probe .* window 0) -> G
+  const int vec0 = (s.offs[0] % 2 == 0) && (s.fc % 2 == 0) && (s.wc % 2 == 0);
+  Src<R> src{static_cast<Cx<R>*>(s.frame), (long long)s.fc, 0, s.doffs, static_cast<Cx<R>*>(s.probe), vec0};
+  launch_fwd_rows<R>(pd, src, static_cast<Cx<R>*>(s.G), 1, s.st);
+  Cx<R>* frame = static_cast<Cx<R>*>(s.frame);
+  Cx<R>* probe = static_cast<Cx<R>*>(s.probe);
+  Cx<R>* G = static_cast<Cx<R>*>(s.G);
+  Cx<R>* Gt = static_cast<Cx<R>*>(s.Gt);
+  const R* dcrop = static_cast<const R*>(s.dcrop);
+  long long ld = (long long)s.fc, mb = (long long)pd.M1 * pd.M2;
+  const long long* offs = s.doffs;
+  int npos = (int)s.npos, vec_base = (s.fc % 2 == 0) && (s.wc % 2 == 0);
+  double beta = s.cfg.beta_pft, gamma = s.cfg.gamma_pft;
+  unsigned* bar = s.bar;
+  void* args[] = {(void*)&pd, &pc, &bp, &frame, &ld, &offs, &npos, &probe, &G, &Gt, &dcrop, &mb, &beta, &gamma,
+                  &vec_base, &bar};
+  PFTG_CUDA(cudaMemsetAsync(s.bar, 0, sizeof(unsigned), s.st));
+  ProfScope prof(s.st, K_ADJ_ROWS);
+  PFTG_CUDA(cudaLaunchCooperativeKernel((void*)k, dim3(nsm), dim3(kBandSweepThreads), args, smem, s.st));
+}
+
 template <class R>
 void enqueue_sweep(pftg_solver& s, bool band) {
   if (persistent_fft<R>(s, band)) {
     if constexpr (sizeof(R) == 4) launch_persistent_fft<R>(s);
+  } else if (persistent_band<R>(s, band)) {
+    if constexpr (sizeof(R) == 4) {
+      if (s.plan->a1.p == 32) launch_persistent_band<R, 8, 9, 32>(s);
+      else launch_persistent_band<R, 8, 9, 64>(s);
+    }
   } else {
     enqueue_positions<R>(s, band);
   }
@@ -526,8 +586,8 @@ void run(pftg_solver& s, int max_sweeps) {
         std::swap(s.order[i - 1], s.order[j]);
       }
       enqueue_sweep<R>(s, band);
-    } else if (persistent_fft<R>(s, band)) {
-      enqueue_sweep<R>(s, band);  // one cooperative launch (+ TV): nothing to capture
+    } else if (persistent_fft<R>(s, band) || persistent_band<R>(s, band)) {
+      enqueue_sweep<R>(s, band);  // cooperative launches (+ TV): nothing to capture
     } else {
       cudaGraphExec_t& g = s.graph[band ? 0 : 1];
       int* delta = s.graph_launches[band ? 0 : 1];

@@ -412,24 +412,28 @@ sys.path.insert(0, sys.argv[1])
 import paper_2408_03532_b200 as P
 rng = np.random.default_rng(31)
 out = {}
-for w, n, blind in ((256, 400, True), (256, 400, False), (512, 700, True)):
+for w, n, blind, band in ((256, 400, True, 0), (256, 400, False, 0), (512, 700, True, 0), (256, 400, True, 1),
+                         (512, 700, True, 1)):
     obj = (rng.random((n, n)) * np.exp(1j * rng.random((n, n)))).astype(np.complex64)
     probe = np.exp(-((np.arange(w) - w / 2) ** 2)[:, None] / (w * w / 8.0)
                    - ((np.arange(w) - w / 2) ** 2)[None, :] / (w * w / 8.0)).astype(np.complex64)
     offs = np.array([[r, c] for r in (0, 37, n - w) for c in (0, 51, n - w)], np.int64)
     d = (np.abs(rng.standard_normal((len(offs), w, w))) * 30).astype(np.float32)
-    cfg = P.SolverConfig(pft_sweeps=0, fft_sweeps=2, beta=0.5, gamma=0.05, blind=blind)
+    cfg = P.SolverConfig(pft_sweeps=2 * band, fft_sweeps=2 * (1 - band), beta=0.5, gamma=0.05,
+                         beta_pft=0.25 / w ** 2, gamma_pft=0.0125 / w ** 2, eps_pft=1e-3, blind=blind)
     r = P.hybrid_solve(d, offs, probe, obj, cfg)
-    out[f"f{w}{int(blind)}"] = r.frame
-    out[f"p{w}{int(blind)}"] = r.probe
+    out[f"f{w}{int(blind)}{band}"] = r.frame
+    out[f"p{w}{int(blind)}{band}"] = r.probe
 np.savez(sys.argv[2], **out)
 """
 
 
 def test_persistent_fft_sweep_bit_identical(tmp_path):
-    """The persistent cooperative full-FFT sweep (epie_sweep.cuh) runs the same
-    arithmetic as the per-position kernel graph: frames and probes after two
-    sweeps are bit-identical (256^2 blind / non-blind, 512^2 blind)."""
+    """The persistent cooperative sweeps (epie_sweep.cuh full-FFT stage,
+    band_sweep.cuh PFT-band stage) run the same arithmetic as the per-position
+    kernel graphs: frames and probes after two sweeps are bit-identical
+    (FFT stage 256^2 blind / non-blind and 512^2 blind; band stage 256^2 / 512^2
+    blind, p = 32 / 64, q = 8, r = 9)."""
     import os
     import subprocess
     import sys
