@@ -83,16 +83,19 @@ __device__ __forceinline__ void gather_smem(C* dst, int n, F&& src) {
   }
 }
 
+__host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
+
 // a in [0, M) with (a - mt) mod p == u: a0 = (u + mt) mod p, then every p-th
 __device__ __forceinline__ int band_first(int u, int mt, int p) { return (u + mt) % p; }
 
-template <class R>
+// QC / RC: compile-time q and r of a specialized square plan (0 = runtime)
+template <class R, int QC = 0, int RC = 0>
 __global__ void __launch_bounds__(256) kq_fwd_ab(PftDev<R> pd, const Cx<R>* __restrict__ z, long long bstride,
                                                  Cx<R>* __restrict__ Cg) {
   using C = Cx<R>;
   extern __shared__ __align__(16) unsigned char sm[];
   const int k2 = blockIdx.x, k1 = blockIdx.y, f = blockIdx.z;
-  const int q1 = pd.q1, q2 = pd.q2, r1 = pd.r1, r2 = pd.r2, n2 = pd.n2;
+  const int q1 = QC ? QC : pd.q1, q2 = QC ? QC : pd.q2, r1 = RC ? RC : pd.r1, r2 = RC ? RC : pd.r2, n2 = pd.n2;
   C* tile = reinterpret_cast<C*>(sm);
   C* T = tile + q1 * q2;
   R* b1 = reinterpret_cast<R*>(T + r1 * q2);
@@ -127,14 +130,15 @@ __global__ void __launch_bounds__(256) kq_fwd_ab(PftDev<R> pd, const Cx<R>* __re
 
 // 2-D unnormalized DFT over (k1, k2) of slice s = blockIdx.x of field blockIdx.y,
 // sign SIGN (-1 forward, +1 backward); iterative radix-2 DIT, rows then columns.
-template <class R, int SIGN>
+template <class R, int SIGN, int PC = 0, int RC = 0>
 __global__ void __launch_bounds__(256) kq_fft2(PftDev<R> pd, Cx<R>* __restrict__ Cg) {
   using C = Cx<R>;
   extern __shared__ __align__(16) unsigned char sm[];
+  const int p1 = PC ? PC : pd.p1, p2 = PC ? PC : pd.p2, lp1 = PC ? ilog2c(PC) : pd.lp1, lp2 = PC ? ilog2c(PC) : pd.lp2;
+  const int rr = RC ? RC * RC : pd.r1 * pd.r2;
   C* s = reinterpret_cast<C*>(sm);
-  C* tw1 = s + pd.p1 * pd.p2;
-  C* tw2 = tw1 + pd.p1 / 2;
-  const int p1 = pd.p1, p2 = pd.p2, lp1 = pd.lp1, lp2 = pd.lp2, rr = pd.r1 * pd.r2;
+  C* tw1 = s + p1 * p2;
+  C* tw2 = tw1 + p1 / 2;
   griddep_launch_dependents();
   for (int i = threadIdx.x; i < p1 / 2; i += blockDim.x) tw1[i] = pd.tw1[i];
   for (int i = threadIdx.x; i < p2 / 2; i += blockDim.x) tw2[i] = pd.tw2[i];
@@ -196,12 +200,12 @@ __global__ void __launch_bounds__(256) kq_fft2(PftDev<R> pd, Cx<R>* __restrict__
   for (int i = threadIdx.x; i < p1 * p2; i += blockDim.x) g[(size_t)i * rr] = s[i];
 }
 
-template <class R>
+template <class R, int RC = 0>
 __global__ void __launch_bounds__(128) kq_band(PftDev<R> pd, const Cx<R>* __restrict__ Cg, Cx<R>* __restrict__ out) {
   using C = Cx<R>;
   extern __shared__ __align__(16) unsigned char sm[];
   const int u2 = blockIdx.x, u1 = blockIdx.y, f = blockIdx.z;
-  const int r1 = pd.r1, r2 = pd.r2, M1 = pd.M1, M2 = pd.M2, p1 = pd.p1, p2 = pd.p2;
+  const int r1 = RC ? RC : pd.r1, r2 = RC ? RC : pd.r2, M1 = pd.M1, M2 = pd.M2, p1 = pd.p1, p2 = pd.p2;
   const int a0 = band_first(u1, pd.mt1, p1), b0 = band_first(u2, pd.mt2, p2);
   const int na = a0 < M1 ? (M1 - 1 - a0) / p1 + 1 : 0;
   const int nb = b0 < M2 ? (M2 - 1 - b0) / p2 + 1 : 0;
@@ -243,20 +247,20 @@ __global__ void __launch_bounds__(128) kq_band(PftDev<R> pd, const Cx<R>* __rest
   }
 }
 
-template <class R>
+template <class R, int RC = 0>
 __global__ void __launch_bounds__(256) kq_adj_band(PftDev<R> pd, const Cx<R>* __restrict__ band,
                                                    Cx<R>* __restrict__ Cg) {
   using C = Cx<R>;
   extern __shared__ __align__(16) unsigned char sm[];
   const int u2 = blockIdx.x, u1 = blockIdx.y, f = blockIdx.z;
-  const int r1 = pd.r1, r2 = pd.r2, M1 = pd.M1, M2 = pd.M2, p1 = pd.p1, p2 = pd.p2;
+  const int r1 = RC ? RC : pd.r1, r2 = RC ? RC : pd.r2, M1 = pd.M1, M2 = pd.M2, p1 = pd.p1, p2 = pd.p2;
   const int a0 = band_first(u1, pd.mt1, p1), b0 = band_first(u2, pd.mt2, p2);
   const int na = a0 < M1 ? (M1 - 1 - a0) / p1 + 1 : 0;
   const int nb = b0 < M2 ? (M2 - 1 - b0) / p2 + 1 : 0;
   C* Y = reinterpret_cast<C*>(sm);  // [na][nb]
   C* w1 = Y + na * nb;              // [na][r1] conj(W1[a][j1])
   C* w2 = w1 + na * r1;             // [nb][r2] conj(W2[b][j2])
-  C* F = w2 + nb * r2;              // [r1][nb] conj(W1[a][j1]) y[a][b] of one a
+  C* F = w2 + nb * r2;              // [na][r1][nb] conj(W1[a][j1]) y[a][b]
   griddep_launch_dependents();
   for (int i = threadIdx.x; i < na * r1; i += blockDim.x) {
     const int ai = i / r1, j1 = i - ai * r1;
@@ -282,29 +286,30 @@ __global__ void __launch_bounds__(256) kq_adj_band(PftDev<R> pd, const Cx<R>* __
   // (conj(w1[j1]) y) conj(w2[j2]) accumulated into C[j1][j2]
   const int o = threadIdx.x;
   const int j1 = o / r2, j2 = o - j1 * r2;
-  C acc = czero<C>();
-  for (int ai = 0; ai < na; ++ai) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < r1 * nb; i += blockDim.x) {
-      const int jj = i / nb, bi = i - jj * nb;
-      F[i] = cmul(w1[ai * r1 + jj], Y[ai * nb + bi]);
-    }
-    __syncthreads();
-    if (o < r1 * r2) {
-#pragma unroll 4
-      for (int bi = 0; bi < nb; ++bi) acc = cadd(acc, cmul(F[j1 * nb + bi], w2[bi * r2 + j2]));
-    }
+  // every c1 = conj(w1) y first (one barrier), then the accumulation chains
+  for (int i = threadIdx.x; i < na * r1 * nb; i += blockDim.x) {
+    const int ai = i / (r1 * nb), rem = i - ai * (r1 * nb), jj = rem / nb, bi = rem - jj * nb;
+    F[i] = cmul(w1[ai * r1 + jj], Y[ai * nb + bi]);
   }
-  if (o < r1 * r2) dst[o] = acc;
+  __syncthreads();
+  C acc = czero<C>();
+  if (o < r1 * r2) {
+    for (int ai = 0; ai < na; ++ai) {
+      const C* Fa = F + (size_t)(ai * r1 + j1) * nb;
+#pragma unroll 4
+      for (int bi = 0; bi < nb; ++bi) acc = cadd(acc, cmul(Fa[bi], w2[bi * r2 + j2]));
+    }
+    dst[o] = acc;
+  }
 }
 
-template <class R>
+template <class R, int QC = 0, int RC = 0>
 __global__ void __launch_bounds__(256) kq_adj_ab(PftDev<R> pd, const Cx<R>* __restrict__ Cg, Cx<R>* __restrict__ z,
                                                  long long bstride) {
   using C = Cx<R>;
   extern __shared__ __align__(16) unsigned char sm[];
   const int k2 = blockIdx.x, k1 = blockIdx.y, f = blockIdx.z;
-  const int q1 = pd.q1, q2 = pd.q2, r1 = pd.r1, r2 = pd.r2, n2 = pd.n2;
+  const int q1 = QC ? QC : pd.q1, q2 = QC ? QC : pd.q2, r1 = RC ? RC : pd.r1, r2 = RC ? RC : pd.r2, n2 = pd.n2;
   C* S = reinterpret_cast<C*>(sm);  // [r1][r2]
   C* T = S + r1 * r2;               // [r1][q2]
   R* b1 = reinterpret_cast<R*>(T + r1 * q2);
@@ -356,6 +361,18 @@ template <class R>
 size_t fft2_smem(const PftDev<R>& pd) {
   return sizeof(Cx<R>) * ((size_t)pd.p1 * pd.p2 + pd.p1 / 2 + pd.p2 / 2 + 2);
 }
+// the literal BASELINE configs[0] plan (q = 32, r = 12 on both axes): compile-time loop bounds
+template <class R>
+bool spec12(const PftDev<R>& pd) {
+  return pd.q1 == 32 && pd.q2 == 32 && pd.r1 == 12 && pd.r2 == 12;
+}
+
+template <class R>
+size_t adj_band_smem(const PftDev<R>& pd) {
+  const size_t na = (pd.M1 + pd.p1 - 1) / pd.p1, nb = (pd.M2 + pd.p2 - 1) / pd.p2;
+  return sizeof(Cx<R>) * (na * nb + na * pd.r1 + nb * pd.r2 + na * pd.r1 * nb);
+}
+
 template <class R>
 int band_rows(int M, int p) {
   return (M + p - 1) / p;
@@ -367,7 +384,7 @@ template <class R>
 bool tile_path_ok(const PftDev<R>& pd, std::size_t batch) {
   if (knobs().no_tile) return false;
   const bool fits = ab_smem(pd) <= 200 * 1024 && adj_ab_smem(pd) <= 200 * 1024 && fft2_smem(pd) <= 200 * 1024 &&
-                    (size_t)pd.r1 * pd.r2 <= 256 && batch <= 65535;
+                    adj_band_smem(pd) <= 200 * 1024 && (size_t)pd.r1 * pd.r2 <= 256 && batch <= 65535;
   if (!fits) return false;
   if (knobs().force_tile) return true;
   // the persistent rows kernels run one CTA per (field, k1): use the tile path
@@ -382,21 +399,23 @@ void tile_apply(const PftDev<R>& pd, const void* z, long long bstride, void* ban
   const dim3 tiles(pd.p2, pd.p1, batch);
   {
     ProfScope prof(st, K_FWD_ROWS);
-    smem_optin(kq_fwd_ab<R>, ab_smem(pd));
-    launch_tile(kq_fwd_ab<R>, tiles, dim3(256), ab_smem(pd), st, pd, static_cast<const Cx<R>*>(z), bstride,
-                Cg.as<Cx<R>>());
+    auto k = spec12(pd) ? kq_fwd_ab<R, 32, 12> : kq_fwd_ab<R>;
+    smem_optin(k, ab_smem(pd));
+    launch_tile(k, tiles, dim3(256), ab_smem(pd), st, pd, static_cast<const Cx<R>*>(z), bstride, Cg.as<Cx<R>>());
   }
   {
     ProfScope prof(st, K_FWD_COLS);
-    smem_optin(kq_fft2<R, -1>, fft2_smem(pd));
-    launch_tile(kq_fft2<R, -1>, dim3(pd.r1 * pd.r2, batch), dim3(256), fft2_smem(pd), st, pd, Cg.as<Cx<R>>());
+    auto k = (spec12(pd) && pd.p1 == 16 && pd.p2 == 16) ? kq_fft2<R, -1, 16, 12> : kq_fft2<R, -1>;
+    smem_optin(k, fft2_smem(pd));
+    launch_tile(k, dim3(pd.r1 * pd.r2, batch), dim3(256), fft2_smem(pd), st, pd, Cg.as<Cx<R>>());
   }
   {
     ProfScope prof(st, K_FWD_COLS);
     const size_t na = band_rows<R>(pd.M1, pd.p1), nb = band_rows<R>(pd.M2, pd.p2);
     const size_t sm = sizeof(Cx<R>) * ((size_t)pd.r1 * pd.r2 + pd.r1 * nb + na * pd.r1 + nb * pd.r2);
-    smem_optin(kq_band<R>, sm);
-    launch_tile(kq_band<R>, tiles, dim3(128), sm, st, pd, (const Cx<R>*)Cg.as<Cx<R>>(), static_cast<Cx<R>*>(band));
+    auto k = spec12(pd) ? kq_band<R, 12> : kq_band<R>;
+    smem_optin(k, sm);
+    launch_tile(k, tiles, dim3(128), sm, st, pd, (const Cx<R>*)Cg.as<Cx<R>>(), static_cast<Cx<R>*>(band));
   }
 }
 
@@ -408,20 +427,23 @@ void tile_adjoint(const PftDev<R>& pd, const void* band, void* z, long long bstr
   {
     ProfScope prof(st, K_ADJ_COLS);
     const size_t na = band_rows<R>(pd.M1, pd.p1), nb = band_rows<R>(pd.M2, pd.p2);
-    const size_t sm = sizeof(Cx<R>) * (na * nb + na * pd.r1 + nb * pd.r2 + pd.r1 * nb);
-    smem_optin(kq_adj_band<R>, sm);
-    launch_tile(kq_adj_band<R>, tiles, dim3(256), sm, st, pd, static_cast<const Cx<R>*>(band), Cg.as<Cx<R>>());
+    const size_t sm = sizeof(Cx<R>) * (na * nb + na * pd.r1 + nb * pd.r2 + na * pd.r1 * nb);
+    auto k = spec12(pd) ? kq_adj_band<R, 12> : kq_adj_band<R>;
+    smem_optin(k, sm);
+    launch_tile(k, tiles, dim3(256), sm, st, pd, static_cast<const Cx<R>*>(band), Cg.as<Cx<R>>());
   }
   {
     ProfScope prof(st, K_ADJ_COLS);
-    smem_optin(kq_fft2<R, 1>, fft2_smem(pd));
-    launch_tile(kq_fft2<R, 1>, dim3(pd.r1 * pd.r2, batch), dim3(256), fft2_smem(pd), st, pd, Cg.as<Cx<R>>());
+    auto k = (spec12(pd) && pd.p1 == 16 && pd.p2 == 16) ? kq_fft2<R, 1, 16, 12> : kq_fft2<R, 1>;
+    smem_optin(k, fft2_smem(pd));
+    launch_tile(k, dim3(pd.r1 * pd.r2, batch), dim3(256), fft2_smem(pd), st, pd, Cg.as<Cx<R>>());
   }
   {
     ProfScope prof(st, K_ADJ_ROWS);
-    smem_optin(kq_adj_ab<R>, adj_ab_smem(pd));
-    launch_tile(kq_adj_ab<R>, tiles, dim3(256), adj_ab_smem(pd), st, pd, (const Cx<R>*)Cg.as<Cx<R>>(),
-                static_cast<Cx<R>*>(z), bstride);
+    auto k = spec12(pd) ? kq_adj_ab<R, 32, 12> : kq_adj_ab<R>;
+    smem_optin(k, adj_ab_smem(pd));
+    launch_tile(k, tiles, dim3(256), adj_ab_smem(pd), st, pd, (const Cx<R>*)Cg.as<Cx<R>>(), static_cast<Cx<R>*>(z),
+                bstride);
   }
 }
 
