@@ -43,6 +43,7 @@ const Knobs& knobs() {
     o.tma_ns = num("PFTG_TMA_NS");
     o.cols_grid = num("PFTG_COLS_GRID");
     o.eval_chunk = num("PFTG_EVAL_CHUNK");
+    o.eval_pchunk = num("PFTG_EVAL_PCHUNK");
     o.eval_one_stream = on("PFTG_EVAL_ONE_STREAM");
     o.no_tile = on("PFTG_NO_TILE");
     o.force_tile = on("PFTG_TILE");
@@ -622,8 +623,13 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
   const PftDev<R>* pd = plan ? &plan_dev<R>(*plan) : nullptr;
   if (pd && (pd->n1 != n1 || pd->n2 != n2))
     throw std::invalid_argument("band_residual: plan does not match the window shape");
-  std::size_t chunk = std::max<std::size_t>(1, std::min<std::size_t>(count, (64u << 20) / (sizeof(Cx<R>) * n)));
-  if (knobs().eval_chunk > 0) chunk = std::max<std::size_t>(1, std::min<std::size_t>(count, knobs().eval_chunk));
+  // spectra per chunk: 512 MB (256 positions of 512^2 complex64; fewer, longer
+  // launches overlap the band chain on the side stream better: 64 MB chunks
+  // 6.91 ms, 512 MB 6.61 ms, 1.6 GB 6.86 ms per 1600 positions), equal chunks
+  std::size_t chunk = std::max<std::size_t>(1, (512ull << 20) / (sizeof(Cx<R>) * n));
+  if (knobs().eval_chunk > 0) chunk = (std::size_t)knobs().eval_chunk;
+  if (count > chunk) chunk = (count + (count + chunk - 1) / chunk - 1) / ((count + chunk - 1) / chunk);
+  chunk = std::max<std::size_t>(1, std::min<std::size_t>(count, chunk));
   Scratch doffs(sizeof(long long) * std::max<std::size_t>(count, 1), st);
   if (count) PFTG_CUDA(cudaMemcpyAsync(doffs.p, offs.data(), sizeof(long long) * count, cudaMemcpyHostToDevice, st));
   Scratch X(sizeof(Cx<R>) * n * chunk, st);
@@ -633,8 +639,18 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
   Scratch part(sizeof(double) * nstrips * std::max<std::size_t>(count, 1), st);
   std::unique_ptr<Scratch> G, bpart;
   int bstrips = 0;
+  // the band chain's own chunk: more positions per persistent rows launch
+  // (fewer tail rounds, fewer launches) than the spectra budget allows the FFT part
+  // (up to 512 MB of G: cfg5's 1600 positions in two launches, 7.51 -> 6.91 ms)
+  std::size_t pchunk = 1;
   if (pd) {
-    G.reset(new Scratch(sizeof(Cx<R>) * (std::size_t)pd->p1 * pd->r1 * pd->M2 * chunk, st));
+    const std::size_t gpos = sizeof(Cx<R>) * (std::size_t)pd->p1 * pd->r1 * pd->M2;
+    pchunk = knobs().eval_pchunk > 0 ? (std::size_t)knobs().eval_pchunk : std::max<std::size_t>(1, (512u << 20) / gpos);
+    if (count > pchunk) pchunk = (count + (count + pchunk - 1) / pchunk - 1) / ((count + pchunk - 1) / pchunk);
+    pchunk = std::min<std::size_t>(std::max<std::size_t>(count, 1), pchunk);
+  }
+  if (pd) {
+    G.reset(new Scratch(sizeof(Cx<R>) * (std::size_t)pd->p1 * pd->r1 * pd->M2 * pchunk, st));
     bstrips = cols_strips<R>(*pd);
     bpart.reset(new Scratch(sizeof(double) * bstrips * std::max<std::size_t>(count, 1), st));
   }
@@ -681,15 +697,17 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
       launch_fft_cols<R>(COL_EVAL_NAT, n1, n2, X.as<Cx<R>>(), n, static_cast<const R*>(d) + (pb + c0) * n, n,
                          nullptr, 0, -1, part.as<double>() + c0 * nstrips, nb, st);
     }
-    if (pd) {
-      bool evec = vec_ok(frame, (long long)fc, 0) && vec_ok(probe, n2, 0);
-      for (std::size_t j = c0; j < c0 + nb; ++j) evec = evec && (offs[j] % 2 == 0);
-      Src<R> s2{static_cast<const Cx<R>*>(frame), (long long)fc, 0, o, static_cast<const Cx<R>*>(probe), evec};
-      launch_fwd_rows<R>(*pd, s2, G->as<Cx<R>>(), nb, sb);
-      const long long mb = (long long)pd->M1 * pd->M2;
-      launch_fwd_cols<R>(*pd, 2, G->as<Cx<R>>(), nullptr, static_cast<const R*>(dcrop) + (pb + c0) * mb, mb,
-                         nullptr, bpart->as<double>() + c0 * bstrips, nb, sb);
-    }
+  }
+  for (std::size_t c0 = 0; pd && c0 < count; c0 += pchunk) {
+    const int nb = (int)std::min(pchunk, count - c0);
+    const long long* o = doffs.as<long long>() + c0;
+    bool evec = vec_ok(frame, (long long)fc, 0) && vec_ok(probe, n2, 0);
+    for (std::size_t j = c0; j < c0 + nb; ++j) evec = evec && (offs[j] % 2 == 0);
+    Src<R> s2{static_cast<const Cx<R>*>(frame), (long long)fc, 0, o, static_cast<const Cx<R>*>(probe), evec};
+    launch_fwd_rows<R>(*pd, s2, G->as<Cx<R>>(), nb, sb);
+    const long long mb = (long long)pd->M1 * pd->M2;
+    launch_fwd_cols<R>(*pd, 2, G->as<Cx<R>>(), nullptr, static_cast<const R*>(dcrop) + (pb + c0) * mb, mb, nullptr,
+                       bpart->as<double>() + c0 * bstrips, nb, sb);
   }
   if (ev_fork) {
     PFTG_CUDA(cudaEventRecord(ev_join, sb));

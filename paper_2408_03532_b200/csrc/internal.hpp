@@ -40,6 +40,7 @@ struct Knobs {
   bool no_pdl, no_tma, no_ws, no_wide, no_split, no_local_cols, eval_lanefft, epie_lanefft;
   int tma_ns, cols_grid;  // 0 = unset
   int eval_chunk;         // evaluator positions per chunk (0 = 64 MB of spectra)
+  int eval_pchunk;        // evaluator positions per band-chain chunk (0 = 2 x eval chunk)
   bool eval_one_stream;   // evaluator: FFT and PFT chains on one stream
   bool no_tile, force_tile;  // small-batch tile path (pft_tile.cu): off / forced
   int host_chunk_mb;         // host-buffer pipelines: MB per copy (0 = 32)

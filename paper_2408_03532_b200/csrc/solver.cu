@@ -692,7 +692,8 @@ void create(pftg_solver& s, const void* frame, const void* probe, const int64_t*
   PFTG_CUDA(cudaStreamSynchronize(s.st));
   PFTG_CUDA(cudaMalloc(&s.X, sizeof(Cx<R>) * pn));
   PFTG_CUDA(cudaMalloc(&s.X2, sizeof(Cx<R>) * pn));
-  s.eval_chunk = std::max<std::size_t>(1, std::min<std::size_t>(s.npos, (64u << 20) / (sizeof(Cx<R>) * pn)));
+  // per-sweep objective: up to 512 MB of spectra per launch pair (fewer launch tails)
+  s.eval_chunk = std::max<std::size_t>(1, std::min<std::size_t>(s.npos, (512ull << 20) / (sizeof(Cx<R>) * pn)));
   PFTG_CUDA(cudaMalloc(&s.Xe, sizeof(Cx<R>) * pn * s.eval_chunk));
   PFTG_CUDA(cudaMalloc(&s.part, sizeof(double) * std::max(64, fft_cols_strips<R>((int)s.wc)) *
                                     std::max<std::size_t>(s.npos, 1)));
