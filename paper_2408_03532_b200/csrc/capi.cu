@@ -450,42 +450,110 @@ void band_residual_dev(const pftg_plan* plan, const void* exit_wave, const void*
   }
 }
 
-// Host-buffer variants: chunks of the batch ping-pong between two streams so
-// H2D of chunk i+1, compute of chunk i and D2H of chunk i-1 overlap.
+// Host-buffer variants: a three-stage ring. One stream per stage -- H2D copy,
+// compute, D2H copy -- and NSLOT device buffer sets; chunk i uses slot i % NSLOT.
+// The H2D stream never waits for a D2H (it only waits until the compute of
+// chunk i - NSLOT has consumed the slot's input), so the H2D copy engine runs
+// back to back over the whole batch while the D2H engine trails it by one
+// chunk: the call costs max(H2D bytes, D2H bytes) / PCIe rate plus one chunk
+// of fill and drain. (Two ping-pong streams each serialising H2D -> compute
+// -> D2H left one direction idle whenever the other stream's copy ran long.)
+// Events are recorded in issue order, so a wait on slot k's event always
+// refers to chunk i - NSLOT (never-recorded events count as complete).
+constexpr int NSLOT = 3;
+struct HostRing {
+  cudaStream_t s[3];  // 0: H2D, 1: compute, 2: D2H
+  cudaEvent_t h2d[NSLOT], comp[NSLOT], d2h[NSLOT];
+};
+HostRing& host_ring() {
+  // per (host thread, device), created once
+  thread_local HostRing rings[64];
+  thread_local bool made[64] = {};
+  int dev = 0;
+  PFTG_CUDA(cudaGetDevice(&dev));
+  if (dev >= 64) throw std::runtime_error("pftg: device index out of range");
+  HostRing& r = rings[dev];
+  if (!made[dev]) {
+    for (auto& s : r.s) PFTG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    for (int k = 0; k < NSLOT; ++k) {
+      PFTG_CUDA(cudaEventCreateWithFlags(&r.h2d[k], cudaEventDisableTiming));
+      PFTG_CUDA(cudaEventCreateWithFlags(&r.comp[k], cudaEventDisableTiming));
+      PFTG_CUDA(cudaEventCreateWithFlags(&r.d2h[k], cudaEventDisableTiming));
+    }
+    made[dev] = true;
+  }
+  return r;
+}
+
+// in(slot, b0, m, st): H2D of chunk [b0, b0 + m); op(slot, m, st): compute;
+// out(slot, b0, m, st): D2H. Device buffers come from the stream-ordered pool
+// on the compute stream (alloc(slot)); the copy streams are forked from it.
+template <class In, class Op, class Out>
+void host_ring_run(std::size_t batch, std::size_t chunk, In&& in, Op&& op, Out&& out) {
+  HostRing& r = host_ring();
+  cudaEvent_t fork = r.comp[0];
+  PFTG_CUDA(cudaEventRecord(fork, r.s[1]));  // buffers allocated on s[1] before this point
+  PFTG_CUDA(cudaStreamWaitEvent(r.s[0], fork));
+  PFTG_CUDA(cudaStreamWaitEvent(r.s[2], fork));
+  // the first chunks ramp up (chunk/4, chunk/2, chunk, ...): the D2H engine,
+  // the busier direction (band + back-projection), starts after a short H2D
+  int k = 0, i = 0;
+  for (std::size_t b0 = 0; b0 < batch; ++i, k = (k + 1) % NSLOT) {
+    const std::size_t c = i == 0 ? std::max<std::size_t>(1, chunk / 4) : i == 1 ? std::max<std::size_t>(1, chunk / 2)
+                                                                              : chunk;
+    const std::size_t m = std::min(c, batch - b0);
+    if (i >= NSLOT) PFTG_CUDA(cudaStreamWaitEvent(r.s[0], r.comp[k]));  // slot input consumed
+    in(k, b0, m, r.s[0]);
+    PFTG_CUDA(cudaEventRecord(r.h2d[k], r.s[0]));
+    PFTG_CUDA(cudaStreamWaitEvent(r.s[1], r.h2d[k]));
+    if (i >= NSLOT) PFTG_CUDA(cudaStreamWaitEvent(r.s[1], r.d2h[k]));  // slot outputs drained
+    op(k, m, r.s[1]);
+    PFTG_CUDA(cudaEventRecord(r.comp[k], r.s[1]));
+    PFTG_CUDA(cudaStreamWaitEvent(r.s[2], r.comp[k]));
+    out(k, b0, m, r.s[2]);
+    PFTG_CUDA(cudaEventRecord(r.d2h[k], r.s[2]));
+    b0 += m;
+  }
+  // join: the buffers are released on the compute stream after the last copies
+  PFTG_CUDA(cudaEventRecord(r.h2d[0], r.s[0]));
+  PFTG_CUDA(cudaStreamWaitEvent(r.s[1], r.h2d[0]));
+  PFTG_CUDA(cudaEventRecord(r.d2h[0], r.s[2]));
+  PFTG_CUDA(cudaStreamWaitEvent(r.s[1], r.d2h[0]));
+}
+
 template <class R, class Op>
 void host_pipeline(std::size_t batch, std::size_t in_elems, std::size_t out_elems, const void* in, void* out,
                    std::size_t chunk, Op&& op) {
   using C = Cx<R>;
-  // two non-blocking streams per (host thread, device), created once
-  thread_local cudaStream_t streams[64][2] = {};
-  int dev = 0;
-  PFTG_CUDA(cudaGetDevice(&dev));
-  if (dev >= 64) throw std::runtime_error("pftg: device index out of range");
-  cudaStream_t* s = streams[dev];
-  for (int k = 0; k < 2; ++k)
-    if (!s[k]) PFTG_CUDA(cudaStreamCreateWithFlags(&s[k], cudaStreamNonBlocking));
+  HostRing& r = host_ring();
   {
-    // buffers from the stream-ordered pool (released on the stream that used them)
-    Scratch din0(sizeof(C) * in_elems * chunk, s[0]), dout0(sizeof(C) * out_elems * chunk, s[0]);
-    Scratch din1(sizeof(C) * in_elems * chunk, s[1]), dout1(sizeof(C) * out_elems * chunk, s[1]);
-    C* din[2] = {din0.as<C>(), din1.as<C>()};
-    C* dout[2] = {dout0.as<C>(), dout1.as<C>()};
-    int k = 0;
-    for (std::size_t b0 = 0; b0 < batch; b0 += chunk, k ^= 1) {
-      const std::size_t nb = std::min(chunk, batch - b0);
-      PFTG_CUDA(cudaMemcpyAsync(din[k], static_cast<const C*>(in) + b0 * in_elems, sizeof(C) * in_elems * nb,
-                                cudaMemcpyHostToDevice, s[k]));
-      op(din[k], dout[k], nb, s[k]);
-      PFTG_CUDA(cudaMemcpyAsync(static_cast<C*>(out) + b0 * out_elems, dout[k], sizeof(C) * out_elems * nb,
-                                cudaMemcpyDeviceToHost, s[k]));
+    std::vector<std::unique_ptr<Scratch>> bufs;
+    C *din[NSLOT], *dout[NSLOT];
+    for (int k = 0; k < NSLOT; ++k) {
+      bufs.emplace_back(new Scratch(sizeof(C) * in_elems * chunk, r.s[1]));
+      din[k] = bufs.back()->as<C>();
+      bufs.emplace_back(new Scratch(sizeof(C) * out_elems * chunk, r.s[1]));
+      dout[k] = bufs.back()->as<C>();
     }
+    host_ring_run(
+        batch, chunk,
+        [&](int k, std::size_t b0, std::size_t m, cudaStream_t s) {
+          PFTG_CUDA(cudaMemcpyAsync(din[k], static_cast<const C*>(in) + b0 * in_elems, sizeof(C) * in_elems * m,
+                                    cudaMemcpyHostToDevice, s));
+        },
+        [&](int k, std::size_t m, cudaStream_t s) { op(din[k], dout[k], m, s); },
+        [&](int k, std::size_t b0, std::size_t m, cudaStream_t s) {
+          PFTG_CUDA(cudaMemcpyAsync(static_cast<C*>(out) + b0 * out_elems, dout[k], sizeof(C) * out_elems * m,
+                                    cudaMemcpyDeviceToHost, s));
+        });
   }
-  PFTG_CUDA(cudaStreamSynchronize(s[0]));
-  PFTG_CUDA(cudaStreamSynchronize(s[1]));
+  PFTG_CUDA(cudaStreamSynchronize(r.s[1]));
 }
 
 std::size_t host_chunk(std::size_t batch, std::size_t bytes_per_field) {
-  // ~32 MiB per copy: large enough to run PCIe at full rate, small enough to overlap.
+  // ~32 MiB per copy: concurrent H2D + D2H run at ~49.7 GB/s each from 16-32 MiB
+  // copies on (48.3 at 8 MiB, tools/pcie_probe.cu); the ramped first chunks
+  // keep the pipeline fill short.
   const std::size_t mb = knobs().host_chunk_mb > 0 ? (std::size_t)knobs().host_chunk_mb : 32;
   std::size_t c = (mb << 20) / std::max<std::size_t>(bytes_per_field, 1);
   c = std::max<std::size_t>(1, c);
@@ -1114,39 +1182,36 @@ int pftg_fwd_adj_2d_host(const pftg_plan* plan, int dtype, const void* z, void* 
       using R = decltype(tag);
       using C = Cx<R>;
       const std::size_t chunk = host_chunk(batch, sizeof(C) * nz);
-      constexpr int NSS = 2;  // two streams (a third measured no faster: 9.76k vs 9.85k transforms/s)
-      thread_local cudaStream_t streams[64][NSS] = {};
-      int dev = 0;
-      PFTG_CUDA(cudaGetDevice(&dev));
-      if (dev >= 64) throw std::runtime_error("pftg: device index out of range");
-      cudaStream_t* st = streams[dev];
-      for (int k = 0; k < NSS; ++k)
-        if (!st[k]) PFTG_CUDA(cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking));
+      HostRing& r = host_ring();
       {
         std::vector<std::unique_ptr<Scratch>> bufs;
-        C *zi[NSS], *bo[NSS], *zo[NSS];
-        for (int k = 0; k < NSS; ++k) {
-          bufs.emplace_back(new Scratch(sizeof(C) * nz * chunk, st[k]));
+        C *zi[NSLOT], *bo[NSLOT], *zo[NSLOT];
+        for (int k = 0; k < NSLOT; ++k) {
+          bufs.emplace_back(new Scratch(sizeof(C) * nz * chunk, r.s[1]));
           zi[k] = bufs.back()->as<C>();
-          bufs.emplace_back(new Scratch(sizeof(C) * nb * chunk, st[k]));
+          bufs.emplace_back(new Scratch(sizeof(C) * nb * chunk, r.s[1]));
           bo[k] = bufs.back()->as<C>();
-          bufs.emplace_back(new Scratch(sizeof(C) * nz * chunk, st[k]));
+          bufs.emplace_back(new Scratch(sizeof(C) * nz * chunk, r.s[1]));
           zo[k] = bufs.back()->as<C>();
         }
-        int k = 0;
-        for (std::size_t b0 = 0; b0 < batch; b0 += chunk, k = (k + 1) % NSS) {
-          const std::size_t m = std::min(chunk, batch - b0);
-          PFTG_CUDA(cudaMemcpyAsync(zi[k], static_cast<const C*>(z) + b0 * nz, sizeof(C) * nz * m,
-                                    cudaMemcpyHostToDevice, st[k]));
-          apply_dev<R>(plan, zi[k], bo[k], m, st[k], batch);
-          adjoint_dev<R>(plan, bo[k], zo[k], m, st[k], batch);
-          PFTG_CUDA(cudaMemcpyAsync(static_cast<C*>(band) + b0 * nb, bo[k], sizeof(C) * nb * m, cudaMemcpyDeviceToHost,
-                                    st[k]));
-          PFTG_CUDA(cudaMemcpyAsync(static_cast<C*>(back) + b0 * nz, zo[k], sizeof(C) * nz * m, cudaMemcpyDeviceToHost,
-                                    st[k]));
-        }
+        host_ring_run(
+            batch, chunk,
+            [&](int k, std::size_t b0, std::size_t m, cudaStream_t s) {
+              PFTG_CUDA(cudaMemcpyAsync(zi[k], static_cast<const C*>(z) + b0 * nz, sizeof(C) * nz * m,
+                                        cudaMemcpyHostToDevice, s));
+            },
+            [&](int k, std::size_t m, cudaStream_t s) {
+              apply_dev<R>(plan, zi[k], bo[k], m, s, batch);
+              adjoint_dev<R>(plan, bo[k], zo[k], m, s, batch);
+            },
+            [&](int k, std::size_t b0, std::size_t m, cudaStream_t s) {
+              PFTG_CUDA(cudaMemcpyAsync(static_cast<C*>(back) + b0 * nz, zo[k], sizeof(C) * nz * m,
+                                        cudaMemcpyDeviceToHost, s));
+              PFTG_CUDA(cudaMemcpyAsync(static_cast<C*>(band) + b0 * nb, bo[k], sizeof(C) * nb * m,
+                                        cudaMemcpyDeviceToHost, s));
+            });
       }
-      for (int k = 0; k < NSS; ++k) PFTG_CUDA(cudaStreamSynchronize(st[k]));
+      PFTG_CUDA(cudaStreamSynchronize(r.s[1]));
     };
     if (dtype == PFTG_C64) run(float{});
     else run(double{});
