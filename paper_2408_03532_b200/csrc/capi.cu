@@ -45,6 +45,7 @@ const Knobs& knobs() {
     o.eval_chunk = num("PFTG_EVAL_CHUNK");
     o.eval_pchunk = num("PFTG_EVAL_PCHUNK");
     o.eval_one_stream = on("PFTG_EVAL_ONE_STREAM");
+    o.eval_band_old = num("PFTG_EVAL_BAND_OLD");
     o.no_tile = on("PFTG_NO_TILE");
     o.force_tile = on("PFTG_TILE");
     o.host_chunk_mb = num("PFTG_HOST_CHUNK_MB");
@@ -717,9 +718,20 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
     if (count > pchunk) pchunk = (count + (count + pchunk - 1) / pchunk - 1) / ((count + pchunk - 1) / pchunk);
     pchunk = std::min<std::size_t>(std::max<std::size_t>(count, 1), pchunk);
   }
+  // q = 8, r = 9 complex64 plans: axis-2-first band chain (eval_band.cu); either
+  // kernel can be swapped for the batched one (same G layout) with PFTG_EVAL_BAND_OLD
+  bool eb_rows = false, eb_cols = false;
+  if constexpr (sizeof(R) == 4) {
+    if (pd) {
+      const bool al = (reinterpret_cast<uintptr_t>(dcrop) & 15) == 0 && (reinterpret_cast<uintptr_t>(frame) & 7) == 0 &&
+                      (reinterpret_cast<uintptr_t>(probe) & 7) == 0;
+      eb_rows = al && eval_band_rows_ok(*pd) && !(knobs().eval_band_old & 1);
+      eb_cols = al && eval_band_cols_ok(*pd) && !(knobs().eval_band_old & 2);
+    }
+  }
   if (pd) {
     G.reset(new Scratch(sizeof(Cx<R>) * (std::size_t)pd->p1 * pd->r1 * pd->M2 * pchunk, st));
-    bstrips = cols_strips<R>(*pd);
+    bstrips = eb_cols ? pd->M2 / 8 : cols_strips<R>(*pd);
     bpart.reset(new Scratch(sizeof(double) * bstrips * std::max<std::size_t>(count, 1), st));
   }
   // The full-FFT residual and the PFT band residual are independent: the band
@@ -772,10 +784,19 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
     bool evec = vec_ok(frame, (long long)fc, 0) && vec_ok(probe, n2, 0);
     for (std::size_t j = c0; j < c0 + nb; ++j) evec = evec && (offs[j] % 2 == 0);
     Src<R> s2{static_cast<const Cx<R>*>(frame), (long long)fc, 0, o, static_cast<const Cx<R>*>(probe), evec};
-    launch_fwd_rows<R>(*pd, s2, G->as<Cx<R>>(), nb, sb);
     const long long mb = (long long)pd->M1 * pd->M2;
-    launch_fwd_cols<R>(*pd, 2, G->as<Cx<R>>(), nullptr, static_cast<const R*>(dcrop) + (pb + c0) * mb, mb, nullptr,
-                       bpart->as<double>() + c0 * bstrips, nb, sb);
+    const R* dcp = static_cast<const R*>(dcrop) + (pb + c0) * mb;
+    double* bp = bpart->as<double>() + c0 * bstrips;
+    if constexpr (sizeof(R) == 4) {
+      if (eb_rows)
+        launch_eval_band_rows(*pd, static_cast<const float2*>(frame), (long long)fc, o,
+                              static_cast<const float2*>(probe), G->as<float2>(), nb, sb);
+    }
+    if (!eb_rows) launch_fwd_rows<R>(*pd, s2, G->as<Cx<R>>(), nb, sb);
+    if constexpr (sizeof(R) == 4) {
+      if (eb_cols) launch_eval_band_cols(*pd, G->as<float2>(), nullptr, dcp, mb, bp, nb, sb);
+    }
+    if (!eb_cols) launch_fwd_cols<R>(*pd, 2, G->as<Cx<R>>(), nullptr, dcp, mb, nullptr, bp, nb, sb);
   }
   if (ev_fork) {
     PFTG_CUDA(cudaEventRecord(ev_join, sb));

@@ -179,6 +179,14 @@ __device__ __forceinline__ void bmacc(float2& acc, float bv, float2 z, bool odd)
 __device__ __forceinline__ float2 cfmar(float2 acc, float s, float2 x) { return f2fma(acc, make_float2(s, s), x); }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return f2mul(a, make_float2(s, s)); }
 
+// e + (-i) o and e - (-i) o
+template <class C>
+__device__ __forceinline__ C cadd_mi(C e, C o) { e.x += o.y; e.y -= o.x; return e; }
+template <class C>
+__device__ __forceinline__ C csub_mi(C e, C o) { e.x -= o.y; e.y += o.x; return e; }
+__device__ __forceinline__ float2 cadd_mi(float2 e, float2 o) { return f2fma(make_float2(o.y, o.x), make_float2(1.f, -1.f), e); }
+__device__ __forceinline__ float2 csub_mi(float2 e, float2 o) { return f2fma(make_float2(o.y, o.x), make_float2(-1.f, 1.f), e); }
+
 template <class C>
 __device__ __forceinline__ C czero() { C r; r.x = 0; r.y = 0; return r; }
 
