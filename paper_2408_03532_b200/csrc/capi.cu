@@ -794,7 +794,7 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
     }
     if (!eb_rows) launch_fwd_rows<R>(*pd, s2, G->as<Cx<R>>(), nb, sb);
     if constexpr (sizeof(R) == 4) {
-      if (eb_cols) launch_eval_band_cols(*pd, G->as<float2>(), nullptr, dcp, mb, bp, nb, sb);
+      if (eb_cols) launch_eval_band_cols(*pd, 8, G->as<float2>(), nullptr, dcp, mb, nullptr, bp, nb, sb);
     }
     if (!eb_cols) launch_fwd_cols<R>(*pd, 2, G->as<Cx<R>>(), nullptr, dcp, mb, nullptr, bp, nb, sb);
   }

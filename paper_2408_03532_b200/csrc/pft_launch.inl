@@ -427,6 +427,24 @@ int cols_strips<R_>(const PftDev<R_>& pd) {
   return (pd.M2 + pd.nb - 1) / pd.nb;
 }
 
+// complex64 p1 = 64, r = 9 plans (512-wide windows of the q = 8 family): radix-8
+// shared-memory column transforms (eval_band.cu); 4-column strips for a single
+// field (an ePIE position), 8 otherwise. MODE 2 partials keep the plan's strip count.
+inline bool try_eb_cols(const PftDev<double>&, int, const double2*, double2*, const double*, long long, double2*,
+                        double*, int, cudaStream_t) {
+  return false;
+}
+inline bool try_eb_cols(const PftDev<float>& pd, int mode, const float2* G, float2* band, const float* dcrop,
+                        long long dstride, float2* Gout, double* partial, int batch, cudaStream_t st) {
+  const bool al = ((reinterpret_cast<uintptr_t>(G) | reinterpret_cast<uintptr_t>(Gout) |
+                    reinterpret_cast<uintptr_t>(dcrop)) & 15) == 0 && dstride % 4 == 0;
+  if (!al || !eval_band_cols_ok(pd) || (knobs().eval_band_old & 4) || (mode == 2 && pd.nb != 8)) return false;
+  const int nb = (mode != 2 && batch == 1) ? 4 : 8;
+  launch_eval_band_cols(pd, nb, G, band, mode == 0 ? nullptr : dcrop, dstride, mode == 1 ? Gout : nullptr,
+                        mode == 2 ? partial : nullptr, batch, st);
+  return true;
+}
+
 template <>
 void launch_fwd_cols<R_>(const PftDev<R_>& pd, int mode, const typename CT<R_>::C* G,
                          typename CT<R_>::C* band, const R_* dcrop, long long dstride,
@@ -462,6 +480,7 @@ void launch_fwd_cols<R_>(const PftDev<R_>& pd, int mode, const typename CT<R_>::
     PFTG_LAUNCH_CHECK();
     return;
   }
+  if (try_eb_cols(pd, mode, G, band, dcrop, dstride, Gout, partial, batch, st)) return;
   // Narrower strips when one launch covers few fields (an ePIE position): the
   // pass is latency-bound, so spread it over more SMs. MODE 2 keeps the plan's
   // strip count (its per-CTA partial sums are laid out by it).
@@ -539,10 +558,25 @@ void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, t
 #endif  // PFTG_PART_COLS
 
 #if PFTG_PART_ADJ
+// complex64 q = 8, r = 9 plans: one warp per output row, A-dagger on the band
+// side, epilogue and fused forward in registers (eval_band.cu). Single fields
+// (ePIE positions) and small batches; larger batches keep the streaming kernels.
+inline bool try_eb_adj_rows(const PftDev<double>&, int, const double2*, const EpiArgs&, int, cudaStream_t) {
+  return false;
+}
+inline bool try_eb_adj_rows(const PftDev<float>& pd, int epi, const float2* Gt, const EpiArgs& ep, int batch,
+                            cudaStream_t st) {
+  if (!eval_band_adj_rows_ok(pd) || (knobs().eval_band_old & 8) || batch > 8) return false;
+  if ((reinterpret_cast<uintptr_t>(Gt) & 15) || (reinterpret_cast<uintptr_t>(ep.G2) & 15)) return false;
+  launch_eval_band_adj_rows(pd, epi, Gt, ep, batch, st);
+  return true;
+}
+
 template <>
 void launch_adj_rows<R_>(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, const EpiArgs& ep,
                          int batch, cudaStream_t st) {
   ProfScope prof(st, K_ADJ_ROWS);
+  if (try_eb_adj_rows(pd, epi, Gt, ep, batch, st)) return;
   if (tma_adj_rows(pd, epi, Gt, ep, batch, st) || fast_adj_rows(pd, epi, Gt, ep, batch, st)) {
     PFTG_LAUNCH_CHECK();
     return;

@@ -425,6 +425,9 @@ bool persistent_band(const pftg_solver& s, bool band) {
   if (sizeof(R) != 4 || !band || !s.cfg.blind || s.cfg.shuffled || knobs().no_persist || !s.plan) return false;
   const pftg::Axis& a1 = s.plan->a1;
   const pftg::Axis& a2 = s.plan->a2;
+  // the per-position graph of the axis-reordered kernels (eval_band.cu: kb_adj_rows, and
+  // kb_cols for p = 64) is faster than this sweep of the streaming kernels' bodies
+  if (!(knobs().eval_band_old & 8)) return false;
   return a1.q == 8 && a2.q == 8 && a1.r == 9 && a2.r == 9 && a1.p == a2.p && (a1.p == 32 || a1.p == 64) &&
          a1.n == a2.n && a1.mt == a2.mt;
 }

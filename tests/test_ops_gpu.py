@@ -166,7 +166,11 @@ def test_hybrid_solve_tv_c128_matches_reference(ref, tv):
 # oracle<float> -- the reference's algorithm run entirely in complex64
 # (oracle/pft_oracle.hybrid_solve(dtype=complex64)) -- on the same problem,
 # measured inside each test, plus an absolute slack for the tiny-divergence case.
-EPIE_FLOOR_FACTOR = 4.0
+# Factor: measured on the full cfg3 problem (1 band + 1 FFT sweep, 800 sequential
+# updates; tools/epie_floor_ratio.py) the streaming band kernels land at 3.7 / 3.9 x
+# the floor (frame / probe), the axis-reordered ones (eval_band.cu) at 4.9 / 5.6 x:
+# two samples of complex64 rounding in different summation orders.
+EPIE_FLOOR_FACTOR = 6.0
 
 
 def _epie_float_floor(init, pinit, offs, d, f_ref, p_ref, **kw):
@@ -441,10 +445,42 @@ def test_persistent_fft_sweep_bit_identical(tmp_path):
     script = tmp_path / "persist.py"
     script.write_text(_PERSIST_SCRIPT)
     res = {}
+    # PFTG_EVAL_BAND_OLD=12: the band stage on the streaming kernels, whose bodies the
+    # persistent band sweep shares (the default band stage runs eval_band.cu's kernels
+    # per position, see test_band_stage_axis_reordered_kernels)
     for tag, extra in (("persist", {}), ("graph", {"PFTG_NO_PERSIST": "1"})):
-        env = {**os.environ, **extra}
+        env = {**os.environ, "PFTG_EVAL_BAND_OLD": "12", **extra}
         out = tmp_path / f"{tag}.npz"
         subprocess.run([sys.executable, str(script), str(ROOT), str(out)], env=env, check=True, timeout=600)
         res[tag] = np.load(out)
     for k in res["persist"].files:
         assert np.array_equal(res["persist"][k], res["graph"][k]), k
+
+
+def test_band_stage_axis_reordered_kernels(tmp_path):
+    """The default PFT-band stage of the q = 8, r = 9 complex64 plans runs the
+    axis-reordered kernels of eval_band.cu (kb_cols: radix-8 column transforms
+    with the residual and the adjoint gather in registers; kb_adj_rows: A-dagger
+    on the band side, epilogue and fused forward per output row). Same operator
+    sequence as the streaming kernels (PFTG_EVAL_BAND_OLD=12), different
+    summation order: frames and probes after two blind band sweeps agree to
+    complex64 rounding."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    script = tmp_path / "band.py"
+    script.write_text(_PERSIST_SCRIPT)
+    res = {}
+    for tag, extra in (("new", {}), ("old", {"PFTG_EVAL_BAND_OLD": "12"})):
+        env = {**os.environ, **extra}
+        out = tmp_path / f"{tag}.npz"
+        subprocess.run([sys.executable, str(script), str(ROOT), str(out)], env=env, check=True, timeout=600)
+        res[tag] = np.load(out)
+    for k in res["new"].files:
+        a, b = res["new"][k], res["old"][k]
+        err = np.linalg.norm(a - b) / np.linalg.norm(b)
+        if k.endswith("1"):  # band-stage cases
+            assert err <= 2e-5, (k, err)
+        else:
+            assert np.array_equal(a, b), k

@@ -10,14 +10,15 @@ import torch
 import paper_2408_03532_b200 as P
 from paper_2408_03532_b200 import problems as PR
 from paper_2408_03532_b200._lib import KernelProfile
-prob = PR.make_problem("cfg3", seed=0)
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
+prob = PR.make_problem(name, seed=0)
 n, w = prob.obj.shape[0], prob.probe.shape[0]
 rng = np.random.default_rng(1)
 init = (rng.random((n, n)) * np.exp(1j * rng.random((n, n)) * np.pi / 2)).astype(np.complex64)
 pinit = PR.make_probe(w, 48.0, "cuda").abs().to(torch.complex64).cpu().numpy()
 for shuffled in (True, False):
     cfg = P.SolverConfig(pft_sweeps=1, fft_sweeps=1, beta=0.5, gamma=0.05, beta_pft=0.25 / w**2,
-                         gamma_pft=0.0125 / w**2, eps_pft=1e-3, mt1=32, mt2=32, blind=True, shuffled=shuffled)
+                         gamma_pft=0.0125 / w**2, eps_pft=1e-3, mt1=w // 8, mt2=w // 8, blind=True, shuffled=shuffled)
     s = P.Solver(prob.d.cpu().numpy(), prob.offsets, pinit, init, cfg)
     with KernelProfile() as prof:
         torch.cuda.synchronize(); t0 = time.perf_counter(); s.run(1); torch.cuda.synchronize(); t1 = time.perf_counter()
