@@ -673,6 +673,15 @@ int grid_for(long long n) {
 }
 
 // ---- evaluator ----
+// out[j] = sum_k part[j * nstrips + k], k ascending (deterministic)
+__global__ void k_sum_strips(const double* __restrict__ part, int nstrips, int count, double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= count) return;
+  double s = 0.0;
+  for (int k = 0; k < nstrips; ++k) s += part[(size_t)j * nstrips + k];
+  out[j] = s;
+}
+
 template <class R>
 void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void* probe, std::size_t wr,
                   std::size_t wc, const int64_t* offsets, std::size_t npos, std::size_t pb, std::size_t pe,
@@ -804,23 +813,28 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
     cudaEventDestroy(ev_fork);
     cudaEventDestroy(ev_join);
   }
-  std::vector<double> h(nstrips * count), hb(bstrips * count);
-  if (count) PFTG_CUDA(cudaMemcpyAsync(h.data(), part.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
-  if (pd && count)
-    PFTG_CUDA(cudaMemcpyAsync(hb.data(), bpart->p, sizeof(double) * hb.size(), cudaMemcpyDeviceToHost, st));
+  // per-position sums of the strip partials on the device (fixed strip order), so
+  // only 2 x count doubles cross PCIe instead of the ~1 MB of per-strip partials
+  Scratch psum(sizeof(double) * 2 * std::max<std::size_t>(count, 1), st);
+  if (count) {
+    k_sum_strips<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(part.as<double>(), nstrips, (int)count,
+                                                                 psum.as<double>());
+    if (pd)
+      k_sum_strips<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(bpart->as<double>(), bstrips, (int)count,
+                                                                   psum.as<double>() + count);
+    PFTG_LAUNCH_CHECK();
+  }
+  std::vector<double> h(2 * count);
+  if (count)
+    PFTG_CUDA(cudaMemcpyAsync(h.data(), psum.p, sizeof(double) * (pd ? 2 : 1) * count, cudaMemcpyDeviceToHost, st));
   PFTG_CUDA(cudaStreamSynchronize(st));
   // (1/n) sum_k (|X_k| - d_k)^2 = ||x - P_M(x)||^2 by Parseval (solver.cpp:89-102)
   double s = 0.0;
-  for (std::size_t j = 0; j < count; ++j) {
-    double sj = 0.0;
-    for (int k = 0; k < nstrips; ++k) sj += h[j * nstrips + k];
-    s += sj / static_cast<double>(n);
-  }
+  for (std::size_t j = 0; j < count; ++j) s += h[j] / static_cast<double>(n);
   *fft_sum = s;
   if (pd && band_sum) {
     double sb = 0.0;
-    for (std::size_t j = 0; j < count; ++j)
-      for (int k = 0; k < bstrips; ++k) sb += hb[j * bstrips + k];
+    for (std::size_t j = 0; j < count; ++j) sb += h[count + j];
     *band_sum = sb;
   }
 }
