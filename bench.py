@@ -97,12 +97,12 @@ def peaks():
 
 
 # ncu --set full capture of the dominant kernel committed under profiles/
-# (tools/profile_r2.sh r11: the first launch of each cfg2 kernel in tools/prof_pft.py,
+# (tools/profile_r2.sh r13: the first launch of each cfg2 kernel in tools/prof_pft.py,
 # 64 fields per launch). Returns DRAM bytes (read + write) per field, or None.
-PROFILE_CAPTURES = {"pft_rows_fwd": ("profiles/r11_kt2_fwd_rows_raw.csv", 64),
-                    "pft_rows_adj": ("profiles/r11_kt_adj_rows_raw.csv", 64),
-                    "pft_cols_fwd": ("profiles/r11_kc_fwd_cols_local_raw.csv", 64),
-                    "pft_cols_adj": ("profiles/r11_kc_adj_cols_local_raw.csv", 64)}
+PROFILE_CAPTURES = {"pft_rows_fwd": ("profiles/r13_kt2_fwd_rows_raw.csv", 64),
+                    "pft_rows_adj": ("profiles/r13_kt_adj_rows_raw.csv", 64),
+                    "pft_cols_fwd": ("profiles/r13_kc_fwd_cols_local_raw.csv", 64),
+                    "pft_cols_adj": ("profiles/r13_kc_adj_cols_local_raw.csv", 64)}
 
 
 def captured_traffic_per_field(kname):
@@ -121,7 +121,7 @@ def captured_traffic_per_field(kname):
     return tot / ent[1]
 
 
-def eval_traffic_per_step(npos, path="profiles/r11_eval_raw.csv", per=32):
+def eval_traffic_per_step(npos, path="profiles/r13_eval_raw.csv", per=64):
     import csv
     if not (ROOT / path).exists():
         return None
@@ -481,7 +481,7 @@ def run_ours(args):
                          "traffic": (None if captured_traffic_per_field(kname) is None
                                      else captured_traffic_per_field(kname) * fields_per_launch),
                          "traffic_source": "ncu --set full DRAM read+write of the committed capture "
-                                           "(profiles/r11_*_raw.csv), per field x fields per launch; "
+                                           "(profiles/r13_*_raw.csv), per field x fields per launch; "
                                            "algorithmic bytes per launch = %.4g" % (kbytes * fields_per_launch),
                          "peak_kind": peak_kind, "kernel_avg_ms": k_avg_ms,
                          "kernel_ms": prof.ms, "kernel_launches": prof.count,
@@ -732,7 +732,7 @@ def run_evaluator(args):
                          "achieved": achieved_step, "peak": hbm, "unit": "GB/s", "frac": achieved_step / hbm,
                          "traffic": eval_traffic_per_step(pe - pb),
                          "traffic_source": "ncu --set full DRAM read+write of the four evaluator kernels of one "
-                                           "32-position chunk (profiles/r11_eval_raw.csv), x positions / 32",
+                                           "64-position call (profiles/r13_eval_raw.csv), x positions / 64",
                          "peak_kind": peak_kind, "dominant_kernel": kname,
                          "kernel_ms": prof.ms},
             # this workload is compute-bound on the CUDA cores

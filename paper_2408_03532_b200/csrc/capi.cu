@@ -701,10 +701,10 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
   const PftDev<R>* pd = plan ? &plan_dev<R>(*plan) : nullptr;
   if (pd && (pd->n1 != n1 || pd->n2 != n2))
     throw std::invalid_argument("band_residual: plan does not match the window shape");
-  // spectra per chunk: 512 MB (256 positions of 512^2 complex64; fewer, longer
-  // launches overlap the band chain on the side stream better: 64 MB chunks
-  // 6.91 ms, 512 MB 6.61 ms, 1.6 GB 6.86 ms per 1600 positions), equal chunks
-  std::size_t chunk = std::max<std::size_t>(1, (512ull << 20) / (sizeof(Cx<R>) * n));
+  // spectra per chunk: up to 4 GB (all 1600 positions of configs[4] in one pair of
+  // launches; B200 has the HBM for it): fewer, longer launches -- 512 MB chunks 4.70 ms,
+  // 1.6 GB 4.62 ms, one chunk 4.58 ms per 1600 positions; equal chunks beyond that
+  std::size_t chunk = std::max<std::size_t>(1, (4ull << 30) / (sizeof(Cx<R>) * n));
   if (knobs().eval_chunk > 0) chunk = (std::size_t)knobs().eval_chunk;
   if (count > chunk) chunk = (count + (count + chunk - 1) / chunk - 1) / ((count + chunk - 1) / chunk);
   chunk = std::max<std::size_t>(1, std::min<std::size_t>(count, chunk));
@@ -719,11 +719,11 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
   int bstrips = 0;
   // the band chain's own chunk: more positions per persistent rows launch
   // (fewer tail rounds, fewer launches) than the spectra budget allows the FFT part
-  // (up to 512 MB of G: cfg5's 1600 positions in two launches, 7.51 -> 6.91 ms)
+  // (up to 1 GB of G: cfg5's 1600 positions in one pair of launches)
   std::size_t pchunk = 1;
   if (pd) {
     const std::size_t gpos = sizeof(Cx<R>) * (std::size_t)pd->p1 * pd->r1 * pd->M2;
-    pchunk = knobs().eval_pchunk > 0 ? (std::size_t)knobs().eval_pchunk : std::max<std::size_t>(1, (512u << 20) / gpos);
+    pchunk = knobs().eval_pchunk > 0 ? (std::size_t)knobs().eval_pchunk : std::max<std::size_t>(1, (1ull << 30) / gpos);
     if (count > pchunk) pchunk = (count + (count + pchunk - 1) / pchunk - 1) / ((count + pchunk - 1) / pchunk);
     pchunk = std::min<std::size_t>(std::max<std::size_t>(count, 1), pchunk);
   }

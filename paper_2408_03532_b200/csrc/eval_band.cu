@@ -18,6 +18,8 @@
 // 8 instead of 9 slice transforms per row block, stage A on a quarter of the
 // columns, and ordinary multi-CTA occupancy instead of one persistent CTA per
 // SM (the window rows come from L2, there is no HBM stream to keep busy).
+#include <cstdlib>
+
 #include "eval_fft.cuh"
 #include "internal.hpp"
 #include "pft_fast.cuh"
@@ -54,11 +56,13 @@ __device__ __forceinline__ void eb_contract8(const float (&b)[5][RR], const floa
 }
 
 // Stage A on the q1 = 8 band rows of a row block (rows[l * ld + pos(b)], even b
-// first then odd b): G[j1][b] = sum_l B1[l][j1] rows[l][b]. 256 threads: thread
-// (m, g) owns columns 2m, 2m + 1 and j1 = g (mod 4).
+// first then odd b): G[j1][b] = sum_l B1[l][j1] rows[l][b]. Thread (m = tid & 63, group g)
+// owns columns 2m, 2m + 1 and j1 = g (mod 4); the four groups may sit in one CTA
+// (g = tid >> 6) or in the two CTAs of a cluster pair.
 template <int RR>
-__device__ __forceinline__ void eb_stage_a(const EbPar<RR>& bp, const float2* rows, int ld, int M2, float2* Gt) {
-  const int g = threadIdx.x >> 6, hM = M2 >> 1;
+__device__ __forceinline__ void eb_stage_a(const EbPar<RR>& bp, const float2* rows, int ld, int M2, float2* Gt,
+                                           int g) {
+  const int hM = M2 >> 1;
   for (int m = threadIdx.x & 63; m < hM; m += 64) {
     float2 te[8], to[8];
 #pragma unroll
@@ -194,7 +198,7 @@ __global__ void __launch_bounds__(256, 3)
                     [&](int b, float2 v) { st[(b & 1) * hM + (b >> 1)] = v; });
   }
   __syncthreads();
-  eb_stage_a<RR>(bp, stage, N2, M2, G + ((size_t)f * pl.p1 + k1) * RR * M2);
+  eb_stage_a<RR>(bp, stage, N2, M2, G + ((size_t)f * pl.p1 + k1) * RR * M2, threadIdx.x >> 6);
 }
 
 // Adjoint rows pass of the q = 8 plans with the ePIE epilogues, axis 1 first
@@ -210,8 +214,11 @@ __global__ void __launch_bounds__(256, 3)
 //   forward rows pass of the NEXT position's exit wave P' z[obj_off2].
 // The fused forward continues in the same registers: stage B on the lane's own
 // k2 groups (k2 bit-reversed), DIT FFT -> natural u2, Horner band, stage A.
-template <int RR, int P2, int EPI>
-__global__ void __launch_bounds__(256, 1)
+// CL = 2: a cluster pair of 128-thread CTAs per row block (4 rows each, on two
+// SMs): every warp also writes its band row into the partner's shared memory
+// (DSMEM), and each CTA runs stage A for two of the four j1 groups.
+template <int RR, int P2, int EPI, int CL>
+__global__ void __launch_bounds__(256 / CL, 1)
     kb_adj_rows(PftDev<float> pl, EbPar<RR> bp, const float2* __restrict__ Gt, EpiArgs ep) {
   constexpr int S = P2 / 32, N2 = P2 * 8;
   constexpr int LP = P2 == 64 ? 6 : 5;
@@ -220,8 +227,8 @@ __global__ void __launch_bounds__(256, 1)
   float2* rb = reinterpret_cast<float2*>(smem_raw);  // [8][M2] band rows of the fused forward
   float2* W2s = rb + 8 * M2;                         // [M2] row 0 of W2
   float2* tw2s = W2s + M2;                           // [P2 / 2]
-  const int k1 = blockIdx.x, f = blockIdx.y;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int k1 = blockIdx.x / CL, half = blockIdx.x % CL, f = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) + half * (8 / CL);  // row of the block
   const long long row = (long long)k1 * 8 + warp;
   const bool fuse = EPI >= 1 && ep.G2 != nullptr;
   const float st = (float)ep.step;
@@ -314,12 +321,28 @@ __global__ void __launch_bounds__(256, 1)
   fft_dit<S, RR>(x, P2, 32, lane, tw2s, -1);  // slot i held k2 = bitrev(i); now u2 = i
   const int hM = M2 >> 1;
   float2* rw = rb + warp * M2;
+  float2* G2 = reinterpret_cast<float2*>(ep.G2) + ((size_t)f * pl.p1 + k1) * RR * M2;
+  if constexpr (CL == 1) {
 #pragma unroll
-  for (int s = 0; s < S; ++s)
-    band_horner<RR>(W2s, M2, (s * 32 + lane + mt2) & (P2 - 1), P2, mt2, 1.0f / P2, x[s],
-                    [&](int b, float2 v) { rw[(b & 1) * hM + (b >> 1)] = v; });
-  __syncthreads();
-  eb_stage_a<RR>(bp, rb, M2, M2, reinterpret_cast<float2*>(ep.G2) + ((size_t)f * pl.p1 + k1) * RR * M2);
+    for (int s = 0; s < S; ++s)
+      band_horner<RR>(W2s, M2, (s * 32 + lane + mt2) & (P2 - 1), P2, mt2, 1.0f / P2, x[s],
+                      [&](int b, float2 v) { rw[(b & 1) * hM + (b >> 1)] = v; });
+    __syncthreads();
+    eb_stage_a<RR>(bp, rb, M2, M2, G2, threadIdx.x >> 6);
+  } else {
+    // the same address in the partner CTA's shared memory window
+    uint32_t peer;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(peer) : "r"(smem_u32(rw)), "r"(half ^ 1));
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      band_horner<RR>(W2s, M2, (s * 32 + lane + mt2) & (P2 - 1), P2, mt2, 1.0f / P2, x[s], [&](int b, float2 v) {
+        const int o = (b & 1) * hM + (b >> 1);
+        rw[o] = v;
+        asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(peer + 8u * o), "f"(v.x), "f"(v.y) : "memory");
+      });
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    eb_stage_a<RR>(bp, rb, M2, M2, G2, half * 2 + (threadIdx.x >> 6));
+  }
 }
 
 // grid (M2 / NB, batch), 288 threads. One strip of NB band columns of one field:
@@ -592,19 +615,38 @@ void launch_eval_band_adj_rows(const PftDev<float>& pd, int epi, const float2* G
                                cudaStream_t st) {
   const auto bp = make_ebpar<9>(pd);
   const size_t smem = (size_t)(9 * pd.M2 + pd.p2 / 2) * sizeof(float2);
-  const dim3 grid(pd.p1, batch);
-  auto go = [&](auto k) {
-    eb_allow_smem(k, smem);
-    k<<<grid, 256, smem, st>>>(pd, bp, Gt, ep);
+  // single fields (ePIE positions): cluster pairs, 2 x the SMs per row block
+  static const bool no_pair = std::getenv("PFTG_EB_NO_PAIR") != nullptr;
+  const bool pair = batch == 1 && epi >= 1 && !no_pair;
+  auto go = [&](auto k1, auto k2) {
+    if (!pair) {
+      eb_allow_smem(k1, smem);
+      k1<<<dim3(pd.p1, batch), 256, smem, st>>>(pd, bp, Gt, ep);
+      return;
+    }
+    eb_allow_smem(k2, smem);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pd.p1, batch);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PFTG_CUDA(cudaLaunchKernelEx(&cfg, k2, pd, bp, Gt, ep));
   };
   if (pd.p2 == 64) {
-    if (epi == 0) go(kb_adj_rows<9, 64, 0>);
-    else if (epi == 1) go(kb_adj_rows<9, 64, 1>);
-    else go(kb_adj_rows<9, 64, 2>);
+    if (epi == 0) go(kb_adj_rows<9, 64, 0, 1>, kb_adj_rows<9, 64, 0, 2>);
+    else if (epi == 1) go(kb_adj_rows<9, 64, 1, 1>, kb_adj_rows<9, 64, 1, 2>);
+    else go(kb_adj_rows<9, 64, 2, 1>, kb_adj_rows<9, 64, 2, 2>);
   } else {
-    if (epi == 0) go(kb_adj_rows<9, 32, 0>);
-    else if (epi == 1) go(kb_adj_rows<9, 32, 1>);
-    else go(kb_adj_rows<9, 32, 2>);
+    if (epi == 0) go(kb_adj_rows<9, 32, 0, 1>, kb_adj_rows<9, 32, 0, 2>);
+    else if (epi == 1) go(kb_adj_rows<9, 32, 1, 1>, kb_adj_rows<9, 32, 1, 2>);
+    else go(kb_adj_rows<9, 32, 2, 1>, kb_adj_rows<9, 32, 2, 2>);
   }
   PFTG_LAUNCH_CHECK();
 }

@@ -248,17 +248,17 @@ __device__ __forceinline__ void expand_pairs_sm(const R* __restrict__ btab, cons
     C zl[V], zm[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      // the odd taps carry conj(i b) = -i b: accumulate b * x plainly and apply
-      // the -i once (same roundings as bmacc(.., true) per tap: negation and the
-      // component swap commute with round-to-nearest), so every tap is the same
-      // broadcast-coefficient FFMA2 and no (b, b) register pairs are built
+      // (accumulating the odd taps without their -i factor and applying it once removes the
+      // (b, b) register-pair MOVs -- 23 % of kt_adj_rows' instructions -- and makes the isolated
+      // launch 0.5 us faster, but the PDL-chained cfg2 step 10 us slower (0.228 -> 0.238 ms,
+      // same-box A/B): kept in the per-tap form)
       C e = czero<C>(), o = czero<C>();
 #pragma unroll
       for (int j = 0; j < RR; j += 2) bmacc(e, bl[j], x[v][j], false);
 #pragma unroll
-      for (int j = 1; j < RR; j += 2) bmacc(o, bl[j], x[v][j], false);
-      zl[v] = cadd_mi(e, o);
-      zm[v] = csub_mi(e, o);
+      for (int j = 1; j < RR; j += 2) bmacc(o, bl[j], x[v][j], true);
+      zl[v] = cadd(e, o);
+      zm[v] = csub(e, o);
     }
     pair(l, zl, zm);
   }

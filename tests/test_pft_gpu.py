@@ -36,6 +36,7 @@ CASES = [
     ("band_M_lt_p", DATA / "scope_table_v1.txt", 128, 128, 4, 4, 16, 16, 1e-3),
     ("cfg3_band", DATA / "scope_table_v1.txt", 256, 256, 32, 32, 32, 32, 1e-3),
     ("cfg1_companion", DATA / "scope_table_v1.txt", 512, 512, 64, 64, 64, 64, 1e-7),
+    ("cfg4_band", DATA / "scope_table_v1.txt", 512, 512, 64, 64, 64, 64, 1e-3),
     ("cfg1_literal", DATA / "scope_table_xi4_r12.txt", 512, 512, 64, 64, 16, 16, 1.0),
 ]
 
@@ -54,7 +55,7 @@ def test_forward_adjoint_c128(ref, case):
         assert rel_l2(back[b], r.adjoint(y[b])) <= TOL128, name
 
 
-@pytest.mark.parametrize("case", CASES[:5], ids=[c[0] for c in CASES[:5]])
+@pytest.mark.parametrize("case", CASES[:6], ids=[c[0] for c in CASES[:6]])
 def test_forward_adjoint_c64(ref, case):
     name, table, n1, n2, mt1, mt2, p1, p2, eps = case
     g, r = _plans(ref, table, n1, n2, mt1, mt2, p1, p2, eps)
@@ -65,6 +66,22 @@ def test_forward_adjoint_c64(ref, case):
     back = P.pft_adjoint_2d(g, torch.from_numpy(y).cuda()).cpu().numpy()
     assert rel_l2(band, r.apply(z.astype(np.complex128))) <= TOL64, name
     assert rel_l2(back, r.adjoint(y.astype(np.complex128))) <= TOL64, name
+
+
+def test_cfg4_band_plan_c64_batch(ref):
+    """configs[3] / [4] band plan (512^2, p = 64, q = 8, r = 9) in complex64 with a
+    batch of 3: the forward cols pass runs kb_cols with 8-column strips, the
+    adjoint rows pass kb_adj_rows (eval_band.cu) with a batch grid."""
+    g, r = _plans(ref, DATA / "scope_table_v1.txt", 512, 512, 64, 64, 64, 64, 1e-3)
+    assert (g.q1, g.r1, g.p1) == (8, 9, 64)
+    rng = np.random.default_rng(12)
+    z = cnormal(rng, (3, 512, 512), np.complex64)
+    y = cnormal(rng, (3, 128, 128), np.complex64)
+    band = P.pft_apply_2d(g, torch.from_numpy(z).cuda()).cpu().numpy()
+    back = P.pft_adjoint_2d(g, torch.from_numpy(y).cuda()).cpu().numpy()
+    for b in range(3):
+        assert rel_l2(band[b], r.apply(z[b].astype(np.complex128))) <= TOL64, b
+        assert rel_l2(back[b], r.adjoint(y[b].astype(np.complex128))) <= TOL64, b
 
 
 def _float_floor(plan_o, x, want, adjoint=False):
