@@ -262,6 +262,8 @@ __global__ void __launch_bounds__(256 / CL, 1)
       for (int s = 0; s < S; ++s) eb_load8(nrow + k2s[s] * 8, vec_n, on[s]);
     }
   }
+  griddep_wait();  // PDL: Gt is the previous kernel's output; everything above is not
+  griddep_launch_dependents();
   const float2* Gblk = Gt + ((size_t)f * pl.p1 + k1) * RR * M2;
   float2 Rv[S][2];
 #pragma unroll
@@ -272,7 +274,7 @@ __global__ void __launch_bounds__(256 / CL, 1)
       float2 acc = czero<float2>();
       if (b < M2) {
 #pragma unroll
-        for (int j = 0; j < RR; ++j) bmacc(acc, b1r[j], __ldg(Gblk + (size_t)j * M2 + b), j & 1);
+        for (int j = 0; j < RR; ++j) bmacc(acc, b1r[j], Gblk[(size_t)j * M2 + b], j & 1);
       }
       Rv[s][i] = acc;
     }
@@ -345,56 +347,206 @@ __global__ void __launch_bounds__(256 / CL, 1)
   }
 }
 
+// kb_adj_rows for one ePIE position of a p2 = 64 plan with every row's two k2
+// slots on two warps (the SPL = 2 idea of kt2_fwd_rows): cluster pair of
+// 256-thread CTAs, warp w <-> (row half * 4 + w / 2, slot w % 2). Both warps of a
+// row run A-dagger and the D-dagger gather of both slots (cheap) and the first,
+// in-thread DIF stage; each then keeps one slot: five shuffle stages on 9 values
+// instead of 18, the B2-dagger expansion, the epilogue and stage B of its 32
+// k2 groups, five DIT stages, and the last (slot-pairing) DIT stage after one
+// exchange through shared memory. Same arithmetic per value as kb_adj_rows
+// (bit-identical results); the per-warp dependent chain is about half as long.
+template <int RR, int EPI>
+__global__ void __launch_bounds__(256, 1)
+    kb_adj_rows_split(PftDev<float> pl, EbPar<RR> bp, const float2* __restrict__ Gt, EpiArgs ep) {
+  constexpr int P2 = 64, N2 = 512, LP = 6;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int M2 = pl.M2, mt2 = pl.mt2;
+  float2* rb = reinterpret_cast<float2*>(smem_raw);  // [8][M2]
+  float2* W2s = rb + 8 * M2;                         // [M2]
+  float2* tw2s = W2s + M2;                           // [32]
+  float2* xch = tw2s + 32;                           // [4 rows][2 slots][RR][32]
+  const int k1 = blockIdx.x >> 1, half = blockIdx.x & 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int rloc = w >> 1, sl = w & 1;
+  const int rowb = half * 4 + rloc;  // row of the block
+  const long long row = (long long)k1 * 8 + rowb;
+  const bool fuse = ep.G2 != nullptr;
+  const float st = (float)ep.step;
+  for (int i = threadIdx.x; i < M2; i += blockDim.x) W2s[i] = pl.W2t[i];
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) tw2s[i] = pl.tw2[i];
+  float b1r[RR];
+#pragma unroll
+  for (int j = 0; j < RR; ++j) b1r[j] = __ldg(pl.Bv1 + rowb * RR + j);
+  const int k2 = bitrev(sl * 32 + lane, LP);
+  float2 pv[8], ov[8], on[8];
+  float2* orow = reinterpret_cast<float2*>(ep.obj) + ep.obj_off + row * ep.obj_ld;
+  float2* prow = reinterpret_cast<float2*>(ep.probe) + row * N2;
+  const bool vec_o = (reinterpret_cast<uintptr_t>(orow) & 15) == 0;
+  const bool vec_p = (reinterpret_cast<uintptr_t>(prow) & 15) == 0;
+  eb_load8(prow + k2 * 8, vec_p, pv);
+  eb_load8(orow + k2 * 8, vec_o, ov);
+  if (EPI == 2 && fuse) {
+    const float2* nrow = reinterpret_cast<const float2*>(ep.obj) + ep.obj_off2 + row * ep.obj_ld;
+    eb_load8(nrow + k2 * 8, (reinterpret_cast<uintptr_t>(nrow) & 15) == 0, on);
+  }
+  griddep_wait();  // PDL: Gt is the previous kernel's output; everything above is not
+  griddep_launch_dependents();
+  const float2* Gblk = Gt + (size_t)k1 * RR * M2;
+  float2 Rv[2][2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int b = ((s * 32 + lane + mt2) & (P2 - 1)) + P2 * i;
+      float2 acc = czero<float2>();
+      if (b < M2) {
+#pragma unroll
+        for (int j = 0; j < RR; ++j) bmacc(acc, b1r[j], Gblk[(size_t)j * M2 + b], j & 1);
+      }
+      Rv[s][i] = acc;
+    }
+  __syncthreads();  // tables
+  float2 xh[1][RR];
+  {
+    float2 x[2][RR];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+#pragma unroll
+      for (int j = 0; j < RR; ++j) x[s][j] = czero<float2>();
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int b = ((s * 32 + lane + mt2) & (P2 - 1)) + P2 * i;
+        if (b < M2) gather_horner<RR>(x[s], W2s[b], static_cast<float>(b - mt2) * (1.0f / P2), Rv[s][i]);
+      }
+    }
+    // first DIF stage (slot pair, h = 32), as fft_dif<2, RR> runs it in-thread
+    const float2 wt = twiddle(tw2s, lane, +1);
+#pragma unroll
+    for (int j = 0; j < RR; ++j) xh[0][j] = sl ? cmul(csub(x[0][j], x[1][j]), wt) : cadd(x[0][j], x[1][j]);
+  }
+  fft_dif<1, RR>(xh, P2, 32, lane, tw2s, +1);
+  {
+    float2 z[8], e[8];
+    eb_expand8<RR>(bp.b2, xh[0], z);
+    if (EPI == 1) {
+#pragma unroll
+      for (int l = 0; l < 8; ++l) {
+        const float2 g = cmulc(pv[l], z[l]);
+        ov[l].x -= st * g.x;
+        ov[l].y -= st * g.y;
+        e[l] = cmul(pv[l], ov[l]);
+      }
+      eb_store8(orow + k2 * 8, vec_o, ov);
+    } else {
+#pragma unroll
+      for (int l = 0; l < 8; ++l) {
+        const float2 g = cmulc(ov[l], z[l]);
+        pv[l].x -= st * g.x;
+        pv[l].y -= st * g.y;
+        e[l] = cmul(pv[l], on[l]);
+      }
+      eb_store8(prow + k2 * 8, vec_p, pv);
+    }
+    if (!fuse) return;
+    eb_contract8<RR>(bp.b2, e, xh[0]);
+  }
+  fft_dit<1, RR>(xh, P2, 32, lane, tw2s, -1);  // the cross-lane stages of fft_dit<2, RR>
+  // last DIT stage (h = 32) pairs the two slots: exchange through shared memory
+  float2* mine = xch + ((rloc * 2 + sl) * RR) * 32 + lane;
+  const float2* other = xch + ((rloc * 2 + (sl ^ 1)) * RR) * 32 + lane;
+#pragma unroll
+  for (int j = 0; j < RR; ++j) mine[j * 32] = xh[0][j];
+  named_sync(1 + rloc, 64);
+  {
+    const float2 wt = twiddle(tw2s, lane, -1);
+#pragma unroll
+    for (int j = 0; j < RR; ++j) {
+      const float2 o = other[j * 32];
+      const float2 a = sl ? o : xh[0][j];                     // slot 0 value
+      const float2 t = cmul(sl ? xh[0][j] : o, wt);           // slot 1 value x twiddle
+      xh[0][j] = sl ? csub(a, t) : cadd(a, t);
+    }
+  }
+  const int hM = M2 >> 1;
+  float2* rw = rb + rowb * M2;
+  uint32_t peer;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(peer) : "r"(smem_u32(rw)), "r"(half ^ 1));
+  band_horner<RR>(W2s, M2, (sl * 32 + lane + mt2) & (P2 - 1), P2, mt2, 1.0f / P2, xh[0], [&](int b, float2 v) {
+    const int o = (b & 1) * hM + (b >> 1);
+    rw[o] = v;
+    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(peer + 8u * o), "f"(v.x), "f"(v.y) : "memory");
+  });
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (threadIdx.x < 128)
+    eb_stage_a<RR>(bp, rb, M2, M2, reinterpret_cast<float2*>(ep.G2) + (size_t)k1 * RR * M2,
+                   half * 2 + (threadIdx.x >> 6));
+}
+
 // grid (M2 / NB, batch), 288 threads. One strip of NB band columns of one field:
-//   G[f][k1][j1][b] -> 64-point FFTs over k1 (two radix-8 passes in shared
-//   memory) -> band rows by Horner over j1 (pft.cpp:150-172, axis-1 half);
+//   G[f][k1][j1][b] -> p1-point FFTs over k1 (two register passes through shared
+//   memory: radix 8 x 8 for p1 = 64, radix 8 x 4 for p1 = 32) -> band rows by
+//   Horner over j1 (pft.cpp:150-172, axis-1 half);
 //   band != nullptr: store the band strip; dcrop + partial: sum (|band| - dcrop)^2
 //   into partial[f * gridDim.x + strip] (evaluator);
 //   ADJ: band residual y - dcrop y / |y| (solver.cpp:61-69), D-dagger gather in
 //   the same registers, inverse FFTs over u1, -> Gout[f][k1][j1][b] (the fused
 //   forward + residual + adjoint cols pass of the ePIE band stage).
-// Transform (j1, bb) lives at Gs[(j1 NB + bb) LDF + ...]: natural index i at
-// i + i / 8, spectrum index m + 8 n at 9 m + n (both radix-8 passes run in
-// place, every half-warp phase on distinct banks).
-constexpr int kEbLdF = 72, kEbColsT = 288;
+// Transform (j1, bb) lives at Gs[(j1 NB + bb) LDF + ...], both passes in place:
+//   p1 = 64: natural index i at i + i / 8, spectrum index m + 8 n at 9 m + n
+//            (every half-warp phase on distinct banks);
+//   p1 = 32: index i = t + 4 k at pad(i), spectrum index m + 8 n at pad(4 m + n),
+//            pad(x) = x + x / 16.
+constexpr int kEbColsT = 288;
+__host__ __device__ constexpr int eb_ldf(int p1) { return p1 == 64 ? 72 : 34; }
 
-template <int RR, int NB, bool ADJ>
+// 4-point DFT, sign -1 (SIGN < 0) or +1, natural in / natural out.
+template <int SIGN>
+__device__ __forceinline__ void dft4(float2 (&a)[4]) {
+  const float2 b0 = cadd(a[0], a[2]), b1 = csub(a[0], a[2]), b2 = cadd(a[1], a[3]), d = csub(a[1], a[3]);
+  const float2 b3 = SIGN < 0 ? make_float2(d.y, -d.x) : make_float2(-d.y, d.x);  // -+ i d
+  a[0] = cadd(b0, b2);
+  a[2] = csub(b0, b2);
+  a[1] = cadd(b1, b3);
+  a[3] = csub(b1, b3);
+}
+
+template <int RR, int NB, bool ADJ, int P1>
 __global__ void __launch_bounds__(kEbColsT, 3)
     kb_cols(PftDev<float> pl, const float2* __restrict__ G, float2* __restrict__ band,
             const float* __restrict__ dcrop, long long dstride, float2* __restrict__ Gout,
             double* __restrict__ partial) {
-  constexpr int P1 = 64, LDF = kEbLdF, NF = RR * NB, NCH = NB / 2;
+  constexpr int LDF = eb_ldf(P1), NF = RR * NB, NCH = NB / 2;
   constexpr int LR = P1 * RR * NCH / kEbColsT;  // 16-byte chunks of the strip per thread
-  constexpr int FR = NF * 8 / kEbColsT;         // radix-8 butterflies per thread and pass
-  static_assert(P1 * RR * NCH % kEbColsT == 0 && NF * 8 % kEbColsT == 0 && NB % 4 == 0, "strip shape");
+  static_assert(P1 * RR * NCH % kEbColsT == 0 && NB % 4 == 0 && (P1 == 64 || P1 == 32), "strip shape");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int M1 = pl.M1, M2 = pl.M2, mt1 = pl.mt1;
   float2* Gs = reinterpret_cast<float2*>(smem_raw);  // [NF][LDF]
-  float2* w64 = Gs + NF * LDF;                       // W64^e, e < 64
-  float2* W1s = w64 + 64;                            // [M1] row 0 of W1
+  float2* wP = Gs + NF * LDF;                        // W_p1^e, e < p1
+  float2* W1s = wP + P1;                             // [M1] row 0 of W1
   float* dcs = reinterpret_cast<float*>(W1s + M1);   // [NB][M1 + 1]
   double* red = reinterpret_cast<double*>(
-      smem_raw + (((size_t)(NF * LDF + 64 + M1) * 8 + (size_t)NB * (M1 + 1) * 4 + 7) & ~size_t(7)));
+      smem_raw + (((size_t)(NF * LDF + P1 + M1) * 8 + (size_t)NB * (M1 + 1) * 4 + 7) & ~size_t(7)));
   const int bx = blockIdx.x, f = blockIdx.y, b0 = bx * NB;
   const int tid = threadIdx.x;
   const float2* Gf = G + (size_t)f * P1 * RR * M2;
+  // position of natural index i / of spectrum index u = m + 8 n inside a transform
+  auto pos_nat = [](int i) { return P1 == 64 ? i + (i >> 3) : i + (i >> 4); };
+  auto pos_spec = [](int u) {
+    if (P1 == 64) return 9 * (u & 7) + (u >> 3);
+    const int x = 4 * (u & 7) + (u >> 3);
+    return x + (x >> 4);
+  };
   // chunk it of the strip: segment (k1, j1) of NB columns, 16-byte chunk c
   auto chunk_of = [&](int it, int& c, int& k1, int& j1) {
     c = (it >> 3) % NCH;
     const int rest = it / (8 * NCH);
-    k1 = (rest & 7) * 8 + (it & 7);
-    j1 = rest >> 3;
+    k1 = (rest % (P1 / 8)) * 8 + (it & 7);
+    j1 = rest / (P1 / 8);
   };
-  float4 q[LR];
-#pragma unroll
-  for (int r = 0; r < LR; ++r) {
-    int c, k1, j1;
-    chunk_of(tid + r * kEbColsT, c, k1, j1);
-    q[r] = __ldg(reinterpret_cast<const float4*>(Gf + ((size_t)k1 * RR + j1) * M2 + b0 + 2 * c));
-  }
-  for (int i = tid; i < 64; i += kEbColsT) {
-    const float2 w = pl.tw1[i & 31];
-    w64[i] = (i & 32) ? make_float2(-w.x, -w.y) : w;
+  for (int i = tid; i < P1; i += kEbColsT) {
+    const float2 w = pl.tw1[i & (P1 / 2 - 1)];
+    wP[i] = (i & (P1 / 2)) ? make_float2(-w.x, -w.y) : w;
   }
   for (int i = tid; i < M1; i += kEbColsT) W1s[i] = pl.W1t[i];
   if (dcrop) {
@@ -408,56 +560,92 @@ __global__ void __launch_bounds__(kEbColsT, 3)
       dcs[(4 * h + 3) * (M1 + 1) + a] = d.w;
     }
   }
+  // programmatic dependent launch (single ePIE positions): the tables above do not
+  // depend on the previous kernel; G does. The dependents are released only after
+  // this kernel's own wait, so their prologues never overlap the kernel before this one.
+  griddep_wait();
+  griddep_launch_dependents();
+  float4 q[LR];
 #pragma unroll
   for (int r = 0; r < LR; ++r) {
     int c, k1, j1;
     chunk_of(tid + r * kEbColsT, c, k1, j1);
-    const int idx = k1 + (k1 >> 3);
+    q[r] = *reinterpret_cast<const float4*>(Gf + ((size_t)k1 * RR + j1) * M2 + b0 + 2 * c);
+  }
+#pragma unroll
+  for (int r = 0; r < LR; ++r) {
+    int c, k1, j1;
+    chunk_of(tid + r * kEbColsT, c, k1, j1);
+    const int idx = pos_nat(k1);
     Gs[(j1 * NB + 2 * c) * LDF + idx] = make_float2(q[r].x, q[r].y);
     Gs[(j1 * NB + 2 * c + 1) * LDF + idx] = make_float2(q[r].z, q[r].w);
   }
   __syncthreads();
-  // pass 1: y[t][m] = W64^(t m) DFT8_k x[t + 8 k], in place at t + 9 m
+  if constexpr (P1 == 64) {
+    // pass 1: y[t][m] = W64^(t m) DFT8_k x[t + 8 k], in place at t + 9 m
+    for (int it = tid; it < NF * 8; it += kEbColsT) {
+      const int t = it & 7;
+      float2* p = Gs + (it >> 3) * LDF + t;
+      float2 a[8];
 #pragma unroll
-  for (int r = 0; r < FR; ++r) {
-    const int it = tid + r * kEbColsT;
-    const int t = it & 7;
-    float2* p = Gs + (it >> 3) * LDF + t;
-    float2 a[8];
+      for (int k = 0; k < 8; ++k) a[k] = p[9 * k];
+      dft8_fwd(a);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = p[9 * k];
-    dft8_fwd(a);
+      for (int m = 1; m < 8; ++m) a[m] = cmul(a[m], wP[(m * t) & 63]);
 #pragma unroll
-    for (int m = 1; m < 8; ++m) a[m] = cmul(a[m], w64[(m * t) & 63]);
+      for (int m = 0; m < 8; ++m) p[9 * m] = a[m];
+    }
+    __syncthreads();
+    // pass 2: X[m + 8 n] = DFT8_t y[t][m], in place at 9 m + n
+    for (int it = tid; it < NF * 8; it += kEbColsT) {
+      float2* p = Gs + (it >> 3) * LDF + 9 * (it & 7);
+      float2 a[8];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) p[9 * m] = a[m];
+      for (int k = 0; k < 8; ++k) a[k] = p[k];
+      dft8_fwd(a);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) p[k] = a[k];
+    }
+  } else {
+    // pass 1: y[t][m] = W32^(t m) DFT8_k x[t + 4 k] (t < 4), in place at pad(t + 4 m)
+    for (int it = tid; it < NF * 4; it += kEbColsT) {
+      const int t = it & 3;
+      float2* p = Gs + (it >> 2) * LDF;
+      float2 a[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = p[pos_nat(t + 4 * k)];
+      dft8_fwd(a);
+#pragma unroll
+      for (int m = 1; m < 8; ++m) a[m] = cmul(a[m], wP[(m * t) & 31]);
+#pragma unroll
+      for (int m = 0; m < 8; ++m) p[pos_nat(t + 4 * m)] = a[m];
+    }
+    __syncthreads();
+    // pass 2: X[m + 8 n] = DFT4_t y[t][m], in place at pad(4 m + n)
+    for (int it = tid; it < NF * 8; it += kEbColsT) {
+      const int m = it & 7;
+      float2* p = Gs + (it >> 3) * LDF;
+      float2 a[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) a[t] = p[pos_nat(4 * m + t)];
+      dft4<-1>(a);
+#pragma unroll
+      for (int n = 0; n < 4; ++n) p[pos_nat(4 * m + n)] = a[n];
+    }
   }
   __syncthreads();
-  // pass 2: X[m + 8 n] = DFT8_t y[t][m], in place at 9 m + n
-#pragma unroll
-  for (int r = 0; r < FR; ++r) {
-    const int it = tid + r * kEbColsT;
-    float2* p = Gs + (it >> 3) * LDF + 9 * (it & 7);
-    float2 a[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = p[k];
-    dft8_fwd(a);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) p[k] = a[k];
-  }
-  __syncthreads();
-  // item (u1, bb): band rows a = u1 + mt1 (mod 64) of column bb by Horner over j1
+  // item (u1, bb): band rows a = u1 + mt1 (mod p1) of column bb by Horner over j1
   double local = 0.0;
   for (int it = tid; it < P1 * NB; it += kEbColsT) {
-    const int u1 = it & 63, bb = it >> 6;
-    float2* p = Gs + bb * LDF + 9 * (u1 & 7) + (u1 >> 3);
+    const int u1 = it & (P1 - 1), bb = it / P1;
+    float2* p = Gs + bb * LDF + pos_spec(u1);
     float2 xs[RR], xa[RR];
 #pragma unroll
     for (int j = 0; j < RR; ++j) {
       xs[j] = p[j * NB * LDF];
       xa[j] = czero<float2>();
     }
-    for (int a = (u1 + mt1) & 63; a < M1; a += P1) {
+    for (int a = (u1 + mt1) & (P1 - 1); a < M1; a += P1) {
       const float base = static_cast<float>(a - mt1) * (1.0f / P1);
       float2 acc = xs[RR - 1];
 #pragma unroll
@@ -492,36 +680,63 @@ __global__ void __launch_bounds__(kEbColsT, 3)
   if (partial) block_sum_store(local, red, partial + (size_t)f * gridDim.x + bx);
   if constexpr (ADJ) {
     __syncthreads();
-    // inverse pass 1: y[t][m] = conj(W64^(t m)) IDFT8_k x[t + 8 k] (index t + 8 k at 9 t + k), in place
+    if constexpr (P1 == 64) {
+      // inverse pass 1: y[t][m] = conj(W64^(t m)) IDFT8_k x[t + 8 k] (index t + 8 k at 9 t + k), in place
+      for (int it = tid; it < NF * 8; it += kEbColsT) {
+        const int t = it & 7;
+        float2* p = Gs + (it >> 3) * LDF + 9 * t;
+        float2 a[8];
 #pragma unroll
-    for (int r = 0; r < FR; ++r) {
-      const int it = tid + r * kEbColsT;
-      const int t = it & 7;
-      float2* p = Gs + (it >> 3) * LDF + 9 * t;
-      float2 a[8];
+        for (int k = 0; k < 8; ++k) a[k] = p[k];
+        dft8<+1>(a);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) a[k] = p[k];
-      dft8<+1>(a);
+        for (int m = 1; m < 8; ++m) {
+          const float2 w = wP[(m * t) & 63];
+          a[m] = cmul(a[m], make_float2(w.x, -w.y));
+        }
 #pragma unroll
-      for (int m = 1; m < 8; ++m) {
-        const float2 w = w64[(m * t) & 63];
-        a[m] = cmul(a[m], make_float2(w.x, -w.y));
+        for (int m = 0; m < 8; ++m) p[m] = a[m];
       }
+      __syncthreads();
+      // inverse pass 2: x[m + 8 n] = IDFT8_t y[t][m] (at 9 t + m), in place: index i at i + i / 8
+      for (int it = tid; it < NF * 8; it += kEbColsT) {
+        float2* p = Gs + (it >> 3) * LDF + (it & 7);
+        float2 a[8];
 #pragma unroll
-      for (int m = 0; m < 8; ++m) p[m] = a[m];
-    }
-    __syncthreads();
-    // inverse pass 2: x[m + 8 n] = IDFT8_t y[t][m] (at 9 t + m), in place: index i at i + i / 8
+        for (int k = 0; k < 8; ++k) a[k] = p[9 * k];
+        dft8<+1>(a);
 #pragma unroll
-    for (int r = 0; r < FR; ++r) {
-      const int it = tid + r * kEbColsT;
-      float2* p = Gs + (it >> 3) * LDF + (it & 7);
-      float2 a[8];
+        for (int k = 0; k < 8; ++k) p[9 * k] = a[k];
+      }
+    } else {
+      // inverse pass 1: y[m][t] = conj(W32^(m t)) IDFT4_n X[m + 8 n] (at pad(4 m + n)), in place
+      for (int it = tid; it < NF * 8; it += kEbColsT) {
+        const int m = it & 7;
+        float2* p = Gs + (it >> 3) * LDF;
+        float2 a[4];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) a[k] = p[9 * k];
-      dft8<+1>(a);
+        for (int n = 0; n < 4; ++n) a[n] = p[pos_nat(4 * m + n)];
+        dft4<+1>(a);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) p[9 * k] = a[k];
+        for (int t = 1; t < 4; ++t) {
+          const float2 w = wP[(m * t) & 31];
+          a[t] = cmul(a[t], make_float2(w.x, -w.y));
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) p[pos_nat(4 * m + t)] = a[t];
+      }
+      __syncthreads();
+      // inverse pass 2: x[t + 4 k] = IDFT8_m y[m][t] (at pad(4 m + t)), in place: index i at pad(i)
+      for (int it = tid; it < NF * 4; it += kEbColsT) {
+        const int t = it & 3;
+        float2* p = Gs + (it >> 2) * LDF;
+        float2 a[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) a[m] = p[pos_nat(4 * m + t)];
+        dft8<+1>(a);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) p[pos_nat(4 * k + t)] = a[k];
+      }
     }
     __syncthreads();
     float2* Go = Gout + (size_t)f * P1 * RR * M2;
@@ -529,7 +744,7 @@ __global__ void __launch_bounds__(kEbColsT, 3)
     for (int r = 0; r < LR; ++r) {
       int c, k1, j1;
       chunk_of(tid + r * kEbColsT, c, k1, j1);
-      const int idx = k1 + (k1 >> 3);
+      const int idx = pos_nat(k1);
       const float2 v0 = Gs[(j1 * NB + 2 * c) * LDF + idx], v1 = Gs[(j1 * NB + 2 * c + 1) * LDF + idx];
       *reinterpret_cast<float4*>(Go + ((size_t)k1 * RR + j1) * M2 + b0 + 2 * c) = make_float4(v0.x, v0.y, v1.x, v1.y);
     }
@@ -547,10 +762,16 @@ EbPar<RR> make_ebpar(const PftDev<float>& pd) {
   return b;
 }
 
-size_t eb_cols_smem(int rr, int nb, int M1) {
-  size_t b = (size_t)(rr * nb * kEbLdF + 64 + M1) * 8 + (size_t)nb * (M1 + 1) * 4;
+size_t eb_cols_smem(int rr, int nb, int M1, int p1) {
+  size_t b = (size_t)(rr * nb * eb_ldf(p1) + p1 + M1) * 8 + (size_t)nb * (M1 + 1) * 4;
   b = (b + 7) & ~size_t(7);
   return b + 16 * sizeof(double);
+}
+
+// programmatic dependent launch between the kernels of one ePIE position (PFTG_EB_NO_PDL: off)
+bool eb_pdl() {
+  static const bool off = std::getenv("PFTG_EB_NO_PDL") != nullptr;
+  return !off;
 }
 
 template <class K>
@@ -566,7 +787,8 @@ bool eval_band_rows_ok(const PftDev<float>& pd) {
 }
 
 bool eval_band_cols_ok(const PftDev<float>& pd) {
-  return pd.p1 == 64 && pd.r1 == 9 && pd.M2 % 8 == 0 && eb_cols_smem(9, 8, pd.M1) <= 200 * 1024;
+  return (pd.p1 == 64 || pd.p1 == 32) && pd.r1 == 9 && pd.M2 % 8 == 0 &&
+         eb_cols_smem(9, 8, pd.M1, pd.p1) <= 200 * 1024;
 }
 
 void launch_eval_band_rows(const PftDev<float>& pd, const float2* frame, long long ld, const long long* offs,
@@ -590,19 +812,39 @@ void launch_eval_band_rows(const PftDev<float>& pd, const float2* frame, long lo
 // one radix-8 butterfly per thread and pass. Gout != nullptr: residual + adjoint (needs dcrop).
 void launch_eval_band_cols(const PftDev<float>& pd, int nb, const float2* G, float2* band, const float* dcrop,
                            long long dstride, float2* Gout, double* partial, int batch, cudaStream_t st) {
-  const size_t smem = eb_cols_smem(9, nb, pd.M1);
+  const size_t smem = eb_cols_smem(9, nb, pd.M1, pd.p1);
   const dim3 grid(pd.M2 / nb, batch);
   ProfScope prof(st, K_FWD_COLS);
   auto go = [&](auto k) {
     eb_allow_smem(k, smem);
-    k<<<grid, kEbColsT, smem, st>>>(pd, G, band, dcrop, dstride, Gout, partial);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kEbColsT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = (batch == 1 && Gout && eb_pdl()) ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PFTG_CUDA(cudaLaunchKernelEx(&cfg, k, pd, G, band, dcrop, dstride, Gout, partial));
   };
-  if (nb == 8) {
-    if (Gout) go(kb_cols<9, 8, true>);
-    else go(kb_cols<9, 8, false>);
+  if (pd.p1 == 64) {
+    if (nb == 8) {
+      if (Gout) go(kb_cols<9, 8, true, 64>);
+      else go(kb_cols<9, 8, false, 64>);
+    } else {
+      if (Gout) go(kb_cols<9, 4, true, 64>);
+      else go(kb_cols<9, 4, false, 64>);
+    }
   } else {
-    if (Gout) go(kb_cols<9, 4, true>);
-    else go(kb_cols<9, 4, false>);
+    if (nb == 8) {
+      if (Gout) go(kb_cols<9, 8, true, 32>);
+      else go(kb_cols<9, 8, false, 32>);
+    } else {
+      if (Gout) go(kb_cols<9, 4, true, 32>);
+      else go(kb_cols<9, 4, false, 32>);
+    }
   }
   PFTG_LAUNCH_CHECK();
 }
@@ -617,27 +859,41 @@ void launch_eval_band_adj_rows(const PftDev<float>& pd, int epi, const float2* G
   const size_t smem = (size_t)(9 * pd.M2 + pd.p2 / 2) * sizeof(float2);
   // single fields (ePIE positions): cluster pairs, 2 x the SMs per row block
   static const bool no_pair = std::getenv("PFTG_EB_NO_PAIR") != nullptr;
+  static const bool no_split = std::getenv("PFTG_EB_NO_SPLIT") != nullptr;
   const bool pair = batch == 1 && epi >= 1 && !no_pair;
+  auto launch_pair = [&](auto k, int threads, size_t sm) {
+    eb_allow_smem(k, sm);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pd.p1, batch);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = eb_pdl() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    PFTG_CUDA(cudaLaunchKernelEx(&cfg, k, pd, bp, Gt, ep));
+  };
+  if (pair && pd.p2 == 64 && !no_split) {
+    // one position of a p2 = 64 plan: the two k2 slots of a row on two warps
+    const size_t sm = smem + (size_t)4 * 2 * 9 * 32 * sizeof(float2);
+    if (epi == 1) launch_pair(kb_adj_rows_split<9, 1>, 256, sm);
+    else launch_pair(kb_adj_rows_split<9, 2>, 256, sm);
+    PFTG_LAUNCH_CHECK();
+    return;
+  }
   auto go = [&](auto k1, auto k2) {
     if (!pair) {
       eb_allow_smem(k1, smem);
       k1<<<dim3(pd.p1, batch), 256, smem, st>>>(pd, bp, Gt, ep);
       return;
     }
-    eb_allow_smem(k2, smem);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * pd.p1, batch);
-    cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    PFTG_CUDA(cudaLaunchKernelEx(&cfg, k2, pd, bp, Gt, ep));
+    launch_pair(k2, 128, smem);
   };
   if (pd.p2 == 64) {
     if (epi == 0) go(kb_adj_rows<9, 64, 0, 1>, kb_adj_rows<9, 64, 0, 2>);
