@@ -129,6 +129,25 @@ __global__ void __launch_bounds__(256) ke_rows512_epie(const float2* __restrict_
   float2* orow = frame + off + (long long)r * ld;
   float2* prow = probe + (size_t)r * 512;
   float2 a[8];
+  // Programmatic dependent launch (per-position graphs): the epilogue's operands
+  // (probe / object rows, next window) were last written at least two kernels back,
+  // so they are requested before the wait; X / X2 (the previous kernel's output)
+  // after it. The dependents are released only after this kernel's own wait.
+  float2 pvv[8], ovv[8], nvv[8];
+  if (MODE != E512_FWD) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      pvv[k] = prow[l + 64 * k];
+      ovv[k] = orow[l + 64 * k];
+    }
+    if (MODE == E512_PROBE && fuse) {
+      const float2* nrow = frame + off_next + (long long)r * ld;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) nvv[k] = nrow[l + 64 * k];
+    }
+  }
+  griddep_wait();
+  griddep_launch_dependents();
   if (MODE == E512_FWD) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) a[k] = cmul(prow[l + 64 * k], orow[l + 64 * k]);
@@ -153,8 +172,8 @@ __global__ void __launch_bounds__(256) ke_rows512_epie(const float2* __restrict_
       float2 proj = a[k];
       proj.x *= scale;
       proj.y *= scale;
-      const float2 pv = prow[c];
-      float2 o = orow[c];
+      const float2 pv = pvv[k];
+      float2 o = ovv[k];
       const float2 resid = csub(cmul(pv, o), proj);  // probe*z - projected
       const float2 gr = cmulc(pv, resid);
       o.x -= step * gr.x;
@@ -177,8 +196,8 @@ __global__ void __launch_bounds__(256) ke_rows512_epie(const float2* __restrict_
     float2 proj = a[k];
     proj.x *= scale;
     proj.y *= scale;
-    float2 pv = prow[c];
-    const float2 o = orow[c];
+    float2 pv = pvv[k];
+    const float2 o = ovv[k];
     const float2 resid = csub(cmul(pv, o), proj);
     const float2 gr = cmulc(o, resid);
     pv.x -= step * gr.x;
@@ -190,9 +209,8 @@ __global__ void __launch_bounds__(256) ke_rows512_epie(const float2* __restrict_
     // the next scan position's forward row transform (E512_FWD of position
     // j+1) from the probe row just updated here: its object rows were final
     // after the object-update kernel, and this group owns probe row r
-    const float2* nrow = frame + off_next + (long long)r * ld;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = cmul(a[k], nrow[l + 64 * k]);
+    for (int k = 0; k < 8; ++k) a[k] = cmul(a[k], nvv[k]);
     gsync();  // S free
     fft512<-1>(a, S, tws, l, gsync);
 #pragma unroll
@@ -215,10 +233,11 @@ __global__ void __launch_bounds__(64 * NCOL) ke_cols512_proj(float2* X, const fl
   float2 a[8];
   float dv[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    a[k] = X[(size_t)(t + 64 * k) * 512 + col];
-    dv[k] = d[(size_t)(t + 64 * k) * 512 + col];
-  }
+  for (int k = 0; k < 8; ++k) dv[k] = d[(size_t)(t + 64 * k) * 512 + col];
+  griddep_wait();  // PDL: the measured magnitudes and the twiddles do not depend on the previous kernel, X does
+  griddep_launch_dependents();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = X[(size_t)(t + 64 * k) * 512 + col];
   __syncthreads();  // tws ready
   float2* S = sbuf + c * CS;
   auto bsync = []() { __syncthreads(); };
@@ -321,6 +340,25 @@ __global__ void __launch_bounds__(128) ke_rows256_epie(const float2* __restrict_
   float2* orow = frame + off + (long long)r * ld;
   float2* prow = probe + (size_t)r * 256;
   float2 a[8];
+  // Programmatic dependent launch (per-position graphs): the epilogue's operands
+  // (probe / object rows, next window) were last written at least two kernels back,
+  // so they are requested before the wait; X / X2 (the previous kernel's output)
+  // after it. The dependents are released only after this kernel's own wait.
+  float2 pvv[8], ovv[8], nvv[8];
+  if (MODE != E512_FWD) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      pvv[k] = prow[l + 32 * k];
+      ovv[k] = orow[l + 32 * k];
+    }
+    if (MODE == E512_PROBE && fuse) {
+      const float2* nrow = frame + off_next + (long long)r * ld;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) nvv[k] = nrow[l + 32 * k];
+    }
+  }
+  griddep_wait();
+  griddep_launch_dependents();
   if (MODE == E512_FWD) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) a[k] = cmul(prow[l + 32 * k], orow[l + 32 * k]);
@@ -345,8 +383,8 @@ __global__ void __launch_bounds__(128) ke_rows256_epie(const float2* __restrict_
       float2 proj = a[k];
       proj.x *= scale;
       proj.y *= scale;
-      const float2 pv = prow[c];
-      float2 o = orow[c];
+      const float2 pv = pvv[k];
+      float2 o = ovv[k];
       const float2 resid = csub(cmul(pv, o), proj);
       const float2 gr = cmulc(pv, resid);
       o.x -= step * gr.x;
@@ -368,8 +406,8 @@ __global__ void __launch_bounds__(128) ke_rows256_epie(const float2* __restrict_
     float2 proj = a[k];
     proj.x *= scale;
     proj.y *= scale;
-    float2 pv = prow[c];
-    const float2 o = orow[c];
+    float2 pv = pvv[k];
+    const float2 o = ovv[k];
     const float2 resid = csub(cmul(pv, o), proj);
     const float2 gr = cmulc(o, resid);
     pv.x -= step * gr.x;
@@ -378,9 +416,8 @@ __global__ void __launch_bounds__(128) ke_rows256_epie(const float2* __restrict_
     a[k] = pv;
   }
   if (fuse) {  // next position's forward row transform (see ke_rows512_epie)
-    const float2* nrow = frame + off_next + (long long)r * ld;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = cmul(a[k], nrow[l + 32 * k]);
+    for (int k = 0; k < 8; ++k) a[k] = cmul(a[k], nvv[k]);
     __syncwarp();
     fft256<-1>(a, S, tws, l, wsync);
 #pragma unroll
@@ -401,10 +438,11 @@ __global__ void __launch_bounds__(32 * NCOL) ke_cols256_proj(float2* X, const fl
   float2 a[8];
   float dv[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    a[k] = X[(size_t)(t + 32 * k) * 256 + col];
-    dv[k] = d[(size_t)(t + 32 * k) * 256 + col];
-  }
+  for (int k = 0; k < 8; ++k) dv[k] = d[(size_t)(t + 32 * k) * 256 + col];
+  griddep_wait();  // PDL: see ke_cols512_proj
+  griddep_launch_dependents();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = X[(size_t)(t + 32 * k) * 256 + col];
   __syncthreads();
   float2* S = sbuf + c * CS;
   auto bsync = []() { __syncthreads(); };

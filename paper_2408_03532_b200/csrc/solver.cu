@@ -233,6 +233,26 @@ inline bool use_fft256(const pftg_solver& s) {
   return !off && s.wr == 256 && s.wc == 256;
 }
 
+// Launch with programmatic stream serialization (also inside stream capture: the
+// graph gets programmatic edges). The kernels release their dependents only after
+// their own griddepcontrol.wait, so a kernel's prologue and operand prefetch overlap
+// its predecessor, never the kernel before that. PFTG_FFT_NO_PDL=1: plain launches.
+template <class... KA, class... A>
+void launch_pdl_pos(void (*kernel)(KA...), dim3 grid, dim3 block, cudaStream_t st, A&&... args) {
+  static const bool off = std::getenv("PFTG_FFT_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  PFTG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...));
+}
+
 // jn: the next position in this sweep's visit order (-1 for the last): blind
 // FFT-stage positions fuse the next position's forward row transform into
 // their probe-update kernel (cross-position fusion, 5 -> 4 launches each).
@@ -289,25 +309,25 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
       const float scale = 1.0f / static_cast<float>(n);
       if (!s.fwd_ready) {
         ProfScope prof(st, K_FFT_ROWS);
-        ke_rows512_epie<E512_FWD><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, 1.f, 0.f, 0,
+        launch_pdl_pos(ke_rows512_epie<E512_FWD>, dim3(128), dim3(256), st, tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, 1.f, 0.f, 0,
                                                          0);
       }
       {
         ProfScope prof(st, K_FFT_COLS);
-        ke_cols512_proj<4><<<128, 256, 0, st>>>(X, dn, tw);
+        launch_pdl_pos(ke_cols512_proj<4>, dim3(128), dim3(256), st, X, dn, tw);
       }
       {
         ProfScope prof(st, K_FFT_ROWS);
-        ke_rows512_epie<E512_OBJ><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
+        launch_pdl_pos(ke_rows512_epie<E512_OBJ>, dim3(128), dim3(256), st, tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
                                                        (float)s.cfg.beta, blind ? 1 : 0, 0);
       }
       if (blind) {
         {
           ProfScope prof(st, K_FFT_COLS);
-          ke_cols512_proj<4><<<128, 256, 0, st>>>(X2, dn, tw);
+          launch_pdl_pos(ke_cols512_proj<4>, dim3(128), dim3(256), st, X2, dn, tw);
         }
         ProfScope prof(st, K_FFT_ROWS);
-        ke_rows512_epie<E512_PROBE><<<128, 256, 0, st>>>(tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
+        launch_pdl_pos(ke_rows512_epie<E512_PROBE>, dim3(128), dim3(256), st, tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
                                                          (float)s.cfg.gamma, jn >= 0 ? 1 : 0,
                                                          jn >= 0 ? s.offs[jn] : 0);
       }
@@ -325,25 +345,25 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
       const float scale = 1.0f / static_cast<float>(n);
       if (!s.fwd_ready) {
         ProfScope prof(st, K_FFT_ROWS);
-        ke_rows256_epie<E512_FWD><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, 1.f, 0.f, 0,
+        launch_pdl_pos(ke_rows256_epie<E512_FWD>, dim3(64), dim3(128), st, tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, 1.f, 0.f, 0,
                                                         0);
       }
       {
         ProfScope prof(st, K_FFT_COLS);
-        ke_cols256_proj<4><<<64, 128, 0, st>>>(X, dn, tw);
+        launch_pdl_pos(ke_cols256_proj<4>, dim3(64), dim3(128), st, X, dn, tw);
       }
       {
         ProfScope prof(st, K_FFT_ROWS);
-        ke_rows256_epie<E512_OBJ><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
+        launch_pdl_pos(ke_rows256_epie<E512_OBJ>, dim3(64), dim3(128), st, tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
                                                       (float)s.cfg.beta, blind ? 1 : 0, 0);
       }
       if (blind) {
         {
           ProfScope prof(st, K_FFT_COLS);
-          ke_cols256_proj<4><<<64, 128, 0, st>>>(X2, dn, tw);
+          launch_pdl_pos(ke_cols256_proj<4>, dim3(64), dim3(128), st, X2, dn, tw);
         }
         ProfScope prof(st, K_FFT_ROWS);
-        ke_rows256_epie<E512_PROBE><<<64, 128, 0, st>>>(tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
+        launch_pdl_pos(ke_rows256_epie<E512_PROBE>, dim3(64), dim3(128), st, tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
                                                         (float)s.cfg.gamma, jn >= 0 ? 1 : 0,
                                                         jn >= 0 ? s.offs[jn] : 0);
       }
@@ -385,7 +405,11 @@ void enqueue_tv(pftg_solver& s, bool band);
 // the per-position graph of four kernels.
 template <class R>
 bool persistent_fft(const pftg_solver& s, bool band) {
-  return sizeof(R) == 4 && !band && !s.cfg.shuffled && !knobs().no_persist && (use_fft512(s) || use_fft256(s));
+  // Default since the per-position kernels prefetch their epilogue operands and are chained by
+  // programmatic dependent launch: the graph (cfg3 FFT stage 74.0k updates/s, cfg4 46.6k) beats
+  // this sweep (49.5k / 44.0k). PFTG_PERSIST=1 selects the persistent sweeps.
+  static const bool want = std::getenv("PFTG_PERSIST") != nullptr;
+  return want && sizeof(R) == 4 && !band && !s.cfg.shuffled && !knobs().no_persist && (use_fft512(s) || use_fft256(s));
 }
 
 template <class R>

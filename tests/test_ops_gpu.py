@@ -448,7 +448,9 @@ def test_persistent_fft_sweep_bit_identical(tmp_path):
     # PFTG_EVAL_BAND_OLD=12: the band stage on the streaming kernels, whose bodies the
     # persistent band sweep shares (the default band stage runs eval_band.cu's kernels
     # per position, see test_band_stage_axis_reordered_kernels)
-    for tag, extra in (("persist", {}), ("graph", {"PFTG_NO_PERSIST": "1"})):
+    # PFTG_PERSIST=1: the persistent sweeps (the default is the per-position graph, whose
+    # kernels are chained by programmatic dependent launch)
+    for tag, extra in (("persist", {"PFTG_PERSIST": "1"}), ("graph", {"PFTG_NO_PERSIST": "1"})):
         env = {**os.environ, "PFTG_EVAL_BAND_OLD": "12", **extra}
         out = tmp_path / f"{tag}.npz"
         subprocess.run([sys.executable, str(script), str(ROOT), str(out)], env=env, check=True, timeout=600)
