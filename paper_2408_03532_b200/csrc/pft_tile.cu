@@ -54,10 +54,12 @@ void launch_tile(void (*kernel)(KA...), dim3 grid, dim3 block, size_t smem, cuda
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  // PDL measured slower for these short kernels (cfg1: 52.6 vs 47.1 us per
-  // forward + adjoint, tools/cfg1_time): plain stream order
+  // Programmatic dependent launch, also inside graph capture. Every tile kernel releases
+  // its dependents right after its own griddepcontrol.wait, so only the next kernel's launch
+  // and table prologue overlap the running one (releasing at entry let three or four
+  // short kernels pile up on the SMs: 52.6 vs 47.1 us per forward + adjoint).
   (void)capturing;
-  at[0].val.programmaticStreamSerializationAllowed = 0;
+  at[0].val.programmaticStreamSerializationAllowed = knobs().no_pdl ? 0 : 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   PFTG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...));
@@ -100,10 +102,10 @@ __global__ void __launch_bounds__(256) kq_fwd_ab(PftDev<R> pd, const Cx<R>* __re
   C* T = tile + q1 * q2;
   R* b1 = reinterpret_cast<R*>(T + r1 * q2);
   R* b2 = b1 + q1 * r1;
-  griddep_launch_dependents();
   for (int i = threadIdx.x; i < q1 * r1; i += blockDim.x) b1[i] = pd.Bv1[i];
   for (int i = threadIdx.x; i < q2 * r2; i += blockDim.x) b2[i] = pd.Bv2[i];
   griddep_wait();  // z may be the previous kernel's output
+  griddep_launch_dependents();  // after the wait: one kernel of look-ahead, never two
   const C* src = z + f * bstride + (long long)k1 * q1 * n2 + (long long)k2 * q2;
   gather_smem<8>(tile, q1 * q2, [&](int i) {
     const int l1 = i / q2, l2 = i - l1 * q2;
@@ -139,10 +141,10 @@ __global__ void __launch_bounds__(256) kq_fft2(PftDev<R> pd, Cx<R>* __restrict__
   C* s = reinterpret_cast<C*>(sm);
   C* tw1 = s + p1 * p2;
   C* tw2 = tw1 + p1 / 2;
-  griddep_launch_dependents();
   for (int i = threadIdx.x; i < p1 / 2; i += blockDim.x) tw1[i] = pd.tw1[i];
   for (int i = threadIdx.x; i < p2 / 2; i += blockDim.x) tw2[i] = pd.tw2[i];
   griddep_wait();
+  griddep_launch_dependents();  // after the wait: one kernel of look-ahead, never two
   C* g = Cg + (size_t)blockIdx.y * p1 * p2 * rr + blockIdx.x;
   {
     constexpr int U = 4;
@@ -209,7 +211,6 @@ __global__ void __launch_bounds__(128) kq_band(PftDev<R> pd, const Cx<R>* __rest
   const int a0 = band_first(u1, pd.mt1, p1), b0 = band_first(u2, pd.mt2, p2);
   const int na = a0 < M1 ? (M1 - 1 - a0) / p1 + 1 : 0;
   const int nb = b0 < M2 ? (M2 - 1 - b0) / p2 + 1 : 0;
-  griddep_launch_dependents();
   if (na == 0 || nb == 0) return;
   C* S = reinterpret_cast<C*>(sm);  // [r1][r2]
   C* E = S + r1 * r2;               // [r1][nb]
@@ -225,6 +226,7 @@ __global__ void __launch_bounds__(128) kq_band(PftDev<R> pd, const Cx<R>* __rest
     w2[i] = pd.W2t[(size_t)j2 * M2 + b0 + bi * p2];
   }
   griddep_wait();
+  griddep_launch_dependents();  // after the wait: one kernel of look-ahead, never two
   const C* slice = Cg + ((size_t)(f * p1 + u1) * p2 + u2) * (size_t)(r1 * r2);
   gather_smem<4>(S, r1 * r2, [&](int i) { return slice[i]; });
   __syncthreads();
@@ -261,7 +263,6 @@ __global__ void __launch_bounds__(256) kq_adj_band(PftDev<R> pd, const Cx<R>* __
   C* w1 = Y + na * nb;              // [na][r1] conj(W1[a][j1])
   C* w2 = w1 + na * r1;             // [nb][r2] conj(W2[b][j2])
   C* F = w2 + nb * r2;              // [na][r1][nb] conj(W1[a][j1]) y[a][b]
-  griddep_launch_dependents();
   for (int i = threadIdx.x; i < na * r1; i += blockDim.x) {
     const int ai = i / r1, j1 = i - ai * r1;
     C w = pd.W1t[(size_t)j1 * M1 + a0 + ai * p1];
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(256) kq_adj_band(PftDev<R> pd, const Cx<R>* __
     w2[i] = w;
   }
   griddep_wait();
+  griddep_launch_dependents();  // after the wait: one kernel of look-ahead, never two
   const C* yf = band + (size_t)f * M1 * M2;
   for (int i = threadIdx.x; i < na * nb; i += blockDim.x) {
     const int ai = i / nb, bi = i - ai * nb;
@@ -314,10 +316,10 @@ __global__ void __launch_bounds__(256) kq_adj_ab(PftDev<R> pd, const Cx<R>* __re
   C* T = S + r1 * r2;               // [r1][q2]
   R* b1 = reinterpret_cast<R*>(T + r1 * q2);
   R* b2 = b1 + q1 * r1;
-  griddep_launch_dependents();
   for (int i = threadIdx.x; i < q1 * r1; i += blockDim.x) b1[i] = pd.Bv1[i];
   for (int i = threadIdx.x; i < q2 * r2; i += blockDim.x) b2[i] = pd.Bv2[i];
   griddep_wait();
+  griddep_launch_dependents();  // after the wait: one kernel of look-ahead, never two
   const C* slice = Cg + ((size_t)(f * pd.p1 + k1) * pd.p2 + k2) * (size_t)(r1 * r2);
   gather_smem<4>(S, r1 * r2, [&](int i) { return slice[i]; });
   __syncthreads();
