@@ -141,6 +141,21 @@ int pftg_adjoint_2d_host(const pftg_plan* plan, int dtype, const void* band, voi
  * streams so H2D and D2H copies overlap (full-duplex PCIe). Results are
  * bit-identical to the two separate calls. */
 int pftg_fwd_adj_2d_host(const pftg_plan* plan, int dtype, const void* z, void* band, void* back, size_t batch);
+/* Multi-device forms of the three host-buffer calls for a C / C++ host that drives
+ * several GPUs from ONE process (BASELINE configs[1]: "batch 64 ... sharded across
+ * 1/2/4/8 GPUs"; fields are independent, pft.cpp:119-226): the batch is
+ * split in contiguous blocks of batch / ndev fields (sizes differ by <= 1, the same
+ * split as paper_2408_03532_b200.dist.shard_range) over devices[0 .. ndev), one host
+ * thread per block running the streamed single-device call on its device. No
+ * data-path collective; the union of the blocks is bit-identical to the
+ * single-device result. A device may be listed more than once. The caller's
+ * current device is unchanged. */
+int pftg_apply_2d_host_multi(const pftg_plan* plan, int dtype, const void* z, void* band, size_t batch,
+                             const int* devices, int ndev);
+int pftg_adjoint_2d_host_multi(const pftg_plan* plan, int dtype, const void* band, void* z, size_t batch,
+                               const int* devices, int ndev);
+int pftg_fwd_adj_2d_host_multi(const pftg_plan* plan, int dtype, const void* z, void* band, void* back,
+                               size_t batch, const int* devices, int ndev);
 
 /* band_residual (solver.hpp:63): A*(A x - dcrop .* exp(i arg(A x))), batched;
  * dcrop is real [batch][2mt1][2mt2]. */

@@ -26,6 +26,7 @@ EXPORTS = (
     "pftg_plan_2d", "pftg_plan_from_tables", "pftg_plan_load", "pftg_plan_save", "pftg_plan_free", "pftg_plan_info",
     "pftg_plan_tables",
     "pftg_apply_2d_dev", "pftg_adjoint_2d_dev", "pftg_apply_2d_host", "pftg_adjoint_2d_host", "pftg_fwd_adj_2d_host",
+    "pftg_apply_2d_host_multi", "pftg_adjoint_2d_host_multi", "pftg_fwd_adj_2d_host_multi",
     "pftg_band_residual_dev",
     "pftg_fft2_dev", "pftg_fft2_host", "pftg_project_modulus_dev", "pftg_crop_centered_dev",
     "pftg_window_slice_dev", "pftg_set_window_dev", "pftg_pie_object_update_dev",
@@ -87,6 +88,10 @@ def lib():
     L.pftg_apply_2d_host.argtypes = [vp, C.c_int, vp, vp, sz]
     L.pftg_adjoint_2d_host.argtypes = [vp, C.c_int, vp, vp, sz]
     L.pftg_fwd_adj_2d_host.argtypes = [vp, C.c_int, vp, vp, vp, sz]
+    ip = C.POINTER(C.c_int)
+    L.pftg_apply_2d_host_multi.argtypes = [vp, C.c_int, vp, vp, sz, ip, C.c_int]
+    L.pftg_adjoint_2d_host_multi.argtypes = [vp, C.c_int, vp, vp, sz, ip, C.c_int]
+    L.pftg_fwd_adj_2d_host_multi.argtypes = [vp, C.c_int, vp, vp, vp, sz, ip, C.c_int]
     L.pftg_band_residual_dev.argtypes = [vp, C.c_int, vp, vp, vp, sz, vp]
     L.pftg_fft2_dev.argtypes = [C.c_int, vp, vp, sz, sz, sz, C.c_int, vp]
     L.pftg_fft2_host.argtypes = [C.c_int, vp, vp, sz, sz, sz, C.c_int]

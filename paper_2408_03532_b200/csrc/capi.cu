@@ -14,6 +14,8 @@
 
 #include "../../include/pftg.h"
 #include "eval_fft.cuh"
+#include <thread>
+
 #include "internal.hpp"
 
 namespace pftg {
@@ -1162,7 +1164,8 @@ int pftg_adjoint_2d_dev(const pftg_plan* plan, int dtype, const void* band, void
   });
 }
 
-int pftg_apply_2d_host(const pftg_plan* plan, int dtype, const void* z, void* band, size_t batch) {
+extern "C++" int apply_2d_host_impl(const pftg_plan* plan, int dtype, const void* z, void* band, size_t batch,
+                                    size_t total) {
   return guarded([&] {
     check_plan(plan);
     check_dtype(dtype);
@@ -1173,7 +1176,7 @@ int pftg_apply_2d_host(const pftg_plan* plan, int dtype, const void* z, void* ba
       using R = decltype(tag);
       const std::size_t chunk = host_chunk(batch, sizeof(Cx<R>) * nz);
       host_pipeline<R>(batch, nz, nb, z, band, chunk, [&](Cx<R>* din, Cx<R>* dout, std::size_t nbat, cudaStream_t s) {
-        apply_dev<R>(plan, din, dout, nbat, s, batch);
+        apply_dev<R>(plan, din, dout, nbat, s, total);
       });
     };
     if (dtype == PFTG_C64) run(float{});
@@ -1181,7 +1184,8 @@ int pftg_apply_2d_host(const pftg_plan* plan, int dtype, const void* z, void* ba
   });
 }
 
-int pftg_adjoint_2d_host(const pftg_plan* plan, int dtype, const void* band, void* z, size_t batch) {
+extern "C++" int adjoint_2d_host_impl(const pftg_plan* plan, int dtype, const void* band, void* z, size_t batch,
+                                      size_t total) {
   return guarded([&] {
     check_plan(plan);
     check_dtype(dtype);
@@ -1192,7 +1196,7 @@ int pftg_adjoint_2d_host(const pftg_plan* plan, int dtype, const void* band, voi
       using R = decltype(tag);
       const std::size_t chunk = host_chunk(batch, sizeof(Cx<R>) * nz);
       host_pipeline<R>(batch, nb, nz, band, z, chunk, [&](Cx<R>* din, Cx<R>* dout, std::size_t nbat, cudaStream_t s) {
-        adjoint_dev<R>(plan, din, dout, nbat, s, batch);
+        adjoint_dev<R>(plan, din, dout, nbat, s, total);
       });
     };
     if (dtype == PFTG_C64) run(float{});
@@ -1205,7 +1209,8 @@ int pftg_adjoint_2d_host(const pftg_plan* plan, int dtype, const void* band, voi
 // so the H2D copy of chunk k+1 runs while chunk k's results (band and
 // back-projection) travel D2H (streams round robin): both PCIe directions are busy at once, which
 // the two separate calls (H2D-bound apply, D2H-bound adjoint) cannot do.
-int pftg_fwd_adj_2d_host(const pftg_plan* plan, int dtype, const void* z, void* band, void* back, size_t batch) {
+extern "C++" int fwd_adj_2d_host_impl(const pftg_plan* plan, int dtype, const void* z, void* band, void* back,
+                                      size_t batch, size_t total) {
   return guarded([&] {
     check_plan(plan);
     check_dtype(dtype);
@@ -1236,8 +1241,8 @@ int pftg_fwd_adj_2d_host(const pftg_plan* plan, int dtype, const void* z, void* 
                                         cudaMemcpyHostToDevice, s));
             },
             [&](int k, std::size_t m, cudaStream_t s) {
-              apply_dev<R>(plan, zi[k], bo[k], m, s, batch);
-              adjoint_dev<R>(plan, bo[k], zo[k], m, s, batch);
+              apply_dev<R>(plan, zi[k], bo[k], m, s, total);
+              adjoint_dev<R>(plan, bo[k], zo[k], m, s, total);
             },
             [&](int k, std::size_t b0, std::size_t m, cudaStream_t s) {
               PFTG_CUDA(cudaMemcpyAsync(static_cast<C*>(back) + b0 * nz, zo[k], sizeof(C) * nz * m,
@@ -1250,6 +1255,98 @@ int pftg_fwd_adj_2d_host(const pftg_plan* plan, int dtype, const void* z, void* 
     };
     if (dtype == PFTG_C64) run(float{});
     else run(double{});
+  });
+}
+
+// `total` = the caller's whole batch: the kernel path (tile / streaming) is chosen on it, so
+// a block of a multi-device call runs the same arithmetic as the single-device call
+int pftg_apply_2d_host(const pftg_plan* plan, int dtype, const void* z, void* band, size_t batch) {
+  return apply_2d_host_impl(plan, dtype, z, band, batch, batch);
+}
+int pftg_adjoint_2d_host(const pftg_plan* plan, int dtype, const void* band, void* z, size_t batch) {
+  return adjoint_2d_host_impl(plan, dtype, band, z, batch, batch);
+}
+int pftg_fwd_adj_2d_host(const pftg_plan* plan, int dtype, const void* z, void* band, void* back, size_t batch) {
+  return fwd_adj_2d_host_impl(plan, dtype, z, band, back, batch, batch);
+}
+
+extern "C++" {
+namespace {
+// Contiguous blocks of the batch over devices[0 .. ndev), one host thread per block;
+// call(b0, m) runs a single-device host-buffer entry point on fields [b0, b0 + m).
+template <class F>
+int run_multi(const pftg_plan* plan, int dtype, std::size_t batch, const int* devices, int ndev, F&& call) {
+  int rc0 = guarded([&] {
+    check_plan(plan);
+    check_dtype(dtype);
+    if (!devices || ndev < 1) throw std::invalid_argument("pftg: multi-device call needs ndev >= 1 devices");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      throw cuda_error("pftg: no CUDA device available (this library has no CPU fallback)");
+    }
+    for (int i = 0; i < ndev; ++i)
+      if (devices[i] < 0 || devices[i] >= n) throw std::out_of_range("pftg: device index out of range");
+  });
+  if (rc0 != PFTG_OK) return rc0;
+  std::vector<int> rc(ndev, PFTG_OK);
+  std::vector<std::string> msg(ndev);
+  std::vector<std::thread> th;
+  const std::size_t base = batch / ndev, rem = batch % ndev;
+  for (int i = 0; i < ndev; ++i) {
+    const std::size_t b0 = i * base + std::min<std::size_t>(i, rem), m = base + ((std::size_t)i < rem ? 1 : 0);
+    th.emplace_back([&, i, b0, m] {
+      if (m == 0) return;
+      if (cudaSetDevice(devices[i]) != cudaSuccess) {
+        rc[i] = PFTG_ECUDA;
+        msg[i] = "pftg: cudaSetDevice failed";
+        return;
+      }
+      rc[i] = call(b0, m);
+      if (rc[i] != PFTG_OK) msg[i] = pftg_last_error();  // thread-local message of the worker
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int i = 0; i < ndev; ++i)
+    if (rc[i] != PFTG_OK) {
+      set_error(msg[i]);
+      return rc[i];
+    }
+  return PFTG_OK;
+}
+}  // namespace
+}  // extern "C++"
+
+int pftg_apply_2d_host_multi(const pftg_plan* plan, int dtype, const void* z, void* band, size_t batch,
+                             const int* devices, int ndev) {
+  if (!plan) return pftg_apply_2d_host(plan, dtype, z, band, batch);  // reports the error
+  const std::size_t es = dtype == PFTG_C64 ? 8 : 16;
+  const std::size_t nz = plan->a1.n * plan->a2.n * es, nb = 4 * plan->a1.mt * plan->a2.mt * es;
+  return run_multi(plan, dtype, batch, devices, ndev, [&](std::size_t b0, std::size_t m) {
+    return apply_2d_host_impl(plan, dtype, static_cast<const char*>(z) + b0 * nz, static_cast<char*>(band) + b0 * nb, m,
+                              batch);
+  });
+}
+
+int pftg_adjoint_2d_host_multi(const pftg_plan* plan, int dtype, const void* band, void* z, size_t batch,
+                               const int* devices, int ndev) {
+  if (!plan) return pftg_adjoint_2d_host(plan, dtype, band, z, batch);
+  const std::size_t es = dtype == PFTG_C64 ? 8 : 16;
+  const std::size_t nz = plan->a1.n * plan->a2.n * es, nb = 4 * plan->a1.mt * plan->a2.mt * es;
+  return run_multi(plan, dtype, batch, devices, ndev, [&](std::size_t b0, std::size_t m) {
+    return adjoint_2d_host_impl(plan, dtype, static_cast<const char*>(band) + b0 * nb, static_cast<char*>(z) + b0 * nz,
+                                m, batch);
+  });
+}
+
+int pftg_fwd_adj_2d_host_multi(const pftg_plan* plan, int dtype, const void* z, void* band, void* back,
+                               size_t batch, const int* devices, int ndev) {
+  if (!plan) return pftg_fwd_adj_2d_host(plan, dtype, z, band, back, batch);
+  const std::size_t es = dtype == PFTG_C64 ? 8 : 16;
+  const std::size_t nz = plan->a1.n * plan->a2.n * es, nb = 4 * plan->a1.mt * plan->a2.mt * es;
+  return run_multi(plan, dtype, batch, devices, ndev, [&](std::size_t b0, std::size_t m) {
+    return fwd_adj_2d_host_impl(plan, dtype, static_cast<const char*>(z) + b0 * nz, static_cast<char*>(band) + b0 * nb,
+                                static_cast<char*>(back) + b0 * nz, m, batch);
   });
 }
 

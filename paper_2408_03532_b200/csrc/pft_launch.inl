@@ -559,14 +559,14 @@ void launch_adj_cols<R_>(const PftDev<R_>& pd, const typename CT<R_>::C* band, t
 
 #if PFTG_PART_ADJ
 // complex64 q = 8, r = 9 plans: one warp per output row, A-dagger on the band
-// side, epilogue and fused forward in registers (eval_band.cu). Single fields
-// (ePIE positions) and small batches; larger batches keep the streaming kernels.
+// side, epilogue and fused forward in registers (eval_band.cu), for every batch size
+// (the choice must not depend on how a host-buffer call or a multi-device call chunks the batch).
 inline bool try_eb_adj_rows(const PftDev<double>&, int, const double2*, const EpiArgs&, int, cudaStream_t) {
   return false;
 }
 inline bool try_eb_adj_rows(const PftDev<float>& pd, int epi, const float2* Gt, const EpiArgs& ep, int batch,
                             cudaStream_t st) {
-  if (!eval_band_adj_rows_ok(pd) || (knobs().eval_band_old & 8) || batch > 8) return false;
+  if (!eval_band_adj_rows_ok(pd) || (knobs().eval_band_old & 8)) return false;  // any batch: results must not depend on chunking
   if ((reinterpret_cast<uintptr_t>(Gt) & 15) || (reinterpret_cast<uintptr_t>(ep.G2) & 15)) return false;
   launch_eval_band_adj_rows(pd, epi, Gt, ep, batch, st);
   return true;

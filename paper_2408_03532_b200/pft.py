@@ -265,11 +265,14 @@ def pft_apply_1d(plan: PftPlan1D, z):
     return out
 
 
-def pft_fwd_adj_2d(plan: "PftPlan2D", z):
+def pft_fwd_adj_2d(plan: "PftPlan2D", z, devices=None):
     """BASELINE configs[1] in one call: (band, back) = (pft_apply_2d(z),
     pft_adjoint_2d(band)). Host numpy input: one streamed C-ABI call
     (pftg_fwd_adj_2d_host, H2D and D2H overlapped); CUDA tensors: the two
-    device calls. Bit-identical to calling the two operators in turn."""
+    device calls. Bit-identical to calling the two operators in turn.
+    devices (host input only): list of CUDA device indices; the batch is split in
+    contiguous blocks over them inside the library (pftg_fwd_adj_2d_host_multi,
+    one host thread per device, no collective)."""
     if isinstance(z, np.ndarray):
         if tuple(z.shape[-2:]) != plan.field_shape:
             raise ValueError("pft_apply_2d: z shape must match the plan")
@@ -277,6 +280,11 @@ def pft_fwd_adj_2d(plan: "PftPlan2D", z):
         b = _batch(z, plan.field_shape)
         band = np.empty(z.shape[:-2] + plan.band_shape, z.dtype)
         back = np.empty(z.shape, z.dtype)
+        if devices is not None:
+            dv = (C.c_int * len(devices))(*[int(d) for d in devices])
+            check(lib().pftg_fwd_adj_2d_host_multi(plan._h, _dtype_code(z), z.ctypes.data, band.ctypes.data,
+                                                   back.ctypes.data, b, dv, len(devices)))
+            return band, back
         check(lib().pftg_fwd_adj_2d_host(plan._h, _dtype_code(z), z.ctypes.data, band.ctypes.data,
                                          back.ctypes.data, b))
         return band, back

@@ -96,6 +96,9 @@ def test_compute_fails_loudly_without_gpu():
         P.pft_apply_2d(pl, np.zeros((64, 64), np.complex128))
     lib = _lib.lib()
     assert lib.pftg_device_ok() == 0
+    # the multi-device host entry fails the same way (before any thread is started)
+    with pytest.raises(P.CudaError, match="no CPU fallback"):
+        P.pft_fwd_adj_2d(pl, np.zeros((2, 64, 64), np.complex128), devices=[0, 1])
 
 
 def test_solver_config_defaults_mirror_reference():

@@ -317,6 +317,37 @@ def test_e1_shard_union_bit_identical():
         assert torch.equal(torch.cat(backs), back), ws
 
 
+def test_multi_device_host_entry_points_bit_identical(ref):
+    """pftg_{apply,adjoint,fwd_adj}_2d_host_multi (the E1 split for a C / C++ host that
+    drives several GPUs from one process): contiguous blocks of the batch on one host
+    thread per listed device. With device 0 listed three times (7 fields -> blocks of
+    3, 2, 2 run concurrently on three threads) the union is bit-identical to the
+    single-device call; more devices than fields leaves blocks empty."""
+    import ctypes as C
+    from paper_2408_03532_b200 import _lib
+    g, _ = _plans(ref, DATA / "scope_table_v1.txt", 256, 256, 32, 32, 32, 32, 1e-3)
+    rng = np.random.default_rng(25)
+    z = cnormal(rng, (7, 256, 256), np.complex64)
+    band1, back1 = P.pft_fwd_adj_2d(g, z)
+    for devs in ([0, 0, 0], [0], [0] * 9):
+        band, back = P.pft_fwd_adj_2d(g, z, devices=devs)
+        assert np.array_equal(band, band1) and np.array_equal(back, back1), devs
+    lib = _lib.lib()
+    dv = (C.c_int * 2)(0, 0)
+    band = np.empty_like(band1)
+    _lib.check(lib.pftg_apply_2d_host_multi(g._h, _lib.PFTG_C64, z.ctypes.data, band.ctypes.data, 7, dv, 2))
+    assert np.array_equal(band, band1)
+    back = np.empty_like(back1)
+    _lib.check(lib.pftg_adjoint_2d_host_multi(g._h, _lib.PFTG_C64, band.ctypes.data, back.ctypes.data, 7, dv, 2))
+    assert np.array_equal(back, back1)
+    # errors: device index out of range -> out_of_range (IndexError), ndev < 1 -> invalid_argument
+    bad = (C.c_int * 1)(4096)
+    with pytest.raises(IndexError):
+        _lib.check(lib.pftg_apply_2d_host_multi(g._h, _lib.PFTG_C64, z.ctypes.data, band.ctypes.data, 7, bad, 1))
+    with pytest.raises(ValueError):
+        _lib.check(lib.pftg_apply_2d_host_multi(g._h, _lib.PFTG_C64, z.ctypes.data, band.ctypes.data, 7, dv, 0))
+
+
 # ---- 1-D PFT (pft.hpp:33-38; SURVEY §8(f) F4) ----
 CASES_1D = [(1024, 64, 64, 1e-7), (4096, 128, 128, 1e-3), (1000, 40, 40, 1e-3), (960, 30, 30, 1e-7),
             (65536, 64, 64, 1e-3), (4096, 16, 128, 1e-3), (64, 4, 8, 1e-3)]
