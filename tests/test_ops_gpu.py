@@ -486,3 +486,26 @@ def test_band_stage_axis_reordered_kernels(tmp_path):
             assert err <= 2e-5, (k, err)
         else:
             assert np.array_equal(a, b), k
+
+
+def test_pdl_chained_positions_bit_identical(tmp_path):
+    """The kernels of an ePIE position are chained by programmatic dependent launch
+    (each waits, then releases its successor, whose table loads and operand prefetch
+    run ahead of its own wait). Hazard check: frames and probes after two sweeps are
+    bit-identical with plain serialized launches (PFTG_EB_NO_PDL / PFTG_FFT_NO_PDL),
+    for the full-FFT stage (256^2 blind / non-blind, 512^2) and the band stage
+    (p = 32 and p = 64 plans)."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    script = tmp_path / "pdl.py"
+    script.write_text(_PERSIST_SCRIPT)
+    res = {}
+    for tag, extra in (("pdl", {}), ("plain", {"PFTG_EB_NO_PDL": "1", "PFTG_FFT_NO_PDL": "1"})):
+        env = {**os.environ, **extra}
+        out = tmp_path / f"{tag}.npz"
+        subprocess.run([sys.executable, str(script), str(ROOT), str(out)], env=env, check=True, timeout=600)
+        res[tag] = np.load(out)
+    for k in res["pdl"].files:
+        assert np.array_equal(res["pdl"][k], res["plain"][k]), k
