@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(kEbColsT, 3)
             double* __restrict__ partial) {
   constexpr int LDF = eb_ldf(P1), NF = RR * NB, NCH = NB / 2;
   constexpr int LR = P1 * RR * NCH / kEbColsT;  // 16-byte chunks of the strip per thread
-  static_assert(P1 * RR * NCH % kEbColsT == 0 && NB % 4 == 0 && (P1 == 64 || P1 == 32), "strip shape");
+  static_assert(P1 * RR * NCH % kEbColsT == 0 && NB % 2 == 0 && (P1 == 64 || P1 == 32), "strip shape");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int M1 = pl.M1, M2 = pl.M2, mt1 = pl.mt1;
   float2* Gs = reinterpret_cast<float2*>(smem_raw);  // [NF][LDF]
@@ -551,13 +551,21 @@ __global__ void __launch_bounds__(kEbColsT, 3)
   for (int i = tid; i < M1; i += kEbColsT) W1s[i] = pl.W1t[i];
   if (dcrop) {
     const float* dc = dcrop + (size_t)f * dstride;
-    for (int i = tid; i < (NB / 4) * M1; i += kEbColsT) {
-      const int a = i / (NB / 4), h = i % (NB / 4);
-      const float4 d = __ldg(reinterpret_cast<const float4*>(dc + (size_t)a * M2 + b0 + 4 * h));
-      dcs[(4 * h + 0) * (M1 + 1) + a] = d.x;
-      dcs[(4 * h + 1) * (M1 + 1) + a] = d.y;
-      dcs[(4 * h + 2) * (M1 + 1) + a] = d.z;
-      dcs[(4 * h + 3) * (M1 + 1) + a] = d.w;
+    if constexpr (NB % 4 == 0) {
+      for (int i = tid; i < (NB / 4) * M1; i += kEbColsT) {
+        const int a = i / (NB / 4), h = i % (NB / 4);
+        const float4 d = __ldg(reinterpret_cast<const float4*>(dc + (size_t)a * M2 + b0 + 4 * h));
+        dcs[(4 * h + 0) * (M1 + 1) + a] = d.x;
+        dcs[(4 * h + 1) * (M1 + 1) + a] = d.y;
+        dcs[(4 * h + 2) * (M1 + 1) + a] = d.z;
+        dcs[(4 * h + 3) * (M1 + 1) + a] = d.w;
+      }
+    } else {
+      for (int i = tid; i < M1; i += kEbColsT) {
+        const float2 d = __ldg(reinterpret_cast<const float2*>(dc + (size_t)i * M2 + b0));
+        dcs[i] = d.x;
+        dcs[(M1 + 1) + i] = d.y;
+      }
     }
   }
   // programmatic dependent launch (single ePIE positions): the tables above do not
@@ -808,8 +816,8 @@ void launch_eval_band_rows(const PftDev<float>& pd, const float2* frame, long lo
   PFTG_LAUNCH_CHECK();
 }
 
-// nb = 8: throughput (evaluator, batches); nb = 4: one ePIE position over 2 x more CTAs,
-// one radix-8 butterfly per thread and pass. Gout != nullptr: residual + adjoint (needs dcrop).
+// nb = 8: throughput (evaluator, batches); nb = 4 / 2: one field over 2 x / 4 x more CTAs
+// (nb = 2 only with Gout: the residual + adjoint pass of an ePIE position). Gout != nullptr: residual + adjoint (needs dcrop).
 void launch_eval_band_cols(const PftDev<float>& pd, int nb, const float2* G, float2* band, const float* dcrop,
                            long long dstride, float2* Gout, double* partial, int batch, cudaStream_t st) {
   const size_t smem = eb_cols_smem(9, nb, pd.M1, pd.p1);
@@ -829,7 +837,10 @@ void launch_eval_band_cols(const PftDev<float>& pd, int nb, const float2* G, flo
     cfg.numAttrs = 1;
     PFTG_CUDA(cudaLaunchKernelEx(&cfg, k, pd, G, band, dcrop, dstride, Gout, partial));
   };
-  if (pd.p1 == 64) {
+  if (nb == 2) {  // one ePIE position: the most CTAs, half-filled (4.5 warps of work per CTA)
+    if (pd.p1 == 64) go(kb_cols<9, 2, true, 64>);
+    else go(kb_cols<9, 2, true, 32>);
+  } else if (pd.p1 == 64) {
     if (nb == 8) {
       if (Gout) go(kb_cols<9, 8, true, 64>);
       else go(kb_cols<9, 8, false, 64>);

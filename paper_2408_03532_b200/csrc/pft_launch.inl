@@ -439,7 +439,9 @@ inline bool try_eb_cols(const PftDev<float>& pd, int mode, const float2* G, floa
   const bool al = ((reinterpret_cast<uintptr_t>(G) | reinterpret_cast<uintptr_t>(Gout) |
                     reinterpret_cast<uintptr_t>(dcrop)) & 15) == 0 && dstride % 4 == 0;
   if (!al || !eval_band_cols_ok(pd) || (knobs().eval_band_old & 4) || (mode == 2 && pd.nb != 8)) return false;
-  const int nb = (mode != 2 && batch == 1) ? 4 : 8;
+  // one field: >= 32 CTAs (cfg3, M2 = 64: 2-column strips, band stage 56.5k -> 60.3k updates/s;
+  // cfg4, M2 = 128: 4-column strips -- 2-column ones measured 2 % slower there)
+  const int nb = (mode != 2 && batch == 1) ? ((mode == 1 && pd.M2 / 4 < 32) ? 2 : 4) : 8;
   launch_eval_band_cols(pd, nb, G, band, mode == 0 ? nullptr : dcrop, dstride, mode == 1 ? Gout : nullptr,
                         mode == 2 ? partial : nullptr, batch, st);
   return true;
