@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(128) ke_rows256_epie(const float2* __restrict_
   __shared__ float2 tws[128];
   __shared__ __align__(16) float2 sbuf[4][kE256Buf];
   const int g = threadIdx.x >> 5, l = threadIdx.x & 31;
-  const int r = blockIdx.x * 4 + g;
+  const int r = blockIdx.x * (blockDim.x >> 5) + g;  // one row per warp: 4 (grid 64) or 2 (grid 128) rows per CTA
   float2* S = sbuf[g];
   auto wsync = []() { __syncwarp(); };
   float2* orow = frame + off + (long long)r * ld;

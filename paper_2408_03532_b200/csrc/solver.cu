@@ -336,6 +336,14 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
       return;
     }
     if (use_fft256(s)) {
+      // 64 CTAs of four rows / four columns each; PFTG_FFT256_GRID=128 (two each, 128 SMs per
+      // position) measured slower: FFT stage 74.5k -> 68.7k updates/s (16-byte row segments
+      // in the column pass)
+      static const int k256g = std::getenv("PFTG_FFT256_GRID") ? std::atoi(std::getenv("PFTG_FFT256_GRID")) : 64;
+      auto launch_cols256 = [&](cudaStream_t st_, float2* Xp, const float* dp_, const float2* twp) {
+        if (k256g == 128) launch_pdl_pos(ke_cols256_proj<2>, dim3(128), dim3(64), st_, Xp, dp_, twp);
+        else launch_pdl_pos(ke_cols256_proj<4>, dim3(64), dim3(128), st_, Xp, dp_, twp);
+      };
       const float2* tw = fft_twiddles<float>(256);
       float2* fr = reinterpret_cast<float2*>(frame);
       float2* pr = reinterpret_cast<float2*>(probe);
@@ -345,25 +353,25 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
       const float scale = 1.0f / static_cast<float>(n);
       if (!s.fwd_ready) {
         ProfScope prof(st, K_FFT_ROWS);
-        launch_pdl_pos(ke_rows256_epie<E512_FWD>, dim3(64), dim3(128), st, tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, 1.f, 0.f, 0,
+        launch_pdl_pos(ke_rows256_epie<E512_FWD>, dim3(k256g), dim3(8192 / k256g), st, tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, 1.f, 0.f, 0,
                                                         0);
       }
       {
         ProfScope prof(st, K_FFT_COLS);
-        launch_pdl_pos(ke_cols256_proj<4>, dim3(64), dim3(128), st, X, dn, tw);
+        launch_cols256( st, X, dn, tw);
       }
       {
         ProfScope prof(st, K_FFT_ROWS);
-        launch_pdl_pos(ke_rows256_epie<E512_OBJ>, dim3(64), dim3(128), st, tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
+        launch_pdl_pos(ke_rows256_epie<E512_OBJ>, dim3(k256g), dim3(8192 / k256g), st, tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
                                                       (float)s.cfg.beta, blind ? 1 : 0, 0);
       }
       if (blind) {
         {
           ProfScope prof(st, K_FFT_COLS);
-          launch_pdl_pos(ke_cols256_proj<4>, dim3(64), dim3(128), st, X2, dn, tw);
+          launch_cols256( st, X2, dn, tw);
         }
         ProfScope prof(st, K_FFT_ROWS);
-        launch_pdl_pos(ke_rows256_epie<E512_PROBE>, dim3(64), dim3(128), st, tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
+        launch_pdl_pos(ke_rows256_epie<E512_PROBE>, dim3(k256g), dim3(8192 / k256g), st, tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
                                                         (float)s.cfg.gamma, jn >= 0 ? 1 : 0,
                                                         jn >= 0 ? s.offs[jn] : 0);
       }
