@@ -542,6 +542,15 @@ void enqueue_tv(pftg_solver& s, bool band) {
   }
 }
 
+// out[j] = sum_k part[j * nstrips + k], k ascending (deterministic)
+__global__ void k_sum_strips_pos(const double* __restrict__ part, int nstrips, int count, double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= count) return;
+  double s = 0.0;
+  for (int k = 0; k < nstrips; ++k) s += part[(size_t)j * nstrips + k];
+  out[j] = s;
+}
+
 template <class R>
 double objective(pftg_solver& s) {
   // (1/N) sum_j (1/n) sum_k (|X_jk| - d_jk)^2  (Parseval form of solver.cpp:89-102)
@@ -575,15 +584,16 @@ double objective(pftg_solver& s) {
     launch_fft_cols<R>(COL_EVAL, n1, n2, static_cast<Cx<R>*>(s.Xe), n, static_cast<const R*>(s.dperm) + c0 * n, n,
                        nullptr, 0, -1, s.part + c0 * strips, nb, s.st);
   }
-  std::vector<double> h(s.npos * strips);
-  PFTG_CUDA(cudaMemcpyAsync(h.data(), s.part, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s.st));
+  // per-position sums of the strip partials on the device (same strip order as the host
+  // loop they replace): npos doubles cross PCIe per sweep instead of npos x strips
+  Scratch psum(sizeof(double) * s.npos, s.st);
+  k_sum_strips_pos<<<(unsigned)((s.npos + 127) / 128), 128, 0, s.st>>>(s.part, strips, (int)s.npos, psum.as<double>());
+  PFTG_LAUNCH_CHECK();
+  std::vector<double> h(s.npos);
+  PFTG_CUDA(cudaMemcpyAsync(h.data(), psum.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s.st));
   PFTG_CUDA(cudaStreamSynchronize(s.st));
   double acc = 0.0;
-  for (std::size_t j = 0; j < s.npos; ++j) {
-    double sj = 0.0;
-    for (int k = 0; k < strips; ++k) sj += h[j * strips + k];
-    acc += sj / static_cast<double>(n);
-  }
+  for (std::size_t j = 0; j < s.npos; ++j) acc += h[j] / static_cast<double>(n);
   return acc / static_cast<double>(s.npos);
 }
 
