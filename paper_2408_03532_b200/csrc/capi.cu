@@ -800,7 +800,7 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
     double* bp = bpart->as<double>() + c0 * bstrips;
     if constexpr (sizeof(R) == 4) {
       if (eb_rows)
-        launch_eval_band_rows(*pd, static_cast<const float2*>(frame), (long long)fc, o,
+        launch_eval_band_rows(*pd, static_cast<const float2*>(frame), (long long)fc, 0, o,
                               static_cast<const float2*>(probe), G->as<float2>(), nb, sb);
     }
     if (!eb_rows) launch_fwd_rows<R>(*pd, s2, G->as<Cx<R>>(), nb, sb);

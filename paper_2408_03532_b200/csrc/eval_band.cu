@@ -143,7 +143,7 @@ __device__ __forceinline__ void eb_store8(float2* p, bool vec, const float2 (&v)
 // grid (p1, batch), 256 threads: warp w <-> row k1 * 8 + w of the window.
 template <int RR, int P2>
 __global__ void __launch_bounds__(256, 3)
-    kb_rows(PftDev<float> pl, EbPar<RR> bp, const float2* __restrict__ frame, long long ld,
+    kb_rows(PftDev<float> pl, EbPar<RR> bp, const float2* __restrict__ frame, long long ld, long long bstride,
             const long long* __restrict__ offs, const float2* __restrict__ probe, float2* __restrict__ G) {
   constexpr int S = P2 / 32;  // k2 slots per lane
   constexpr int N2 = P2 * 8;  // row length
@@ -157,20 +157,26 @@ __global__ void __launch_bounds__(256, 3)
   const int M2 = pl.M2, mt2 = pl.mt2;
   float2* st = stage + warp * N2;
   {
-    // exit wave row, coalesced: element c = 32 m + lane
-    const float2* zrow = frame + offs[f] + (long long)(k1 * 8 + warp) * ld;
-    const float2* prow = probe + (size_t)(k1 * 8 + warp) * N2;
-    float2 v[N2 / 32], pv[N2 / 32];
+    // field row (scan window: frame + offs[f]; batched fields: frame + f * bstride), times the
+    // probe row when there is one (exit wave), coalesced: element c = 32 m + lane
+    const float2* zrow = frame + (offs ? offs[f] : (long long)f * bstride) + (long long)(k1 * 8 + warp) * ld;
+    float2 v[N2 / 32];
 #pragma unroll
     for (int m = 0; m < N2 / 32; ++m) v[m] = __ldg(zrow + 32 * m + lane);
+    if (probe) {
+      const float2* prow = probe + (size_t)(k1 * 8 + warp) * N2;
+      float2 pv[N2 / 32];
 #pragma unroll
-    for (int m = 0; m < N2 / 32; ++m) pv[m] = __ldg(prow + 32 * m + lane);
+      for (int m = 0; m < N2 / 32; ++m) pv[m] = __ldg(prow + 32 * m + lane);
+#pragma unroll
+      for (int m = 0; m < N2 / 32; ++m) v[m] = cmul(pv[m], v[m]);
+    }
     for (int i = threadIdx.x; i < M2; i += blockDim.x) W2s[i] = pl.W2t[i];
     for (int i = threadIdx.x; i < P2 / 2; i += blockDim.x) tw2s[i] = pl.tw2[i];
 #pragma unroll
     for (int m = 0; m < N2 / 32; ++m) {
       const int c = 32 * m + lane, g = c >> 3, e = c & 7;
-      st[eb_chunk(g, e >> 1) * 2 + (e & 1)] = cmul(pv[m], v[m]);
+      st[eb_chunk(g, e >> 1) * 2 + (e & 1)] = v[m];
     }
   }
   __syncthreads();
@@ -799,19 +805,19 @@ bool eval_band_cols_ok(const PftDev<float>& pd) {
          eb_cols_smem(9, 8, pd.M1, pd.p1) <= 200 * 1024;
 }
 
-void launch_eval_band_rows(const PftDev<float>& pd, const float2* frame, long long ld, const long long* offs,
-                           const float2* probe, float2* G, int batch, cudaStream_t st) {
+void launch_eval_band_rows(const PftDev<float>& pd, const float2* frame, long long ld, long long bstride,
+                           const long long* offs, const float2* probe, float2* G, int batch, cudaStream_t st) {
   const auto bp = make_ebpar<9>(pd);
   const size_t smem = (size_t)(8 * pd.n2 + pd.M2 + pd.p2 / 2) * sizeof(float2);
   ProfScope prof(st, K_FWD_ROWS);
   if (pd.p2 == 64) {
     auto k = kb_rows<9, 64>;
     eb_allow_smem(k, smem);
-    k<<<dim3(pd.p1, batch), 256, smem, st>>>(pd, bp, frame, ld, offs, probe, G);
+    k<<<dim3(pd.p1, batch), 256, smem, st>>>(pd, bp, frame, ld, bstride, offs, probe, G);
   } else {
     auto k = kb_rows<9, 32>;
     eb_allow_smem(k, smem);
-    k<<<dim3(pd.p1, batch), 256, smem, st>>>(pd, bp, frame, ld, offs, probe, G);
+    k<<<dim3(pd.p1, batch), 256, smem, st>>>(pd, bp, frame, ld, bstride, offs, probe, G);
   }
   PFTG_LAUNCH_CHECK();
 }

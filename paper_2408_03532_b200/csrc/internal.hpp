@@ -42,7 +42,7 @@ struct Knobs {
   int eval_chunk;         // evaluator positions per chunk (0 = 64 MB of spectra)
   int eval_pchunk;        // evaluator positions per band-chain chunk (0 = 2 x eval chunk)
   bool eval_one_stream;   // evaluator: FFT and PFT chains on one stream
-  int eval_band_old;      // eval_band.cu off: bit 0 = evaluator rows, bit 1 = evaluator cols, bit 2 = launch_fwd_cols, bit 3 = launch_adj_rows (ePIE band stage, pft_apply_2d / pft_adjoint_2d)
+  int eval_band_old;      // eval_band.cu off: bit 0 = forward rows (evaluator, launch_fwd_rows), bit 1 = evaluator cols, bit 2 = launch_fwd_cols, bit 3 = launch_adj_rows (ePIE band stage, pft_apply_2d / pft_adjoint_2d)
   bool no_tile, force_tile;  // small-batch tile path (pft_tile.cu): off / forced
   int host_chunk_mb;         // host-buffer pipelines: MB per copy (0 = 32)
   bool no_persist;           // ePIE full-FFT stage: per-position kernel graph instead of the persistent sweep
@@ -125,8 +125,8 @@ void launch_adj_rows(const PftDev<R>& pd, int epi, const typename CT<R>::C* Gt, 
 // cols (strips of nb = 8 or 4 columns) -> band / residual partials [batch][M2 / nb] / residual + adjoint cols -> Gout.
 bool eval_band_rows_ok(const PftDev<float>& pd);
 bool eval_band_cols_ok(const PftDev<float>& pd);
-void launch_eval_band_rows(const PftDev<float>& pd, const float2* frame, long long ld, const long long* offs,
-                           const float2* probe, float2* G, int batch, cudaStream_t st);
+void launch_eval_band_rows(const PftDev<float>& pd, const float2* frame, long long ld, long long bstride,
+                           const long long* offs, const float2* probe, float2* G, int batch, cudaStream_t st);
 void launch_eval_band_cols(const PftDev<float>& pd, int nb, const float2* G, float2* band, const float* dcrop,
                            long long dstride, float2* Gout, double* partial, int batch, cudaStream_t st);
 

@@ -388,9 +388,19 @@ bool fast_adj_rows(const PftDev<R_>& pd, int epi, const typename CT<R_>::C* Gt, 
 }  // namespace
 
 #if PFTG_PART_FWD
+// complex64 q = 8, r = 9 plans: axis 2 first (kb_rows, eval_band.cu), for every batch size and
+// source kind (batched fields, scan windows, exit waves); G in the row-block layout.
+inline bool try_eb_fwd_rows(const PftDev<double>&, const Src<double>&, double2*, int, cudaStream_t) { return false; }
+inline bool try_eb_fwd_rows(const PftDev<float>& pd, const Src<float>& src, float2* G, int batch, cudaStream_t st) {
+  if (!eval_band_rows_ok(pd) || (knobs().eval_band_old & 1) || (reinterpret_cast<uintptr_t>(G) & 15)) return false;
+  launch_eval_band_rows(pd, src.base, src.ld, src.bstride, src.offs, src.probe, G, batch, st);
+  return true;
+}
+
 template <>
 bool launch_fwd_rows<R_>(const PftDev<R_>& pd, const Src<R_>& src, typename CT<R_>::C* G, int batch,
                          cudaStream_t st, bool want_strip) {
+  if (try_eb_fwd_rows(pd, src, G, batch, st)) return false;
   ProfScope prof(st, K_FWD_ROWS);
   // strip-major G only when the persistent cols kernel can consume it
   const bool strip = want_strip && fast_cols_ok(pd);
