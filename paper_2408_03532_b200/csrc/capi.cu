@@ -768,7 +768,8 @@ void evaluate_dev(const void* frame, std::size_t fr, std::size_t fc, const void*
         const float2* tw = fft_twiddles<float>(512);
         {
           ProfScope prof(st, K_FFT_ROWS);
-          ke_rows512<4><<<dim3(512 / (4 * 4), nb), 256, 0, st>>>(static_cast<const float2*>(frame), (long long)fc, o,
+          // rows per 64-thread group: 8 (4: 4.58 ms, 8 / 16: 4.56 ms, 2: 4.68, 32: 4.94 per 1600 positions)
+          ke_rows512<8><<<dim3(512 / (4 * 8), nb), 256, 0, st>>>(static_cast<const float2*>(frame), (long long)fc, o,
                                                                  static_cast<const float2*>(probe), tw,
                                                                  X.as<float2>());
           PFTG_LAUNCH_CHECK();
