@@ -300,6 +300,14 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
   if constexpr (sizeof(R) == 4) {
     if (use_fft512(s)) {
       // 512 x 512 complex64 windows (BASELINE configs[3]): radix-8 register FFTs, natural-order spectrum
+      // columns per CTA of the projection pass: 8 (64 CTAs x 512 threads, 64-byte row segments):
+      // FFT stage 47.1k -> 47.8k updates/s over 4; 2 (256 CTAs): 37.4k
+      static const int c512 = std::getenv("PFTG_FFT512_NCOL") ? std::atoi(std::getenv("PFTG_FFT512_NCOL")) : 8;
+      auto launch_cols512 = [&](cudaStream_t st_, float2* Xp, const float* dp_, const float2* twp) {
+        if (c512 == 2) launch_pdl_pos(ke_cols512_proj<2>, dim3(256), dim3(128), st_, Xp, dp_, twp);
+        else if (c512 == 8) launch_pdl_pos(ke_cols512_proj<8>, dim3(64), dim3(512), st_, Xp, dp_, twp);
+        else launch_pdl_pos(ke_cols512_proj<4>, dim3(128), dim3(256), st_, Xp, dp_, twp);
+      };
       const float2* tw = fft_twiddles<float>(512);
       float2* fr = reinterpret_cast<float2*>(frame);
       float2* pr = reinterpret_cast<float2*>(probe);
@@ -314,7 +322,7 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
       }
       {
         ProfScope prof(st, K_FFT_COLS);
-        launch_pdl_pos(ke_cols512_proj<4>, dim3(128), dim3(256), st, X, dn, tw);
+        launch_cols512(st, X, dn, tw);
       }
       {
         ProfScope prof(st, K_FFT_ROWS);
@@ -324,7 +332,7 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
       if (blind) {
         {
           ProfScope prof(st, K_FFT_COLS);
-          launch_pdl_pos(ke_cols512_proj<4>, dim3(128), dim3(256), st, X2, dn, tw);
+          launch_cols512(st, X2, dn, tw);
         }
         ProfScope prof(st, K_FFT_ROWS);
         launch_pdl_pos(ke_rows512_epie<E512_PROBE>, dim3(128), dim3(256), st, tw, fr, (long long)s.fc, s.offs[j], pr, X, X2, scale,
