@@ -349,7 +349,10 @@ void enqueue_position(pftg_solver& s, std::size_t j, bool band, long long jn) {
       // in the column pass)
       static const int k256g = std::getenv("PFTG_FFT256_GRID") ? std::atoi(std::getenv("PFTG_FFT256_GRID")) : 64;
       auto launch_cols256 = [&](cudaStream_t st_, float2* Xp, const float* dp_, const float2* twp) {
+        // 8 columns per CTA (32 CTAs) measured slower here: 73.6k -> 67.7k updates/s
+        static const int c256 = std::getenv("PFTG_FFT256_NCOL") ? std::atoi(std::getenv("PFTG_FFT256_NCOL")) : 4;
         if (k256g == 128) launch_pdl_pos(ke_cols256_proj<2>, dim3(128), dim3(64), st_, Xp, dp_, twp);
+        else if (c256 == 8) launch_pdl_pos(ke_cols256_proj<8>, dim3(32), dim3(256), st_, Xp, dp_, twp);
         else launch_pdl_pos(ke_cols256_proj<4>, dim3(64), dim3(128), st_, Xp, dp_, twp);
       };
       const float2* tw = fft_twiddles<float>(256);
