@@ -417,7 +417,7 @@ import paper_2408_03532_b200 as P
 rng = np.random.default_rng(31)
 out = {}
 for w, n, blind, band in ((256, 400, True, 0), (256, 400, False, 0), (512, 700, True, 0), (256, 400, True, 1),
-                         (512, 700, True, 1)):
+                         (512, 700, True, 1), (256, 400, False, 1)):
     obj = (rng.random((n, n)) * np.exp(1j * rng.random((n, n)))).astype(np.complex64)
     probe = np.exp(-((np.arange(w) - w / 2) ** 2)[:, None] / (w * w / 8.0)
                    - ((np.arange(w) - w / 2) ** 2)[None, :] / (w * w / 8.0)).astype(np.complex64)
