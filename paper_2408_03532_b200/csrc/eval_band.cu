@@ -669,7 +669,9 @@ __global__ void __launch_bounds__(kEbColsT, 3)
       if (band) band[((size_t)f * M1 + a) * M2 + b0 + bb] = y;
       if (dcrop) {
         const float d = dcs[bb * (M1 + 1) + a];
-        const float mag = hypotf(y.x, y.y);
+        // evaluator (no projection): |y| as sqrt(x^2 + y^2), as ke_cols512_eval; the band
+        // residual of the ePIE stage keeps hypotf (its quotient y / |y| follows)
+        const float mag = ADJ ? hypotf(y.x, y.y) : sqrtf(fmaf(y.x, y.x, y.y * y.y));
         if (partial) {
           const double e = (double)mag - (double)d;
           local += e * e;
